@@ -1,0 +1,333 @@
+/*
+ * ffx.h -- C ABI of the B200-native state-backup / failover-recovery path.
+ *
+ * This is the drop-in boundary for FFTrainer's per-iteration snapshot ->
+ * neighbour replica -> failure -> recover/verify path.  The reference exposes
+ * that path as a C++ API (proj/include/ftsim/{ckpt,storage,hash,evolution,
+ * domain}.hpp); it has no C ABI of its own.  Every entry point below names the
+ * reference interface it replaces (file:line, relative to the reference's
+ * proj/ directory).  The C++ facade in paper_2512_03644_b200/facade/ re-exposes
+ * the reference's exact class/function names on top of these calls, mapping
+ * status codes back to the reference's exception types 1:1.
+ *
+ * Conventions
+ *  - Plain pointers and sizes only; no torch or CUDA types in signatures.
+ *    `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
+ *  - "dev" pointers are device (or peer-mapped) global memory on the context's
+ *    device.  Region and replica pointers must be 16-byte aligned.
+ *  - Every call returns an ffx_status; ffx_last_error() gives the detail
+ *    message of the last failure on the calling thread.
+ *  - One ffx_ctx per rank (one process per GPU, or one thread per GPU).  Calls
+ *    on one context are not internally locked.
+ */
+#ifndef FFX_H_
+#define FFX_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FFX_ABI_VERSION 1
+#define FFX_MAX_REGIONS 16
+#define FFX_HANDLE_BYTES 256
+
+typedef enum ffx_status {
+  FFX_OK = 0,
+  FFX_ECONFIG = 1,  /* ckpt::ConfigError         ckpt.hpp:58-60 */
+  FFX_EVERSION = 2, /* ckpt::VersionError        ckpt.hpp:62-64 */
+  FFX_ERESTORE = 3, /* ckpt::RestoreError        ckpt.hpp:66-68 */
+  FFX_ECORRUPT = 4, /* store::CorruptSnapshot    storage.hpp:55-57 */
+  FFX_EINVAL = 5,   /* std::invalid_argument     storage.cpp:49, evolution.cpp:90 */
+  FFX_ERANGE = 6,   /* std::out_of_range         domain.cpp:22, :36 */
+  FFX_ECUDA = 7,    /* CUDA runtime / driver failure */
+  FFX_ENOMEM = 8,   /* device allocation failed */
+  FFX_ESTATE = 9    /* call out of order (e.g. snapshot with no target) */
+} ffx_status;
+
+const char* ffx_status_str(int status);
+const char* ffx_last_error(void);
+int ffx_abi_version(void);
+
+/* ---- domain (domain.hpp:15-110) ------------------------------------------ */
+
+typedef struct ffx_role {
+  uint16_t dp, pp, tp;
+} ffx_role;
+
+/* The sizing subset of ftsim::ClusterSpec (domain.hpp:49-73). */
+typedef struct ffx_cluster_spec {
+  uint32_t num_nodes;
+  uint32_t gpus_per_node;
+  uint32_t data_parallel;
+  uint32_t pipeline_parallel;
+  uint32_t tensor_parallel;
+  uint32_t distributed_optimizer; /* bool */
+  uint64_t params_per_device;
+} ffx_cluster_spec;
+
+/* ckpt::UniquenessPlan (ckpt.hpp:38-42) */
+typedef struct ffx_uniqueness_plan {
+  uint32_t weights_redundant;
+  uint32_t optimizer_redundant;
+  uint64_t unique_bytes_per_device;
+} ffx_uniqueness_plan;
+
+int ffx_role_of(const ffx_cluster_spec* spec, uint32_t global_index, ffx_role* out); /* domain.cpp:18-30 */
+int ffx_index_of(const ffx_cluster_spec* spec, ffx_role role, uint32_t* out);        /* domain.cpp:32-40 */
+int ffx_node_of(const ffx_cluster_spec* spec, ffx_role role, uint32_t* out);         /* domain.cpp:47-49 */
+int ffx_dp_neighbor(const ffx_cluster_spec* spec, ffx_role role, ffx_role* out);     /* domain.cpp:51-55 */
+int ffx_dp_predecessor(const ffx_cluster_spec* spec, ffx_role role, ffx_role* out);  /* domain.cpp:57-62 */
+
+/* ---- recovery planning (ctl::plan_recovery, controller.cpp:144-209) ------ */
+
+typedef struct ffx_forward { /* ForwardInstruction, controller.hpp:143-147 */
+  ffx_role origin;
+  uint16_t pad_;
+  uint32_t holder_node;
+  uint32_t dest_node;
+  uint32_t holder_dp; /* which replica holder serves it (dp+1 .. dp+replicas) */
+} ffx_forward;
+
+typedef struct ffx_redundant_source { /* RedundantSource, controller.hpp:151-154 */
+  ffx_role target;
+  ffx_role source;
+} ffx_redundant_source;
+
+/* RecoveryPlan (controller.hpp:156-169).  The caller provides the arrays,
+ * each with room for `capacity` entries (world size suffices). */
+typedef struct ffx_recovery_plan {
+  uint32_t kind; /* 0 Neighbor, 1 Fallback (RestoreKind) */
+  uint32_t capacity;
+  uint64_t resume_iteration;
+  uint32_t* failed_pods;
+  ffx_role* failed_roles;
+  ffx_role* lazy_backup_targets;
+  ffx_forward* forwards;
+  ffx_redundant_source* redundant_from;
+  uint32_t n_failed_pods, n_failed_roles, n_lazy, n_forwards, n_redundant;
+} ffx_recovery_plan;
+
+/* replicas = 1 is the reference rule (neighbour path iff no lost role's ring
+ * successor is lost).  replicas = 2 is the double-neighbour extension: a lost
+ * role is served by the first surviving holder among dp+1, dp+2. */
+int ffx_plan_recovery(const ffx_cluster_spec* spec, const uint32_t* failed_pods, uint32_t n_pods,
+                      const ffx_role* failed_roles, uint32_t n_roles, uint64_t global_consistent,
+                      uint64_t latest_fallback_round, uint32_t replicas, ffx_recovery_plan* out);
+
+/* ---- sizing: the state partitioner's rules ------------------------------- */
+
+int ffx_razor(const ffx_cluster_spec* spec, ffx_uniqueness_plan* out); /* ckpt.cpp:13-21 */
+uint64_t ffx_weights_bytes(const ffx_cluster_spec* spec);               /* evolution.cpp:11-13 */
+uint64_t ffx_optimizer_bytes(const ffx_cluster_spec* spec);             /* evolution.cpp:15-19 */
+/* *out = 0 current / 1 previous; FFX_EVERSION outside the window.  ckpt.cpp:27-33 */
+int ffx_version_for_target(uint64_t held_iteration, uint64_t target, int* out);
+
+/* ---- SNP1 framing (storage.hpp:12-25) ------------------------------------ */
+
+typedef struct ffx_blob_info { /* store::BlobInfo, storage.hpp:46-52 */
+  ffx_role role;
+  uint8_t kind; /* 0 weights, 1 optimizer */
+  uint8_t pad_[1];
+  uint32_t payload_len;
+  uint64_t iteration;
+  uint64_t checksum;
+} ffx_blob_info;
+
+/* Header bytes of store::pack_blob (storage.cpp:45-66); `checksum` is the
+ * whole-payload FNV-1a (ffx_checksum64).  FFX_EINVAL when len > 4 GiB-1. */
+int ffx_pack_header(ffx_role role, uint64_t iteration, uint8_t kind, uint64_t len,
+                    uint64_t checksum, uint8_t out[32]);
+/* store::parse_header (storage.cpp:74-90) plus the length check of
+ * unpack_blob (:95-96) when framed_len != 0.  FFX_ECORRUPT on failure. */
+int ffx_parse_header(const uint8_t* header, uint64_t framed_len, ffx_blob_info* out);
+
+/* ---- device primitives (hash.cpp, evolution.cpp) ------------------------ */
+
+/* checksum64 (hash.cpp:102-110) over a whole device buffer, bit-exact.
+ * Byte-serial FNV-1a is parallelised by low-byte-state speculation and an
+ * affine combine.  Blocks until *host_out is set. */
+int ffx_checksum64(const void* dev, uint64_t len, uint64_t* host_out, void* stream);
+/* dev_out[s] = checksum64(dev + s*slice_bytes, min(slice_bytes, len - s*slice_bytes)). */
+int ffx_slice_checksums(const void* dev, uint64_t len, uint64_t slice_bytes,
+                        uint64_t* dev_out, void* stream);
+/* Fused copy + per-slice checksum: dst <- src, dev_out as above. */
+int ffx_copy_checksums(void* dst, const void* src, uint64_t len, uint64_t slice_bytes,
+                       uint64_t* dev_out, void* stream);
+/* Fused copy + verify against dev_expected; dev_result[0] <- first bad slice
+ * (UINT64_MAX if none), dev_result[1] <- number of bad slices. */
+int ffx_copy_verify(void* dst, const void* src, uint64_t len, uint64_t slice_bytes,
+                    const uint64_t* dev_expected, uint64_t* dev_result, void* stream);
+/* evo::expand / evo::materialize (evolution.cpp:71-97) into device memory.
+ * materialize: FFX_EINVAL when bytes < 32. */
+int ffx_expand(void* dst, const uint8_t digest[32], uint64_t bytes, void* stream);
+int ffx_materialize(void* dst, const uint8_t digest[32], uint64_t bytes, void* stream);
+/* evo::blob_is_sound (evolution.cpp:106-110).  Blocks; *host_first_bad is the
+ * first byte that differs from materialize(prefix), UINT64_MAX if sound. */
+int ffx_blob_check(const void* dev, uint64_t bytes, uint64_t* host_first_bad, void* stream);
+
+/* ---- contexts and the state registry -------------------------------------- */
+
+typedef struct ffx_ctx ffx_ctx;
+typedef struct ffx_replica ffx_replica;
+
+enum ffx_region_kind {
+  FFX_REGION_MASTER = 0, /* fp32 master params shard */
+  FFX_REGION_ADAM_M = 1,
+  FFX_REGION_ADAM_V = 2,
+  FFX_REGION_PARAMS = 3, /* bf16 params (unique under ZeRO-3, else redundant) */
+  FFX_REGION_CURSOR = 4, /* data-loader cursor */
+  FFX_REGION_RNG = 5,    /* RNG state */
+  FFX_REGION_BLOB = 6    /* an opaque unique-state blob (the reference's model) */
+};
+
+/* slice_bytes: integrity/scheduling unit, a multiple of 256 (0 = default 4096). */
+int ffx_open(int device, const ffx_cluster_spec* spec, ffx_role self, uint64_t slice_bytes,
+             ffx_ctx** out);
+int ffx_close(ffx_ctx* ctx);
+
+/* Register a device region.  unique != 0: carried by every snapshot (the
+ * razor's per-iteration payload); unique == 0: redundant across the DP ring,
+ * re-read from a live peer on recovery.  Order of registration is the payload
+ * order.  FFX_ECONFIG when the registry is full, FFX_EINVAL on misalignment. */
+int ffx_register_region(ffx_ctx* ctx, int kind, void* dev, uint64_t bytes, int unique);
+int ffx_clear_regions(ffx_ctx* ctx);
+
+typedef struct ffx_plan_info {
+  ffx_uniqueness_plan razor;           /* the reference rule for ctx's spec */
+  uint64_t registered_unique_bytes;    /* what one snapshot moves */
+  uint64_t registered_redundant_bytes; /* what a recovery re-reads from a live peer */
+  uint64_t slice_bytes;
+  uint64_t num_slices; /* unique slices (checksum table entries) */
+  uint32_t num_regions;
+  uint32_t num_unique_regions;
+} ffx_plan_info;
+int ffx_plan(ffx_ctx* ctx, ffx_plan_info* out);
+
+/* ---- neighbour replica manager (NeighborBuffer, ckpt.hpp:105-120) --------- */
+
+/* Holder side: device slots for `origin`'s snapshots, `versions` of them
+ * (the reference keeps 2: ckpt.cpp:92), each with `capacity` payload bytes.
+ * capacity mirrors HostSnapshots(role, capacity) (ckpt.hpp:82-86). */
+int ffx_replica_create(ffx_ctx* ctx, ffx_role origin, uint64_t capacity, uint32_t versions,
+                       ffx_replica** out);
+/* Opaque FFX_HANDLE_BYTES blob (CUDA IPC handle + layout) for another rank. */
+int ffx_replica_export(const ffx_replica* r, uint8_t handle[FFX_HANDLE_BYTES]);
+/* Map a replica exported by another rank (or this process) into ctx. */
+int ffx_replica_open(ffx_ctx* ctx, const uint8_t handle[FFX_HANDLE_BYTES], ffx_replica** out);
+int ffx_replica_destroy(ffx_replica* r);
+
+typedef struct ffx_slot_info {
+  uint32_t state; /* 0 empty, 1 writing (torn if seen at rest), 2 committed */
+  uint32_t num_regions;
+  ffx_role role;
+  uint8_t kind;
+  uint8_t whole_checksum_valid;
+  uint64_t iteration;
+  uint64_t payload_len;
+  uint64_t slice_bytes;
+  uint64_t num_slices;
+  uint64_t whole_checksum;
+  uint64_t seq; /* write sequence number: larger is newer */
+} ffx_slot_info;
+int ffx_replica_slots(const ffx_replica* r, uint32_t* versions);
+int ffx_replica_slot_info(ffx_replica* r, uint32_t slot, ffx_slot_info* out);
+/* NeighborBuffer::newest() (ckpt.cpp:102-105): FFX_ERESTORE if nothing committed. */
+int ffx_replica_newest(ffx_replica* r, uint64_t* iteration);
+/* Device pointers into slot `slot` (payload, checksum table). */
+int ffx_replica_slot_ptrs(ffx_replica* r, uint32_t slot, void** payload, uint64_t** sums);
+/* NeighborBuffer::clear() (ckpt.hpp:117). */
+int ffx_replica_clear(ffx_replica* r);
+/* SNP1 frame export (framed_at(), ckpt.cpp:95-100 + pack_blob layout): copies
+ * header + payload (regions concatenated) to host memory; computes the
+ * whole-payload FNV on the device if not yet known.  *framed_len = 32 + len.
+ * FFX_ERESTORE when the iteration is not held, FFX_ECONFIG when cap is short,
+ * FFX_EINVAL when the payload exceeds the 4 GiB SNP1 limit (storage.cpp:48). */
+int ffx_replica_export_frame(ffx_replica* r, uint64_t iteration, void* host_dst, uint64_t cap,
+                             uint64_t* framed_len, void* stream);
+
+/* ---- snapshot (HostSnapshots::take + ring stream, ckpt.cpp:38-53) --------- */
+
+/* Where this rank's snapshots land: normally the replica its ring successor
+ * created for it and exported (opened with ffx_replica_open). */
+int ffx_snapshot_target(ffx_ctx* ctx, ffx_replica* target);
+
+typedef struct ffx_snapshot_opts {
+  uint32_t max_ctas;       /* SM budget for the snapshot kernel (0 = whole GPU) */
+  uint32_t batches;        /* slice batches the scheduler splits one snapshot into (0/1 = one) */
+  void* gate_events;       /* cudaEvent_t[batches] each batch waits on (NULL = none) */
+  uint32_t verify_on_store;/* holder-side re-verify after landing (ckpt.cpp:78 semantics) */
+  uint32_t weights_kind;   /* nonzero: frame as BlobKind::Weights (0), else Optimizer (1) */
+} ffx_snapshot_opts;
+
+/* Snapshot all unique regions into the target replica at `iteration`, async
+ * on `stream`.  Slot choice follows the two-version rule: replace the slot
+ * already holding `iteration`, else overwrite the older of the two
+ * (ckpt.cpp:46-52, :86-92).  FFX_ECONFIG when the registered unique bytes
+ * exceed the target capacity (ckpt.cpp:40-43). */
+int ffx_snapshot(ffx_ctx* ctx, uint64_t iteration, void* stream, const ffx_snapshot_opts* opts);
+
+/* Copy the checksum table written by this ctx's most recent snapshot into
+ * host memory (async on `stream`; pinned memory for true overlap).
+ * *n_out = entries copied (min(table, max_entries)). */
+int ffx_snapshot_read_sums(ffx_ctx* ctx, uint64_t* host_dst, uint64_t max_entries, uint64_t* n_out,
+                           void* stream);
+
+/* ---- recovery (assemble_restore, ckpt.cpp:111-167) ------------------------ */
+
+typedef struct ffx_recover_report {
+  uint64_t bytes;          /* payload bytes pulled and verified */
+  uint64_t first_bad_slice;/* UINT64_MAX when every slice verified */
+  uint64_t bad_slices;
+  uint32_t slot;           /* replica slot used */
+  uint32_t pad_;
+  double seconds;          /* device time of the gather/verify */
+} ffx_recover_report;
+
+/* Rebuild ctx's unique regions at `target` from a replica (the holder's
+ * NeighborBuffer for this role), pulling over NVLink/P2P with fused slice
+ * verification.  FFX_ERESTORE: slot missing / stale / torn / wrong role or
+ * kind / region layout mismatch / checksum mismatch (report says which slice).
+ * Blocks until verified. */
+int ffx_recover(ffx_ctx* ctx, ffx_replica* src, uint64_t target, void* stream,
+                ffx_recover_report* report);
+
+/* Pull one redundant region (weights from a live DP peer, ckpt.cpp:150-152)
+ * from a peer device pointer, verifying against the peer's slice table
+ * (computed by the peer with ffx_slice_checksums). */
+int ffx_recover_region(ffx_ctx* ctx, uint32_t region_index, const void* peer_src,
+                       const uint64_t* peer_sums, void* stream, ffx_recover_report* report);
+
+/* Map / unmap a raw device allocation exported by another process (for the
+ * redundant-region pull).  handle = cudaIpcMemHandle_t bytes (64). */
+int ffx_ipc_export(void* dev_base, uint8_t handle[64]);
+int ffx_ipc_open(const uint8_t handle[64], void** dev_base);
+int ffx_ipc_close(void* dev_base);
+
+/* ---- failure injection ---------------------------------- */
+
+enum ffx_fault {
+  FFX_FAULT_POISON_STATE = 0,   /* fill ctx's unique regions with a poison pattern */
+  FFX_FAULT_CORRUPT_REPLICA = 1,/* flip one payload byte (arg = slot<<48 | offset) */
+  FFX_FAULT_TEAR_SLOT = 2,      /* leave slot (arg) in the "writing" state */
+  FFX_FAULT_CORRUPT_SUMS = 3    /* flip one checksum-table entry (arg = slot<<48 | index) */
+};
+int ffx_inject(ffx_ctx* ctx, int fault, ffx_replica* r, uint64_t arg);
+
+typedef struct ffx_stats {
+  uint64_t snapshots;
+  uint64_t snapshot_bytes; /* backup_bytes in the reference's metrics (metrics.hpp:32-83) */
+  uint64_t recoveries;
+  uint64_t recovered_bytes;
+  uint64_t verify_failures;
+  uint64_t kernel_launches;
+} ffx_stats;
+int ffx_get_stats(ffx_ctx* ctx, ffx_stats* out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* FFX_H_ */

@@ -1,0 +1,212 @@
+"""Python handle on the CPU oracle (TEST INFRASTRUCTURE ONLY).
+
+Loads oracle/liboracle.so (the C restatement, ffx_oracle.c) and, when built,
+oracle/_ref/libftsim_ref.so (the reference itself).  Only tests/,
+__graft_entry__.smoke() and bench.py's cpu_baseline / reference legs may
+import this module; the product path never does.
+
+plan_recovery below is a small pure-Python restatement of
+proj/src/controller.cpp:144-209 used as the oracle for ffx_plan_recovery.
+"""
+import ctypes
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ORACLE_SO = os.path.join(HERE, "liboracle.so")
+REF_SO = os.path.join(HERE, "_ref", "libftsim_ref.so")
+
+_u64 = ctypes.c_uint64
+_P = ctypes.c_void_p
+
+
+def _load_oracle():
+    lib = ctypes.CDLL(ORACLE_SO)
+    sig = {
+        "orc_fnv1a64": (_u64, [_P, _u64]),
+        "orc_fnv1a64_from": (_u64, [_u64, _P, _u64]),
+        "orc_slice_fnv": (_u64, [_P, _u64, _u64, _P]),
+        "orc_fold64": (_u64, [_P]),
+        "orc_mix64": (_u64, [_u64]),
+        "orc_expand": (None, [_P, _u64, _P]),
+        "orc_materialize": (ctypes.c_int, [_P, _u64, _P]),
+        "orc_blob_is_sound": (ctypes.c_int, [_P, _u64]),
+        "orc_weights_bytes": (_u64, [_u64]),
+        "orc_optimizer_bytes": (_u64, [_u64, ctypes.c_uint32, ctypes.c_int]),
+        "orc_razor": (_u64, [_u64, ctypes.c_uint32, ctypes.c_int, ctypes.POINTER(ctypes.c_int)]),
+        "orc_version_for_target": (ctypes.c_int, [_u64, _u64]),
+        "orc_pack_header": (ctypes.c_int, [ctypes.c_uint16] * 3 + [_u64, ctypes.c_uint8, _u64, _u64, _P]),
+        "orc_pack_blob": (ctypes.c_int, [ctypes.c_uint16] * 3 + [_u64, ctypes.c_uint8, _P, _u64, _P]),
+        "orc_unpack": (ctypes.c_int, [_P, _u64, ctypes.POINTER(_u64)]),
+        "orc_sha256": (ctypes.c_int, [_P, _u64, _P]),
+        "orc_weights_init": (None, [_u64, ctypes.c_uint16, ctypes.c_uint16, _P]),
+        "orc_optimizer_init": (None, [_u64] + [ctypes.c_uint16] * 3 + [ctypes.c_int, _P]),
+        "orc_state_next": (None, [ctypes.c_char_p, _P, _P, _P]),
+        "orc_materialize_range": (ctypes.c_int, [_P, _u64, _u64, _u64, _P]),
+    }
+    for n, (r, a) in sig.items():
+        f = getattr(lib, n)
+        f.restype = r
+        f.argtypes = a
+    return lib
+
+
+lib = _load_oracle()
+
+
+def _buf(n):
+    return ctypes.create_string_buffer(max(n, 1))
+
+
+def fnv1a64(data: bytes) -> int:
+    return lib.orc_fnv1a64(data, len(data))
+
+
+def slice_fnv(data: bytes, slice_bytes: int):
+    n = (len(data) + slice_bytes - 1) // slice_bytes
+    out = (ctypes.c_uint64 * max(n, 1))()
+    lib.orc_slice_fnv(data, len(data), slice_bytes, out)
+    return [out[i] for i in range(n)]
+
+
+def expand(digest: bytes, n: int) -> bytes:
+    b = _buf(n)
+    lib.orc_expand(digest, n, b)
+    return b.raw[:n]
+
+
+def materialize(digest: bytes, n: int) -> bytes:
+    b = _buf(n)
+    if lib.orc_materialize(digest, n, b) != 0:
+        raise ValueError("state blob smaller than its digest prefix")
+    return b.raw[:n]
+
+
+def materialize_range(digest: bytes, total: int, lo: int, n: int) -> bytes:
+    b = _buf(n)
+    if lib.orc_materialize_range(digest, total, lo, n, b) != 0:
+        raise ValueError("range outside blob")
+    return b.raw[:n]
+
+
+def blob_is_sound(blob: bytes) -> bool:
+    return bool(lib.orc_blob_is_sound(blob, len(blob)))
+
+
+def optimizer_init(seed, dp, pp, tp, distributed=True) -> bytes:
+    b = _buf(32)
+    lib.orc_optimizer_init(seed, dp, pp, tp, int(distributed), b)
+    return b.raw[:32]
+
+
+def weights_init(seed, pp, tp) -> bytes:
+    b = _buf(32)
+    lib.orc_weights_init(seed, pp, tp, b)
+    return b.raw[:32]
+
+
+def optimizer_bytes(phi, d, distributed) -> int:
+    return lib.orc_optimizer_bytes(phi, d, int(distributed))
+
+
+def razor(phi, d, distributed):
+    fl = (ctypes.c_int * 2)()
+    u = lib.orc_razor(phi, d, int(distributed), fl)
+    return bool(fl[0]), bool(fl[1]), u
+
+
+def version_for_target(held, target):
+    return lib.orc_version_for_target(held, target)
+
+
+def pack_header(role, iteration, kind, length, checksum) -> bytes:
+    b = _buf(32)
+    if lib.orc_pack_header(role[0], role[1], role[2], iteration, kind, length, checksum, b) != 0:
+        raise ValueError("snapshot payload exceeds 4 GiB framing limit")
+    return b.raw[:32]
+
+
+def pack_blob(role, iteration, kind, payload: bytes) -> bytes:
+    b = _buf(32 + len(payload))
+    if lib.orc_pack_blob(role[0], role[1], role[2], iteration, kind, payload, len(payload), b) != 0:
+        raise ValueError("snapshot payload exceeds 4 GiB framing limit")
+    return b.raw[:32 + len(payload)]
+
+
+def unpack(frame: bytes):
+    f = (ctypes.c_uint64 * 7)()
+    rc = lib.orc_unpack(frame, len(frame), f)
+    return rc, tuple(f[i] for i in range(7))
+
+
+def sha256(data: bytes) -> bytes:
+    b = _buf(32)
+    lib.orc_sha256(data, len(data), b)
+    return b.raw[:32]
+
+
+def ref_lib():
+    """The reference library itself, or None when not built (GPU box w/o build)."""
+    if not os.path.exists(REF_SO):
+        return None
+    r = ctypes.CDLL(REF_SO)
+    r.ref_checksum64.restype = _u64
+    r.ref_checksum64.argtypes = [_P, _u64]
+    r.ref_materialize.restype = ctypes.c_int
+    r.ref_materialize.argtypes = [_P, _u64, _P]
+    r.ref_ring_setup.restype = _P
+    r.ref_ring_setup.argtypes = [ctypes.c_int, _u64]
+    r.ref_ring_run.restype = ctypes.c_int
+    r.ref_ring_run.argtypes = [_P, _u64, ctypes.POINTER(ctypes.c_double)]
+    r.ref_ring_free.argtypes = [_P]
+    r.ref_optimizer_init.argtypes = [_u64, ctypes.c_uint16, ctypes.c_uint16, ctypes.c_uint16, ctypes.c_int, _P]
+    return r
+
+
+# ---- controller.cpp:144-209, restated (small cases only) ---------------------
+
+def role_of(idx, d, p, t):
+    return (idx // (t * p), (idx // t) % p, idx % t)
+
+
+def index_of(role, p, t):
+    return (role[0] * p + role[1]) * t + role[2]
+
+
+def plan_recovery(d, p, t, gpus_per_node, distributed, failed_pods, failed_roles,
+                  global_consistent, latest_fallback, phi=1):
+    pods = sorted(set(failed_pods))
+    lost = set(tuple(r) for r in failed_roles)
+    for pod in pods:
+        for lr in range(gpus_per_node):
+            lost.add(role_of(pod * gpus_per_node + lr, d, p, t))
+    lost = sorted(lost)
+    nb = lambda r: ((r[0] + 1) % d, r[1], r[2])
+    neighbor_ok = d > 1 and not any(nb(f) in lost for f in lost)
+    wr, orr, unique = razor(phi, d, distributed)
+    plan = {"kind": "neighbor" if neighbor_ok else "fallback", "failed_pods": pods,
+            "failed_roles": lost, "forwards": [], "redundant_from": [], "lazy": []}
+    if not neighbor_ok:
+        plan["resume"] = latest_fallback
+        return plan
+    plan["resume"] = global_consistent
+    if global_consistent == 0:
+        return plan
+    node = lambda r: index_of(r, p, t) // gpus_per_node
+    for f in lost:
+        if unique > 0:
+            plan["forwards"].append((f, node(nb(f)), node(f)))
+        if wr or orr:
+            for dp in range(d):
+                c = (dp, f[1], f[2])
+                if c not in lost:
+                    plan["redundant_from"].append((f, c))
+                    break
+    if wr or orr:
+        for pp in range(p):
+            for tp in range(t):
+                for dp in range(d):
+                    c = (dp, pp, tp)
+                    if c not in lost:
+                        plan["lazy"].append(c)
+                        break
+    return plan

@@ -1,0 +1,189 @@
+// ref_shim.cpp -- extern "C" entry points onto the UNMODIFIED reference
+// library (proj/src/{hash,storage,ckpt,evolution,domain}.cpp), compiled by
+// oracle/Makefile into oracle/_ref/libftsim_ref.so.
+//
+// TEST INFRASTRUCTURE ONLY: used by oracle/gen_golden.py to produce the golden
+// fixtures, by tests/ to cross-check the C restatement, and by bench.py's
+// reference arm / cpu_baseline leg to time the reference's own CPU path.
+// Nothing here is linked into libffx.so.
+#include <chrono>
+#include <cstdint>
+#include <cstring>
+#include <stdexcept>
+#include <thread>
+#include <vector>
+
+#include "ftsim/ckpt.hpp"
+#include "ftsim/evolution.hpp"
+#include "ftsim/hash.hpp"
+#include "ftsim/storage.hpp"
+
+using namespace ftsim;
+
+extern "C" {
+
+std::uint64_t ref_checksum64(const void* p, std::uint64_t n) { return checksum64(p, n); }
+
+void ref_optimizer_init(std::uint64_t seed, std::uint16_t dp, std::uint16_t pp,
+                        std::uint16_t tp, int distributed, std::uint8_t* out) {
+  const auto d = evo::optimizer_init(seed, Role{dp, pp, tp}, distributed != 0);
+  std::memcpy(out, d.data(), 32);
+}
+
+void ref_weights_init(std::uint64_t seed, std::uint16_t pp, std::uint16_t tp, std::uint8_t* out) {
+  const auto d = evo::weights_init(seed, Role{0, pp, tp});
+  std::memcpy(out, d.data(), 32);
+}
+
+int ref_materialize(const std::uint8_t* digest, std::uint64_t bytes, std::uint8_t* out) {
+  Digest d;
+  std::memcpy(d.data(), digest, 32);
+  try {
+    const auto v = evo::materialize(d, bytes);
+    std::memcpy(out, v.data(), v.size());
+    return 0;
+  } catch (const std::invalid_argument&) {
+    return -1;
+  }
+}
+
+void ref_expand(const std::uint8_t* digest, std::uint64_t bytes, std::uint8_t* out) {
+  Digest d;
+  std::memcpy(d.data(), digest, 32);
+  const auto v = evo::expand(d, bytes);
+  if (!v.empty()) std::memcpy(out, v.data(), v.size());
+}
+
+int ref_blob_is_sound(const std::uint8_t* p, std::uint64_t n) {
+  return evo::blob_is_sound(std::vector<std::uint8_t>(p, p + n)) ? 1 : 0;
+}
+
+std::uint64_t ref_optimizer_bytes(std::uint64_t phi, std::uint32_t d, int distributed) {
+  ClusterSpec cs;
+  cs.params_per_device = phi;
+  cs.data_parallel = d;
+  cs.distributed_optimizer = distributed != 0;
+  return evo::optimizer_bytes(cs);
+}
+
+std::uint64_t ref_razor(std::uint64_t phi, std::uint32_t d, int distributed, int* flags) {
+  ClusterSpec cs;
+  cs.params_per_device = phi;
+  cs.data_parallel = d;
+  cs.distributed_optimizer = distributed != 0;
+  const auto p = ckpt::razor(cs);
+  flags[0] = p.weights_redundant;
+  flags[1] = p.optimizer_redundant;
+  return p.unique_bytes_per_device;
+}
+
+int ref_version_for_target(std::uint64_t held, std::uint64_t target) {
+  try {
+    return ckpt::version_for_target(held, target);
+  } catch (const ckpt::VersionError&) {
+    return -1;
+  }
+}
+
+// Frame into `out` (32 + len bytes).  -1 where pack_blob throws.
+int ref_pack_blob(std::uint16_t dp, std::uint16_t pp, std::uint16_t tp, std::uint64_t it,
+                  int kind, const void* payload, std::uint64_t len, std::uint8_t* out) {
+  try {
+    const auto f = store::pack_blob(Role{dp, pp, tp}, it, static_cast<store::BlobKind>(kind),
+                                    payload, len);
+    std::memcpy(out, f.data(), f.size());
+    return 0;
+  } catch (const std::invalid_argument&) {
+    return -1;
+  }
+}
+
+// 0 valid, 1 CorruptSnapshot.
+int ref_unpack_ok(const std::uint8_t* f, std::uint64_t n) {
+  try {
+    store::unpack_blob(std::vector<std::uint8_t>(f, f + n));
+    return 0;
+  } catch (const store::CorruptSnapshot&) {
+    return 1;
+  }
+}
+
+// The reference's per-iteration CPU hot path, timed.  One std::thread per
+// ring rank: HostSnapshots::take (pack + FNV) ->
+// NeighborBuffer::store at the holder (by-value copy + unpack + FNV verify)
+// -> assemble_restore of the unique piece (unpack + FNV).  Payloads are
+// evo::materialize(optimizer_init(42, role, true), bytes), built once by
+// ref_ring_setup outside any timed region.
+struct RefRing {
+  int threads;
+  std::uint64_t bytes;
+  std::vector<std::vector<std::uint8_t>> blobs;
+};
+
+void* ref_ring_setup(int threads, std::uint64_t bytes) {
+  auto* r = new RefRing{threads, bytes, std::vector<std::vector<std::uint8_t>>(threads)};
+  std::vector<std::thread> pool;
+  for (int t = 0; t < threads; ++t)
+    pool.emplace_back([r, t] {
+      r->blobs[t] = evo::materialize(
+          evo::optimizer_init(42, Role{static_cast<std::uint16_t>(t), 0, 0}, true), r->bytes);
+    });
+  for (auto& th : pool) th.join();
+  return r;
+}
+
+void ref_ring_free(void* h) { delete static_cast<RefRing*>(h); }
+
+// Per-stage seconds (max over threads) into secs[0..2] (take, store,
+// restore) and the wall time of the whole parallel iteration into secs[3].
+// Returns 0, or -1 if any stage threw or restored the wrong size.
+int ref_ring_run(void* h, std::uint64_t iteration, double* secs) {
+  auto* r = static_cast<RefRing*>(h);
+  const int threads = r->threads;
+  const std::uint64_t bytes = r->bytes;
+  std::vector<double> st(3 * threads, 0.0);
+  std::vector<int> ok(threads, 0);
+  std::vector<std::thread> pool;
+  using clk = std::chrono::steady_clock;
+  const auto w0 = clk::now();
+  for (int t = 0; t < threads; ++t)
+    pool.emplace_back([&, t] {
+      try {
+        const Role me{static_cast<std::uint16_t>(t), 0, 0};
+        ckpt::HostSnapshots hs(me, bytes);
+        ckpt::NeighborBuffer nb(me);  // the ring successor's buffer for `me`
+        auto t0 = clk::now();
+        hs.take(iteration, r->blobs[t].data(), r->blobs[t].size());
+        auto t1 = clk::now();
+        nb.store(*hs.framed(iteration));
+        auto t2 = clk::now();
+        ckpt::UniquenessPlan plan;
+        plan.weights_redundant = true;
+        plan.unique_bytes_per_device = bytes;
+        const auto w = store::pack_blob(me, iteration, store::BlobKind::Weights, nullptr, 0);
+        ckpt::RestorePieces pieces;
+        pieces.unique = nb.framed_at(iteration);
+        pieces.weights = &w;
+        auto t3 = clk::now();
+        const auto bundle = ckpt::assemble_restore(me, iteration, plan, pieces);
+        auto t4 = clk::now();
+        ok[t] = bundle.optimizer_current.blob.size() == bytes;
+        st[3 * t + 0] = std::chrono::duration<double>(t1 - t0).count();
+        st[3 * t + 1] = std::chrono::duration<double>(t2 - t1).count();
+        st[3 * t + 2] = std::chrono::duration<double>(t4 - t3).count();
+      } catch (...) {
+        ok[t] = 0;
+      }
+    });
+  for (auto& th : pool) th.join();
+  secs[3] = std::chrono::duration<double>(clk::now() - w0).count();
+  for (int k = 0; k < 3; ++k) {
+    secs[k] = 0;
+    for (int t = 0; t < threads; ++t) secs[k] = st[3 * t + k] > secs[k] ? st[3 * t + k] : secs[k];
+  }
+  for (int t = 0; t < threads; ++t)
+    if (!ok[t]) return -1;
+  return 0;
+}
+
+}  // extern "C"

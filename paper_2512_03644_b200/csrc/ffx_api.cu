@@ -1,0 +1,1238 @@
+// ffx_api.cu -- the C ABI (include/ffx.h): state registry / partitioner,
+// neighbour replica manager, snapshot issue + slice scheduler, recovery
+// gather/verify, SNP1 export, failure injection.
+//
+// Host code over the sm_100a kernels in ffx_kernels.cu.  No CPU compute
+// path exists for any payload byte: every copy, checksum and verification
+// runs on the GPU; the host only sizes, chooses slots and launches.
+#include <cuda_runtime.h>
+#include <unistd.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/ffx.h"
+#include "ffx_device.cuh"
+#include "ffx_kernels.h"
+#include "ffx_layout.h"
+
+using namespace ffx;
+
+// ---------------------------------------------------------------------------
+// errors
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int status, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return status;
+}
+
+int cuda_fail(cudaError_t e, const char* what) {
+  return fail(FFX_ECUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+#define FFX_CUDA(call)                                   \
+  do {                                                   \
+    cudaError_t e_ = (call);                             \
+    if (e_ != cudaSuccess) return cuda_fail(e_, #call);  \
+  } while (0)
+
+cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+void le(uint8_t* p, uint64_t v, int n) {
+  for (int i = 0; i < n; ++i) p[i] = static_cast<uint8_t>(v >> (8 * i));
+}
+uint64_t rd(const uint8_t* p, int n) {
+  uint64_t v = 0;
+  for (int i = n - 1; i >= 0; --i) v = (v << 8) | p[i];
+  return v;
+}
+
+bool valid_spec(const ffx_cluster_spec* s) {
+  return s && s->data_parallel && s->pipeline_parallel && s->tensor_parallel && s->gpus_per_node;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// objects
+
+struct Region {
+  int kind;
+  uint8_t* dev;
+  uint64_t bytes;
+  bool unique;
+};
+
+struct SlotCache {
+  bool known = false;
+  uint32_t state = kSlotEmpty;
+  uint64_t iteration = 0;
+  uint64_t seq = 0;
+};
+
+struct ffx_replica {
+  int device = 0;          // device the memory lives on
+  int owner_pid = 0;
+  bool owned = false;      // cudaMalloc'd here
+  bool ipc_opened = false; // cudaIpcOpenMemHandle'd here
+  uint8_t* base = nullptr;
+  ffx_role origin{};
+  uint64_t capacity = 0;
+  uint64_t slice_bytes = 0;
+  uint32_t versions = 0;
+  SlotLayout layout{};
+  std::vector<SlotCache> cache;  // writer-side view of the slots
+  ffx_ctx* ctx = nullptr;        // context that created/opened it
+
+  uint8_t* slot(uint32_t v) const { return base + v * layout.slot_stride; }
+  uint8_t* payload(uint32_t v) const { return slot(v) + layout.payload_off; }
+  uint64_t* sums(uint32_t v) const { return reinterpret_cast<uint64_t*>(slot(v) + kMetaBytes); }
+};
+
+struct ffx_ctx {
+  int device = 0;
+  ffx_cluster_spec spec{};
+  ffx_role self{};
+  uint64_t slice_bytes = 4096;
+  std::vector<Region> regions;
+  ffx_replica* target = nullptr;
+  unsigned int* done = nullptr;            // commit counter (device)
+  unsigned long long* result = nullptr;    // verify result (device, 2 words)
+  unsigned long long* result_host = nullptr;  // pinned mirror
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  uint64_t seq = 0;
+  uint32_t last_slot = 0;
+  uint64_t last_nslices = 0;
+  ffx_stats stats{};
+};
+
+namespace {
+
+struct HandleBlob {  // FFX_HANDLE_BYTES on the wire
+  uint32_t magic;    // "FFXH"
+  uint32_t abi;
+  int32_t pid;
+  int32_t device;
+  uint64_t raw;      // device pointer (valid in the exporting process)
+  uint64_t capacity, slice_bytes;
+  uint32_t versions;
+  uint16_t dp, pp, tp, pad_;
+  SlotLayout layout;
+  cudaIpcMemHandle_t ipc;
+};
+static_assert(sizeof(HandleBlob) <= FFX_HANDLE_BYTES, "handle too large");
+constexpr uint32_t kHandleMagic = 0x48584646u;
+
+int read_meta(ffx_replica* r, uint32_t v, SlotMeta* m) {
+  DeviceGuard g(r->ctx ? r->ctx->device : r->device);
+  FFX_CUDA(cudaMemcpy(m, r->slot(v), sizeof(SlotMeta), cudaMemcpyDefault));
+  return FFX_OK;
+}
+
+// Unique regions in registration order and their offsets in a slot payload.
+struct PayloadMap {
+  std::vector<const Region*> regs;
+  std::vector<uint64_t> offs;
+  uint64_t logical = 0;
+  uint64_t physical = 0;
+};
+
+PayloadMap payload_map(const ffx_ctx* c) {
+  PayloadMap m;
+  for (const auto& r : c->regions)
+    if (r.unique) {
+      m.regs.push_back(&r);
+      m.offs.push_back(m.physical);
+      m.logical += r.bytes;
+      m.physical = align_up(m.physical + r.bytes, kRegionAlign);
+    }
+  return m;
+}
+
+uint64_t slices_of(uint64_t bytes, uint64_t s) { return (bytes + s - 1) / s; }
+
+int refresh_cache(ffx_replica* r) {
+  for (uint32_t v = 0; v < r->versions; ++v) {
+    SlotMeta m;
+    int st = read_meta(r, v, &m);
+    if (st) return st;
+    SlotCache& c = r->cache[v];
+    c.known = true;
+    if (m.magic == kSlotMagic) {
+      c.state = m.state;
+      c.iteration = m.iteration;
+      c.seq = m.seq;
+    } else {
+      c.state = kSlotEmpty;
+      c.iteration = 0;
+      c.seq = 0;
+    }
+  }
+  return FFX_OK;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// status
+
+extern "C" const char* ffx_status_str(int s) {
+  switch (s) {
+    case FFX_OK: return "ok";
+    case FFX_ECONFIG: return "config error";
+    case FFX_EVERSION: return "version error";
+    case FFX_ERESTORE: return "restore error";
+    case FFX_ECORRUPT: return "corrupt snapshot";
+    case FFX_EINVAL: return "invalid argument";
+    case FFX_ERANGE: return "out of range";
+    case FFX_ECUDA: return "cuda error";
+    case FFX_ENOMEM: return "out of device memory";
+    case FFX_ESTATE: return "invalid state";
+  }
+  return "unknown";
+}
+extern "C" const char* ffx_last_error(void) { return g_err.c_str(); }
+extern "C" int ffx_abi_version(void) { return FFX_ABI_VERSION; }
+
+// ---------------------------------------------------------------------------
+// domain (domain.cpp:18-62)
+
+extern "C" int ffx_role_of(const ffx_cluster_spec* s, uint32_t idx, ffx_role* out) {
+  if (!valid_spec(s) || !out) return fail(FFX_EINVAL, "role_of: bad spec");
+  const uint64_t world = uint64_t{s->num_nodes} * s->gpus_per_node;
+  if (idx >= world) return fail(FFX_ERANGE, "role_of: index %u outside world of %llu", idx,
+                                (unsigned long long)world);
+  out->tp = static_cast<uint16_t>(idx % s->tensor_parallel);
+  out->pp = static_cast<uint16_t>((idx / s->tensor_parallel) % s->pipeline_parallel);
+  out->dp = static_cast<uint16_t>(idx / (s->tensor_parallel * s->pipeline_parallel));
+  return FFX_OK;
+}
+
+extern "C" int ffx_index_of(const ffx_cluster_spec* s, ffx_role r, uint32_t* out) {
+  if (!valid_spec(s) || !out) return fail(FFX_EINVAL, "index_of: bad spec");
+  if (r.tp >= s->tensor_parallel || r.pp >= s->pipeline_parallel || r.dp >= s->data_parallel)
+    return fail(FFX_ERANGE, "index_of: role d%up%ut%u outside layout", r.dp, r.pp, r.tp);
+  *out = (uint32_t{r.dp} * s->pipeline_parallel + r.pp) * s->tensor_parallel + r.tp;
+  return FFX_OK;
+}
+
+extern "C" int ffx_node_of(const ffx_cluster_spec* s, ffx_role r, uint32_t* out) {
+  uint32_t idx = 0;
+  int st = ffx_index_of(s, r, &idx);
+  if (st) return st;
+  *out = idx / s->gpus_per_node;
+  return FFX_OK;
+}
+
+extern "C" int ffx_dp_neighbor(const ffx_cluster_spec* s, ffx_role r, ffx_role* out) {
+  if (!valid_spec(s) || !out) return fail(FFX_EINVAL, "dp_neighbor: bad spec");
+  *out = r;
+  out->dp = static_cast<uint16_t>((r.dp + 1u) % s->data_parallel);
+  return FFX_OK;
+}
+
+extern "C" int ffx_dp_predecessor(const ffx_cluster_spec* s, ffx_role r, ffx_role* out) {
+  if (!valid_spec(s) || !out) return fail(FFX_EINVAL, "dp_predecessor: bad spec");
+  *out = r;
+  out->dp = static_cast<uint16_t>((r.dp + s->data_parallel - 1u) % s->data_parallel);
+  return FFX_OK;
+}
+
+// ---------------------------------------------------------------------------
+// recovery planning (controller.cpp:144-209)
+
+extern "C" int ffx_plan_recovery(const ffx_cluster_spec* s, const uint32_t* pods, uint32_t n_pods,
+                                 const ffx_role* roles, uint32_t n_roles, uint64_t global_consistent,
+                                 uint64_t latest_fallback, uint32_t replicas, ffx_recovery_plan* out) {
+  if (!valid_spec(s) || !out) return fail(FFX_EINVAL, "plan_recovery: bad arguments");
+  if ((n_pods && !pods) || (n_roles && !roles)) return fail(FFX_EINVAL, "plan_recovery: null list");
+  if (replicas < 1) replicas = 1;
+  auto key = [](const ffx_role& r) {
+    return (uint64_t{r.dp} << 32) | (uint64_t{r.pp} << 16) | r.tp;
+  };
+  std::vector<uint32_t> fp(pods, pods + n_pods);
+  std::sort(fp.begin(), fp.end());
+  fp.erase(std::unique(fp.begin(), fp.end()), fp.end());
+  std::vector<ffx_role> lost(roles, roles + n_roles);
+  for (uint32_t pod : fp)
+    for (uint32_t lr = 0; lr < s->gpus_per_node; ++lr) {
+      ffx_role r;
+      int st = ffx_role_of(s, pod * s->gpus_per_node + lr, &r);
+      if (st) return st;
+      lost.push_back(r);
+    }
+  // std::set<Role> ordering: (dp, pp, tp) lexicographic.
+  std::sort(lost.begin(), lost.end(), [&](const ffx_role& a, const ffx_role& b) { return key(a) < key(b); });
+  lost.erase(std::unique(lost.begin(), lost.end(),
+                         [&](const ffx_role& a, const ffx_role& b) { return key(a) == key(b); }),
+             lost.end());
+  auto is_lost = [&](const ffx_role& r) {
+    return std::binary_search(lost.begin(), lost.end(), r,
+                              [&](const ffx_role& a, const ffx_role& b) { return key(a) < key(b); });
+  };
+  const uint32_t cap = out->capacity;
+  if (fp.size() > cap || lost.size() > cap) return fail(FFX_ECONFIG, "plan_recovery: capacity %u too small", cap);
+  out->n_failed_pods = static_cast<uint32_t>(fp.size());
+  out->n_failed_roles = static_cast<uint32_t>(lost.size());
+  out->n_lazy = out->n_forwards = out->n_redundant = 0;
+  if (out->failed_pods) std::copy(fp.begin(), fp.end(), out->failed_pods);
+  if (out->failed_roles) std::copy(lost.begin(), lost.end(), out->failed_roles);
+
+  // Serving holder per lost role: first survivor among dp+1 .. dp+replicas.
+  const uint32_t d = s->data_parallel;
+  const uint32_t k = std::min<uint32_t>(replicas, d > 1 ? d - 1 : 1);
+  bool neighbor_ok = d > 1;
+  std::vector<uint32_t> holder(lost.size(), 0);
+  for (size_t i = 0; i < lost.size() && neighbor_ok; ++i) {
+    bool found = false;
+    for (uint32_t j = 1; j <= k; ++j) {
+      ffx_role h = lost[i];
+      h.dp = static_cast<uint16_t>((lost[i].dp + j) % d);
+      if (!is_lost(h)) {
+        holder[i] = h.dp;
+        found = true;
+        break;
+      }
+    }
+    if (!found) neighbor_ok = false;
+  }
+  ffx_uniqueness_plan up;
+  ffx_razor(s, &up);
+  if (!neighbor_ok) {
+    out->kind = 1;
+    out->resume_iteration = latest_fallback;
+    return FFX_OK;
+  }
+  out->kind = 0;
+  out->resume_iteration = global_consistent;
+  if (global_consistent == 0) return FFX_OK;  // rebuilt from the seed (controller.cpp:172-174)
+  for (size_t i = 0; i < lost.size(); ++i) {
+    const ffx_role f = lost[i];
+    if (up.unique_bytes_per_device > 0) {
+      ffx_role h = f;
+      h.dp = static_cast<uint16_t>(holder[i]);
+      ffx_forward fw{};
+      fw.origin = f;
+      fw.holder_dp = holder[i];
+      int st = ffx_node_of(s, h, &fw.holder_node);
+      if (!st) st = ffx_node_of(s, f, &fw.dest_node);
+      if (st) return st;
+      if (out->forwards) out->forwards[out->n_forwards] = fw;
+      out->n_forwards++;
+    }
+    if (up.weights_redundant || up.optimizer_redundant) {
+      for (uint32_t dp = 0; dp < d; ++dp) {
+        ffx_role cand{static_cast<uint16_t>(dp), f.pp, f.tp};
+        if (!is_lost(cand)) {
+          if (out->redundant_from) out->redundant_from[out->n_redundant] = ffx_redundant_source{f, cand};
+          out->n_redundant++;
+          break;
+        }
+      }
+    }
+  }
+  if (up.weights_redundant || up.optimizer_redundant) {
+    for (uint32_t pp = 0; pp < s->pipeline_parallel; ++pp)
+      for (uint32_t tp = 0; tp < s->tensor_parallel; ++tp)
+        for (uint32_t dp = 0; dp < d; ++dp) {
+          ffx_role cand{static_cast<uint16_t>(dp), static_cast<uint16_t>(pp), static_cast<uint16_t>(tp)};
+          if (!is_lost(cand)) {
+            if (out->n_lazy >= cap) return fail(FFX_ECONFIG, "plan_recovery: capacity %u too small", cap);
+            if (out->lazy_backup_targets) out->lazy_backup_targets[out->n_lazy] = cand;
+            out->n_lazy++;
+            break;
+          }
+        }
+  }
+  return FFX_OK;
+}
+
+// ---------------------------------------------------------------------------
+// sizing (ckpt.cpp:13-33, evolution.cpp:11-19)
+
+extern "C" uint64_t ffx_weights_bytes(const ffx_cluster_spec* s) {
+  return s ? 2 * s->params_per_device : 0;
+}
+
+extern "C" uint64_t ffx_optimizer_bytes(const ffx_cluster_spec* s) {
+  if (!s) return 0;
+  const uint64_t full = 12 * s->params_per_device;
+  if (!s->distributed_optimizer || s->data_parallel <= 1) return full;
+  return (full + s->data_parallel - 1) / s->data_parallel;
+}
+
+extern "C" int ffx_razor(const ffx_cluster_spec* s, ffx_uniqueness_plan* out) {
+  if (!s || !out) return fail(FFX_EINVAL, "razor: null argument");
+  out->weights_redundant = s->data_parallel > 1;
+  out->optimizer_redundant = s->data_parallel > 1 && !s->distributed_optimizer;
+  out->unique_bytes_per_device = out->optimizer_redundant ? 0 : ffx_optimizer_bytes(s);
+  return FFX_OK;
+}
+
+extern "C" int ffx_version_for_target(uint64_t held, uint64_t target, int* out) {
+  if (!out) return fail(FFX_EINVAL, "version_for_target: null out");
+  if (held == target) {
+    *out = 0;
+    return FFX_OK;
+  }
+  if (held == target + 1) {
+    *out = 1;
+    return FFX_OK;
+  }
+  return fail(FFX_EVERSION, "backup target %llu outside the retained window ending at %llu",
+              (unsigned long long)target, (unsigned long long)held);
+}
+
+// ---------------------------------------------------------------------------
+// SNP1 framing (storage.cpp:45-101)
+
+extern "C" int ffx_pack_header(ffx_role role, uint64_t iteration, uint8_t kind, uint64_t len,
+                               uint64_t checksum, uint8_t out[32]) {
+  if (!out) return fail(FFX_EINVAL, "pack_header: null out");
+  if (len > 0xffffffffull) return fail(FFX_EINVAL, "snapshot payload exceeds 4 GiB framing limit");
+  std::memset(out, 0, 32);
+  le(out + 0, 0x31504E53u, 4);
+  out[4] = 1;
+  out[5] = kind;
+  le(out + 6, role.dp, 2);
+  le(out + 8, role.pp, 2);
+  le(out + 10, role.tp, 2);
+  le(out + 12, iteration, 8);
+  le(out + 20, len, 4);
+  le(out + 24, checksum, 8);
+  return FFX_OK;
+}
+
+extern "C" int ffx_parse_header(const uint8_t* h, uint64_t framed_len, ffx_blob_info* out) {
+  if (!h || !out) return fail(FFX_EINVAL, "parse_header: null argument");
+  if (framed_len != 0 && framed_len < 32) return fail(FFX_ECORRUPT, "snapshot shorter than header");
+  if (rd(h, 4) != 0x31504E53u) return fail(FFX_ECORRUPT, "bad snapshot magic");
+  if (h[4] != 1) return fail(FFX_ECORRUPT, "unsupported snapshot format version");
+  if (h[5] > 1) return fail(FFX_ECORRUPT, "unknown blob kind");
+  out->kind = h[5];
+  out->role.dp = static_cast<uint16_t>(rd(h + 6, 2));
+  out->role.pp = static_cast<uint16_t>(rd(h + 8, 2));
+  out->role.tp = static_cast<uint16_t>(rd(h + 10, 2));
+  out->iteration = rd(h + 12, 8);
+  out->payload_len = static_cast<uint32_t>(rd(h + 20, 4));
+  out->checksum = rd(h + 24, 8);
+  if (framed_len != 0 && framed_len != 32 + uint64_t{out->payload_len})
+    return fail(FFX_ECORRUPT, "snapshot length disagrees with header");
+  return FFX_OK;
+}
+
+// ---------------------------------------------------------------------------
+// device primitives
+
+namespace {
+
+SliceJob single_job(const void* src, void* dst, uint64_t len, uint64_t slice_bytes) {
+  SliceJob job{};
+  job.nregions = 1;
+  job.reg[0] = SliceRegion{static_cast<const uint8_t*>(src), static_cast<uint8_t*>(dst), len, 0, 0};
+  job.slice_bytes = slice_bytes;
+  finalize_job(job);
+  return job;
+}
+
+bool slice_ok(uint64_t s) { return s >= 256 && s % 256 == 0; }
+
+}  // namespace
+
+extern "C" int ffx_checksum64(const void* dev, uint64_t len, uint64_t* host_out, void* stream) {
+  if (!host_out || (len && !dev)) return fail(FFX_EINVAL, "checksum64: null argument");
+  cudaError_t e = whole_fnv(static_cast<const uint8_t*>(dev), len, kFnvBasis, host_out,
+                            as_stream(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "whole_fnv");
+  return FFX_OK;
+}
+
+extern "C" int ffx_slice_checksums(const void* dev, uint64_t len, uint64_t slice_bytes,
+                                   uint64_t* dev_out, void* stream) {
+  if (!slice_ok(slice_bytes)) return fail(FFX_EINVAL, "slice_bytes must be a multiple of 256");
+  if (len == 0) return FFX_OK;
+  if (!dev || !dev_out) return fail(FFX_EINVAL, "slice_checksums: null argument");
+  SliceJob job = single_job(dev, nullptr, len, slice_bytes);
+  job.sums_out = dev_out;
+  FFX_CUDA(launch_slices(job, SliceMode::Hash, false, 0, as_stream(stream)));
+  return FFX_OK;
+}
+
+extern "C" int ffx_copy_checksums(void* dst, const void* src, uint64_t len, uint64_t slice_bytes,
+                                  uint64_t* dev_out, void* stream) {
+  if (!slice_ok(slice_bytes)) return fail(FFX_EINVAL, "slice_bytes must be a multiple of 256");
+  if (len == 0) return FFX_OK;
+  if (!dst || !src) return fail(FFX_EINVAL, "copy_checksums: null argument");
+  SliceJob job = single_job(src, dst, len, slice_bytes);
+  job.sums_out = dev_out;
+  FFX_CUDA(launch_slices(job, SliceMode::Copy, false, 0, as_stream(stream)));
+  return FFX_OK;
+}
+
+extern "C" int ffx_copy_verify(void* dst, const void* src, uint64_t len, uint64_t slice_bytes,
+                               const uint64_t* dev_expected, uint64_t* dev_result, void* stream) {
+  if (!slice_ok(slice_bytes)) return fail(FFX_EINVAL, "slice_bytes must be a multiple of 256");
+  if (!dev_result || !dev_expected) return fail(FFX_EINVAL, "copy_verify: null argument");
+  const unsigned long long init[2] = {~0ull, 0ull};
+  FFX_CUDA(cudaMemcpyAsync(dev_result, init, sizeof init, cudaMemcpyHostToDevice, as_stream(stream)));
+  if (len == 0) return FFX_OK;
+  SliceJob job = single_job(src, dst, len, slice_bytes);
+  job.sums_expected = dev_expected;
+  job.result = reinterpret_cast<unsigned long long*>(dev_result);
+  FFX_CUDA(launch_slices(job, dst ? SliceMode::CopyVerify : SliceMode::HashVerify, false, 0,
+                         as_stream(stream)));
+  return FFX_OK;
+}
+
+extern "C" int ffx_expand(void* dst, const uint8_t digest[32], uint64_t bytes, void* stream) {
+  if (!digest || (bytes && !dst)) return fail(FFX_EINVAL, "expand: null argument");
+  uint64_t fold = rd(digest, 8);
+  FFX_CUDA(launch_expand(static_cast<uint8_t*>(dst), fold, bytes, nullptr, as_stream(stream)));
+  return FFX_OK;
+}
+
+extern "C" int ffx_materialize(void* dst, const uint8_t digest[32], uint64_t bytes, void* stream) {
+  if (!digest) return fail(FFX_EINVAL, "materialize: null digest");
+  if (bytes < 32) return fail(FFX_EINVAL, "state blob smaller than its digest prefix");
+  if (!dst) return fail(FFX_EINVAL, "materialize: null dst");
+  FFX_CUDA(launch_expand(static_cast<uint8_t*>(dst), rd(digest, 8), bytes, digest,
+                         as_stream(stream)));
+  return FFX_OK;
+}
+
+extern "C" int ffx_blob_check(const void* dev, uint64_t bytes, uint64_t* host_first_bad,
+                              void* stream) {
+  if (!host_first_bad) return fail(FFX_EINVAL, "blob_check: null out");
+  if (bytes < 32) {  // evolution.cpp:107: shorter than the digest is never sound
+    *host_first_bad = 0;
+    return FFX_OK;
+  }
+  unsigned long long* d = nullptr;
+  cudaStream_t s = as_stream(stream);
+  FFX_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d), 8, s));
+  const unsigned long long init = ~0ull;
+  FFX_CUDA(cudaMemcpyAsync(d, &init, 8, cudaMemcpyHostToDevice, s));
+  FFX_CUDA(launch_blob_check(static_cast<const uint8_t*>(dev), bytes, d, s));
+  unsigned long long r = 0;
+  FFX_CUDA(cudaMemcpyAsync(&r, d, 8, cudaMemcpyDeviceToHost, s));
+  FFX_CUDA(cudaFreeAsync(d, s));
+  FFX_CUDA(cudaStreamSynchronize(s));
+  *host_first_bad = r;
+  return FFX_OK;
+}
+
+// ---------------------------------------------------------------------------
+// context + registry
+
+extern "C" int ffx_open(int device, const ffx_cluster_spec* spec, ffx_role self,
+                        uint64_t slice_bytes, ffx_ctx** out) {
+  if (!out || !valid_spec(spec)) return fail(FFX_EINVAL, "open: bad arguments");
+  if (slice_bytes == 0) slice_bytes = 4096;
+  if (!slice_ok(slice_bytes)) return fail(FFX_EINVAL, "slice_bytes must be a multiple of 256");
+  int ndev = 0;
+  FFX_CUDA(cudaGetDeviceCount(&ndev));
+  if (device < 0 || device >= ndev) return fail(FFX_EINVAL, "open: no device %d", device);
+  DeviceGuard g(device);
+  auto* c = new ffx_ctx;
+  c->device = device;
+  c->spec = *spec;
+  c->self = self;
+  c->slice_bytes = slice_bytes;
+  cudaError_t e = cudaMalloc(&c->done, 256);
+  if (e == cudaSuccess) e = cudaMemset(c->done, 0, 256);
+  if (e == cudaSuccess) e = cudaMalloc(&c->result, 16);
+  if (e == cudaSuccess) e = cudaMallocHost(&c->result_host, 16);
+  if (e == cudaSuccess) e = cudaEventCreate(&c->ev0);
+  if (e == cudaSuccess) e = cudaEventCreate(&c->ev1);
+  if (e != cudaSuccess) {
+    ffx_close(c);
+    return cuda_fail(e, "open");
+  }
+  *out = c;
+  return FFX_OK;
+}
+
+extern "C" int ffx_close(ffx_ctx* c) {
+  if (!c) return FFX_OK;
+  DeviceGuard g(c->device);
+  if (c->done) cudaFree(c->done);
+  if (c->result) cudaFree(c->result);
+  if (c->result_host) cudaFreeHost(c->result_host);
+  if (c->ev0) cudaEventDestroy(c->ev0);
+  if (c->ev1) cudaEventDestroy(c->ev1);
+  delete c;
+  return FFX_OK;
+}
+
+extern "C" int ffx_register_region(ffx_ctx* c, int kind, void* dev, uint64_t bytes, int unique) {
+  if (!c) return fail(FFX_EINVAL, "register_region: null ctx");
+  if (c->regions.size() >= kMaxRegions)
+    return fail(FFX_ECONFIG, "state registry holds at most %u regions", kMaxRegions);
+  if (bytes && !dev) return fail(FFX_EINVAL, "register_region: null pointer");
+  if (reinterpret_cast<uintptr_t>(dev) % 16)
+    return fail(FFX_EINVAL, "register_region: device pointer must be 16-byte aligned");
+  if (kind < FFX_REGION_MASTER || kind > FFX_REGION_BLOB)
+    return fail(FFX_EINVAL, "register_region: unknown kind %d", kind);
+  c->regions.push_back(Region{kind, static_cast<uint8_t*>(dev), bytes, unique != 0});
+  return FFX_OK;
+}
+
+extern "C" int ffx_clear_regions(ffx_ctx* c) {
+  if (!c) return fail(FFX_EINVAL, "clear_regions: null ctx");
+  c->regions.clear();
+  return FFX_OK;
+}
+
+extern "C" int ffx_plan(ffx_ctx* c, ffx_plan_info* out) {
+  if (!c || !out) return fail(FFX_EINVAL, "plan: null argument");
+  std::memset(out, 0, sizeof *out);
+  ffx_razor(&c->spec, &out->razor);
+  out->slice_bytes = c->slice_bytes;
+  out->num_regions = static_cast<uint32_t>(c->regions.size());
+  for (const auto& r : c->regions) {
+    if (r.unique) {
+      out->registered_unique_bytes += r.bytes;
+      out->num_slices += slices_of(r.bytes, c->slice_bytes);
+      out->num_unique_regions++;
+    } else {
+      out->registered_redundant_bytes += r.bytes;
+    }
+  }
+  return FFX_OK;
+}
+
+// ---------------------------------------------------------------------------
+// replicas
+
+extern "C" int ffx_replica_create(ffx_ctx* c, ffx_role origin, uint64_t capacity, uint32_t versions,
+                                  ffx_replica** out) {
+  if (!c || !out) return fail(FFX_EINVAL, "replica_create: null argument");
+  if (versions < 1 || versions > 8) return fail(FFX_EINVAL, "replica_create: 1..8 versions");
+  DeviceGuard g(c->device);
+  auto* r = new ffx_replica;
+  r->device = c->device;
+  r->owner_pid = getpid();
+  r->owned = true;
+  r->origin = origin;
+  r->capacity = capacity;
+  r->slice_bytes = c->slice_bytes;
+  r->versions = versions;
+  r->layout = make_layout(capacity, c->slice_bytes);
+  r->cache.assign(versions, SlotCache{});
+  r->ctx = c;
+  const uint64_t total = r->layout.slot_stride * versions;
+  cudaError_t e = cudaMalloc(&r->base, total);
+  if (e != cudaSuccess) {
+    delete r;
+    cudaGetLastError();
+    return fail(FFX_ENOMEM, "replica_create: cudaMalloc(%llu): %s", (unsigned long long)total,
+                cudaGetErrorString(e));
+  }
+  for (uint32_t v = 0; v < versions; ++v) {
+    e = cudaMemset(r->slot(v), 0, kMetaBytes);
+    if (e != cudaSuccess) break;
+    r->cache[v].known = true;
+  }
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) {
+    cudaFree(r->base);
+    delete r;
+    return cuda_fail(e, "replica_create");
+  }
+  *out = r;
+  return FFX_OK;
+}
+
+extern "C" int ffx_replica_export(const ffx_replica* r, uint8_t handle[FFX_HANDLE_BYTES]) {
+  if (!r || !handle) return fail(FFX_EINVAL, "replica_export: null argument");
+  HandleBlob h{};
+  h.magic = kHandleMagic;
+  h.abi = FFX_ABI_VERSION;
+  h.pid = r->owner_pid;
+  h.device = r->device;
+  h.raw = reinterpret_cast<uint64_t>(r->base);
+  h.capacity = r->capacity;
+  h.slice_bytes = r->slice_bytes;
+  h.versions = r->versions;
+  h.dp = r->origin.dp;
+  h.pp = r->origin.pp;
+  h.tp = r->origin.tp;
+  h.layout = r->layout;
+  if (r->owned) {
+    DeviceGuard g(r->device);
+    FFX_CUDA(cudaIpcGetMemHandle(&h.ipc, r->base));
+  }
+  std::memset(handle, 0, FFX_HANDLE_BYTES);
+  std::memcpy(handle, &h, sizeof h);
+  return FFX_OK;
+}
+
+extern "C" int ffx_replica_open(ffx_ctx* c, const uint8_t handle[FFX_HANDLE_BYTES],
+                                ffx_replica** out) {
+  if (!c || !handle || !out) return fail(FFX_EINVAL, "replica_open: null argument");
+  HandleBlob h;
+  std::memcpy(&h, handle, sizeof h);
+  if (h.magic != kHandleMagic || h.abi != FFX_ABI_VERSION)
+    return fail(FFX_EINVAL, "replica_open: not an ffx replica handle");
+  DeviceGuard g(c->device);
+  auto* r = new ffx_replica;
+  r->device = h.device;
+  r->owner_pid = h.pid;
+  r->origin = ffx_role{h.dp, h.pp, h.tp};
+  r->capacity = h.capacity;
+  r->slice_bytes = h.slice_bytes;
+  r->versions = h.versions;
+  r->layout = h.layout;
+  r->cache.assign(h.versions, SlotCache{});
+  r->ctx = c;
+  if (h.pid == getpid()) {
+    r->base = reinterpret_cast<uint8_t*>(h.raw);
+    if (h.device != c->device) {
+      int can = 0;
+      FFX_CUDA(cudaDeviceCanAccessPeer(&can, c->device, h.device));
+      if (!can) {
+        delete r;
+        return fail(FFX_ECONFIG, "device %d cannot access peer %d", c->device, h.device);
+      }
+      cudaError_t e = cudaDeviceEnablePeerAccess(h.device, 0);
+      if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+      else if (e != cudaSuccess) {
+        delete r;
+        return cuda_fail(e, "cudaDeviceEnablePeerAccess");
+      }
+    }
+  } else {
+    void* p = nullptr;
+    cudaError_t e = cudaIpcOpenMemHandle(&p, h.ipc, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) {
+      delete r;
+      return cuda_fail(e, "cudaIpcOpenMemHandle");
+    }
+    r->base = static_cast<uint8_t*>(p);
+    r->ipc_opened = true;
+  }
+  int st = refresh_cache(r);
+  if (st) {
+    ffx_replica_destroy(r);
+    return st;
+  }
+  *out = r;
+  return FFX_OK;
+}
+
+extern "C" int ffx_replica_destroy(ffx_replica* r) {
+  if (!r) return FFX_OK;
+  if (r->ctx && r->ctx->target == r) r->ctx->target = nullptr;
+  DeviceGuard g(r->ctx ? r->ctx->device : r->device);
+  if (r->owned && r->base) cudaFree(r->base);
+  if (r->ipc_opened && r->base) cudaIpcCloseMemHandle(r->base);
+  delete r;
+  return FFX_OK;
+}
+
+extern "C" int ffx_replica_slots(const ffx_replica* r, uint32_t* versions) {
+  if (!r || !versions) return fail(FFX_EINVAL, "replica_slots: null argument");
+  *versions = r->versions;
+  return FFX_OK;
+}
+
+extern "C" int ffx_replica_slot_info(ffx_replica* r, uint32_t slot, ffx_slot_info* out) {
+  if (!r || !out) return fail(FFX_EINVAL, "slot_info: null argument");
+  if (slot >= r->versions) return fail(FFX_ERANGE, "slot_info: slot %u of %u", slot, r->versions);
+  SlotMeta m;
+  int st = read_meta(r, slot, &m);
+  if (st) return st;
+  std::memset(out, 0, sizeof *out);
+  if (m.magic != kSlotMagic) return FFX_OK;  // never written: empty
+  out->state = m.state;
+  out->num_regions = m.num_regions;
+  out->role = ffx_role{m.dp, m.pp, m.tp};
+  out->kind = m.kind;
+  out->whole_checksum_valid = m.whole_checksum_valid;
+  out->iteration = m.iteration;
+  out->payload_len = m.payload_len;
+  out->slice_bytes = m.slice_bytes;
+  out->num_slices = m.num_slices;
+  out->whole_checksum = m.whole_checksum;
+  out->seq = m.seq;
+  return FFX_OK;
+}
+
+extern "C" int ffx_replica_newest(ffx_replica* r, uint64_t* iteration) {
+  if (!r || !iteration) return fail(FFX_EINVAL, "replica_newest: null argument");
+  uint64_t best_seq = 0;
+  bool any = false;
+  for (uint32_t v = 0; v < r->versions; ++v) {
+    SlotMeta m;
+    int st = read_meta(r, v, &m);
+    if (st) return st;
+    if (m.magic == kSlotMagic && m.state == kSlotCommitted && (!any || m.seq > best_seq)) {
+      any = true;
+      best_seq = m.seq;
+      *iteration = m.iteration;
+    }
+  }
+  if (!any) return fail(FFX_ERESTORE, "replica holds no committed snapshot");
+  return FFX_OK;
+}
+
+extern "C" int ffx_replica_slot_ptrs(ffx_replica* r, uint32_t slot, void** payload, uint64_t** sums) {
+  if (!r) return fail(FFX_EINVAL, "slot_ptrs: null replica");
+  if (slot >= r->versions) return fail(FFX_ERANGE, "slot_ptrs: slot %u of %u", slot, r->versions);
+  if (payload) *payload = r->payload(slot);
+  if (sums) *sums = r->sums(slot);
+  return FFX_OK;
+}
+
+extern "C" int ffx_replica_clear(ffx_replica* r) {
+  if (!r) return fail(FFX_EINVAL, "replica_clear: null replica");
+  DeviceGuard g(r->ctx ? r->ctx->device : r->device);
+  for (uint32_t v = 0; v < r->versions; ++v) {
+    FFX_CUDA(cudaMemset(r->slot(v), 0, kMetaBytes));
+    r->cache[v] = SlotCache{true, kSlotEmpty, 0, 0};
+  }
+  FFX_CUDA(cudaDeviceSynchronize());
+  return FFX_OK;
+}
+
+namespace {
+
+// Locate the slot holding `iteration` in any state.  -1 when absent.
+int find_slot(ffx_replica* r, uint64_t iteration, SlotMeta* meta) {
+  int found = -1;
+  uint64_t best_seq = 0;
+  for (uint32_t v = 0; v < r->versions; ++v) {
+    SlotMeta m;
+    if (read_meta(r, v, &m)) return -2;
+    if (m.magic != kSlotMagic || m.state == kSlotEmpty || m.iteration != iteration) continue;
+    // Prefer a committed copy; among equals the newest write.
+    const bool better = found < 0 || (m.state == kSlotCommitted && meta->state != kSlotCommitted) ||
+                        (m.state == meta->state && m.seq > best_seq);
+    if (better) {
+      found = static_cast<int>(v);
+      best_seq = m.seq;
+      *meta = m;
+    }
+  }
+  return found;
+}
+
+}  // namespace
+
+extern "C" int ffx_replica_export_frame(ffx_replica* r, uint64_t iteration, void* host_dst,
+                                        uint64_t cap, uint64_t* framed_len, void* stream) {
+  if (!r || !framed_len) return fail(FFX_EINVAL, "export_frame: null argument");
+  DeviceGuard g(r->ctx ? r->ctx->device : r->device);
+  SlotMeta m;
+  const int v = find_slot(r, iteration, &m);
+  if (v == -2) return fail(FFX_ECUDA, "export_frame: cannot read slot metadata: %s", g_err.c_str());
+  if (v < 0 || m.state != kSlotCommitted)
+    return fail(FFX_ERESTORE, "no committed snapshot at iteration %llu", (unsigned long long)iteration);
+  if (m.payload_len > 0xffffffffull)
+    return fail(FFX_EINVAL, "snapshot payload exceeds 4 GiB framing limit");
+  *framed_len = 32 + m.payload_len;
+  if (!host_dst) return FFX_OK;  // size query
+  if (cap < *framed_len) return fail(FFX_ECONFIG, "export_frame: buffer of %llu < %llu bytes",
+                                     (unsigned long long)cap, (unsigned long long)*framed_len);
+  cudaStream_t s = as_stream(stream);
+  uint8_t* pay = r->payload(static_cast<uint32_t>(v));
+  // Region offsets inside the slot payload (256-byte aligned, registration order).
+  std::vector<uint64_t> offs, lens;
+  uint64_t phys = 0;
+  for (uint32_t i = 0; i < m.num_regions; ++i) {
+    offs.push_back(phys);
+    lens.push_back(m.region_bytes[i]);
+    phys = align_up(phys + m.region_bytes[i], kRegionAlign);
+  }
+  if (!m.whole_checksum_valid) {
+    uint64_t h = kFnvBasis;
+    for (size_t i = 0; i < offs.size(); ++i) {
+      cudaError_t e = whole_fnv(pay + offs[i], lens[i], h, &h, s);
+      if (e != cudaSuccess) return cuda_fail(e, "whole_fnv");
+    }
+    m.whole_checksum = h;
+    m.whole_checksum_valid = 1;
+    // Persist into the slot meta and the SNP1 header so later exports are free.
+    uint8_t hdr[32];
+    int st = ffx_pack_header(ffx_role{m.dp, m.pp, m.tp}, m.iteration, m.kind, m.payload_len, h, hdr);
+    if (st) return st;
+    FFX_CUDA(cudaMemcpyAsync(r->slot(v) + offsetof(SlotMeta, whole_checksum), &m.whole_checksum, 8,
+                             cudaMemcpyHostToDevice, s));
+    FFX_CUDA(cudaMemcpyAsync(r->slot(v) + offsetof(SlotMeta, whole_checksum_valid),
+                             &m.whole_checksum_valid, 1, cudaMemcpyHostToDevice, s));
+    FFX_CUDA(cudaMemcpyAsync(pay - 32, hdr, 32, cudaMemcpyHostToDevice, s));
+    FFX_CUDA(cudaStreamSynchronize(s));
+  }
+  uint8_t* dst = static_cast<uint8_t*>(host_dst);
+  FFX_CUDA(cudaMemcpyAsync(dst, pay - 32, 32, cudaMemcpyDeviceToHost, s));
+  uint64_t o = 32;
+  for (size_t i = 0; i < offs.size(); ++i) {
+    if (lens[i]) FFX_CUDA(cudaMemcpyAsync(dst + o, pay + offs[i], lens[i], cudaMemcpyDeviceToHost, s));
+    o += lens[i];
+  }
+  FFX_CUDA(cudaStreamSynchronize(s));
+  return FFX_OK;
+}
+
+// ---------------------------------------------------------------------------
+// snapshot
+
+extern "C" int ffx_snapshot_target(ffx_ctx* c, ffx_replica* t) {
+  if (!c) return fail(FFX_EINVAL, "snapshot_target: null ctx");
+  c->target = t;
+  if (t) {
+    int st = refresh_cache(t);
+    if (st) return st;
+    for (const auto& sc : t->cache) c->seq = std::max(c->seq, sc.seq);
+  }
+  return FFX_OK;
+}
+
+extern "C" int ffx_snapshot(ffx_ctx* c, uint64_t iteration, void* stream, const ffx_snapshot_opts* o) {
+  if (!c) return fail(FFX_EINVAL, "snapshot: null ctx");
+  ffx_replica* t = c->target;
+  if (!t) return fail(FFX_ESTATE, "snapshot: no target replica (ffx_snapshot_target)");
+  ffx_snapshot_opts opts{};
+  if (o) opts = *o;
+  const PayloadMap pm = payload_map(c);
+  if (pm.logical > t->capacity)
+    return fail(FFX_ECONFIG, "snapshot payload %llu exceeds the replica buffer of %llu bytes",
+                (unsigned long long)pm.logical, (unsigned long long)t->capacity);
+  if (pm.physical > t->layout.payload_cap)
+    return fail(FFX_ECONFIG, "snapshot regions need %llu payload bytes, slot has %llu",
+                (unsigned long long)pm.physical, (unsigned long long)t->layout.payload_cap);
+  uint64_t nslices = 0;
+  for (const Region* r : pm.regs) nslices += slices_of(r->bytes, c->slice_bytes);
+  if (nslices > t->layout.table_cap)
+    return fail(FFX_ECONFIG, "snapshot needs %llu checksum entries, slot has %llu",
+                (unsigned long long)nslices, (unsigned long long)t->layout.table_cap);
+  if (c->slice_bytes != t->slice_bytes && t->layout.table_cap < nslices)
+    return fail(FFX_ECONFIG, "slice size mismatch");
+
+  // Two-version rule (ckpt.cpp:46-52): replace the slot holding this
+  // iteration, else an empty slot, else the oldest.
+  int v = -1;
+  for (uint32_t i = 0; i < t->versions; ++i)
+    if (t->cache[i].state != kSlotEmpty && t->cache[i].iteration == iteration) v = static_cast<int>(i);
+  if (v < 0)
+    for (uint32_t i = 0; i < t->versions && v < 0; ++i)
+      if (t->cache[i].state == kSlotEmpty) v = static_cast<int>(i);
+  if (v < 0) {
+    v = 0;
+    for (uint32_t i = 1; i < t->versions; ++i)
+      if (t->cache[i].seq < t->cache[static_cast<uint32_t>(v)].seq) v = static_cast<int>(i);
+  }
+  const uint32_t slot = static_cast<uint32_t>(v);
+  const uint64_t seq = ++c->seq;
+
+  DeviceGuard g(c->device);
+  SliceJob job{};
+  job.nregions = static_cast<uint32_t>(pm.regs.size());
+  for (size_t i = 0; i < pm.regs.size(); ++i)
+    job.reg[i] = SliceRegion{pm.regs[i]->dev, t->payload(slot) + pm.offs[i], pm.regs[i]->bytes, 0, 0};
+  job.slice_bytes = c->slice_bytes;
+  job.sums_out = t->sums(slot);
+  finalize_job(job);
+
+  SlotMeta m{};
+  m.magic = kSlotMagic;
+  m.state = kSlotCommitted;
+  m.iteration = iteration;
+  m.seq = seq;
+  m.payload_len = pm.logical;
+  m.slice_bytes = c->slice_bytes;
+  m.num_slices = nslices;
+  m.dp = c->self.dp;
+  m.pp = c->self.pp;
+  m.tp = c->self.tp;
+  m.kind = opts.weights_kind ? 0 : 1;
+  m.num_regions = job.nregions;
+  for (size_t i = 0; i < pm.regs.size(); ++i) m.region_bytes[i] = pm.regs[i]->bytes;
+  uint8_t hdr[32];
+  ffx_pack_header(c->self, iteration, m.kind, pm.logical > 0xffffffffull ? 0 : pm.logical, 0, hdr);
+
+  SlotCommit& cm = job.commit;
+  cm.slot = t->slot(slot);
+  cm.done = c->done;
+  cm.payload_off = t->layout.payload_off;
+  cm.iteration = iteration;
+  cm.seq = seq;
+  std::memcpy(cm.meta, &m, sizeof m);
+  std::memcpy(cm.snp1, hdr, 32);
+
+  // Slice scheduler: split the warp tasks into `batches` launches, each
+  // optionally gated on a caller event (a measured gap in the step's own
+  // collectives), all on the caller's (low-priority) stream.
+  cudaStream_t s = as_stream(stream);
+  const uint32_t batches = std::max<uint32_t>(1, opts.batches);
+  const uint64_t G = job.total_groups;
+  auto* gates = static_cast<cudaEvent_t*>(opts.gate_events);
+  for (uint32_t b = 0; b < batches; ++b) {
+    SliceJob bj = job;
+    bj.group_lo = G * b / batches;
+    bj.group_hi = G * (b + 1) / batches;
+    bj.commit.finalize = (b + 1 == batches);
+    if (gates && gates[b]) FFX_CUDA(cudaStreamWaitEvent(s, gates[b], 0));
+    if (bj.group_lo == bj.group_hi && !bj.commit.finalize) continue;
+    FFX_CUDA(launch_slices(bj, SliceMode::Copy, true, opts.max_ctas, s));
+    c->stats.kernel_launches++;
+  }
+  t->cache[slot] = SlotCache{true, kSlotCommitted, iteration, seq};
+  c->last_slot = slot;
+  c->last_nslices = nslices;
+  c->stats.snapshots++;
+  c->stats.snapshot_bytes += pm.logical;
+
+  if (opts.verify_on_store) {
+    // Holder-side re-verification of the landed slot (NeighborBuffer::store
+    // validates before accepting, ckpt.cpp:78): HBM read of the replica.
+    const unsigned long long init[2] = {~0ull, 0ull};
+    FFX_CUDA(cudaMemcpyAsync(c->result, init, sizeof init, cudaMemcpyHostToDevice, s));
+    SliceJob vj = job;
+    for (size_t i = 0; i < pm.regs.size(); ++i) {
+      vj.reg[i].src = t->payload(slot) + pm.offs[i];
+      vj.reg[i].dst = nullptr;
+    }
+    vj.sums_out = nullptr;
+    vj.sums_expected = t->sums(slot);
+    vj.result = c->result;
+    vj.commit = SlotCommit{};
+    FFX_CUDA(launch_slices(vj, SliceMode::HashVerify, false, opts.max_ctas, s));
+    c->stats.kernel_launches++;
+    FFX_CUDA(cudaMemcpyAsync(c->result_host, c->result, 16, cudaMemcpyDeviceToHost, s));
+    FFX_CUDA(cudaStreamSynchronize(s));
+    if (c->result_host[1]) {
+      c->stats.verify_failures++;
+      return fail(FFX_ECORRUPT, "snapshot verify-on-store: %llu bad slices (first %llu)",
+                  c->result_host[1], c->result_host[0]);
+    }
+  }
+  return FFX_OK;
+}
+
+extern "C" int ffx_snapshot_read_sums(ffx_ctx* c, uint64_t* host_dst, uint64_t max_entries,
+                                      uint64_t* n_out, void* stream) {
+  if (!c || !n_out) return fail(FFX_EINVAL, "snapshot_read_sums: null argument");
+  if (!c->target || !c->stats.snapshots) return fail(FFX_ESTATE, "snapshot_read_sums: no snapshot taken");
+  const uint64_t n = std::min(max_entries, c->last_nslices);
+  *n_out = n;
+  if (n && host_dst) {
+    DeviceGuard g(c->device);
+    FFX_CUDA(cudaMemcpyAsync(host_dst, c->target->sums(c->last_slot), n * 8, cudaMemcpyDefault,
+                             as_stream(stream)));
+  }
+  return FFX_OK;
+}
+
+// ---------------------------------------------------------------------------
+// recovery
+
+extern "C" int ffx_recover(ffx_ctx* c, ffx_replica* src, uint64_t target, void* stream,
+                           ffx_recover_report* rep) {
+  if (!c || !src) return fail(FFX_EINVAL, "recover: null argument");
+  DeviceGuard g(c->device);
+  ffx_recover_report local{};
+  ffx_recover_report& R = rep ? *rep : local;
+  std::memset(&R, 0, sizeof R);
+  R.first_bad_slice = ~0ull;
+  SlotMeta m;
+  const int v = find_slot(src, target, &m);
+  if (v == -2) return fail(FFX_ECUDA, "recover: cannot read replica metadata: %s", g_err.c_str());
+  // ckpt.cpp:111-136 (checked): missing, invalid, wrong kind, stale, wrong role.
+  if (v < 0) return fail(FFX_ERESTORE, "unique-state source missing: no snapshot at iteration %llu",
+                         (unsigned long long)target);
+  R.slot = static_cast<uint32_t>(v);
+  if (m.state != kSlotCommitted)
+    return fail(FFX_ERESTORE, "unique-state source invalid: slot %d torn (write never committed)", v);
+  if (m.kind != 1) return fail(FFX_ERESTORE, "unique-state source has the wrong kind");
+  if (m.iteration != target)
+    return fail(FFX_ERESTORE, "unique-state source is at iteration %llu, want %llu",
+                (unsigned long long)m.iteration, (unsigned long long)target);
+  if (m.dp != c->self.dp || m.pp != c->self.pp || m.tp != c->self.tp)
+    return fail(FFX_ERESTORE, "unique-state source is for d%up%ut%u, want d%up%ut%u", m.dp, m.pp,
+                m.tp, c->self.dp, c->self.pp, c->self.tp);
+  const PayloadMap pm = payload_map(c);
+  if (m.num_regions != pm.regs.size())
+    return fail(FFX_ERESTORE, "snapshot has %u regions, %zu registered", m.num_regions, pm.regs.size());
+  for (size_t i = 0; i < pm.regs.size(); ++i)
+    if (m.region_bytes[i] != pm.regs[i]->bytes)
+      return fail(FFX_ERESTORE, "region %zu: snapshot %llu bytes, registered %llu", i,
+                  (unsigned long long)m.region_bytes[i], (unsigned long long)pm.regs[i]->bytes);
+
+  cudaStream_t s = as_stream(stream);
+  SliceJob job{};
+  job.nregions = static_cast<uint32_t>(pm.regs.size());
+  for (size_t i = 0; i < pm.regs.size(); ++i)
+    job.reg[i] = SliceRegion{src->payload(R.slot) + pm.offs[i], pm.regs[i]->dev, pm.regs[i]->bytes, 0, 0};
+  job.slice_bytes = m.slice_bytes;
+  job.sums_expected = src->sums(R.slot);
+  job.result = c->result;
+  finalize_job(job);
+  const unsigned long long init[2] = {~0ull, 0ull};
+  FFX_CUDA(cudaMemcpyAsync(c->result, init, sizeof init, cudaMemcpyHostToDevice, s));
+  FFX_CUDA(cudaEventRecord(c->ev0, s));
+  FFX_CUDA(launch_slices(job, SliceMode::CopyVerify, false, 0, s));
+  FFX_CUDA(cudaEventRecord(c->ev1, s));
+  c->stats.kernel_launches++;
+  FFX_CUDA(cudaMemcpyAsync(c->result_host, c->result, 16, cudaMemcpyDeviceToHost, s));
+  FFX_CUDA(cudaStreamSynchronize(s));
+  float ms = 0;
+  cudaEventElapsedTime(&ms, c->ev0, c->ev1);
+  R.seconds = ms * 1e-3;
+  R.bytes = pm.logical;
+  R.first_bad_slice = c->result_host[0];
+  R.bad_slices = c->result_host[1];
+  c->stats.recoveries++;
+  c->stats.recovered_bytes += pm.logical;
+  if (R.bad_slices) {
+    c->stats.verify_failures++;
+    return fail(FFX_ERESTORE, "unique-state source invalid: snapshot checksum mismatch in %llu "
+                "slices (first slice %llu)", (unsigned long long)R.bad_slices,
+                (unsigned long long)R.first_bad_slice);
+  }
+  return FFX_OK;
+}
+
+extern "C" int ffx_recover_region(ffx_ctx* c, uint32_t idx, const void* peer_src,
+                                  const uint64_t* peer_sums, void* stream, ffx_recover_report* rep) {
+  if (!c || !peer_src || !peer_sums) return fail(FFX_EINVAL, "recover_region: null argument");
+  if (idx >= c->regions.size()) return fail(FFX_ERANGE, "recover_region: no region %u", idx);
+  DeviceGuard g(c->device);
+  ffx_recover_report local{};
+  ffx_recover_report& R = rep ? *rep : local;
+  std::memset(&R, 0, sizeof R);
+  const Region& reg = c->regions[idx];
+  cudaStream_t s = as_stream(stream);
+  SliceJob job = single_job(peer_src, reg.dev, reg.bytes, c->slice_bytes);
+  job.sums_expected = peer_sums;
+  job.result = c->result;
+  const unsigned long long init[2] = {~0ull, 0ull};
+  FFX_CUDA(cudaMemcpyAsync(c->result, init, sizeof init, cudaMemcpyHostToDevice, s));
+  FFX_CUDA(cudaEventRecord(c->ev0, s));
+  if (reg.bytes) FFX_CUDA(launch_slices(job, SliceMode::CopyVerify, false, 0, s));
+  FFX_CUDA(cudaEventRecord(c->ev1, s));
+  FFX_CUDA(cudaMemcpyAsync(c->result_host, c->result, 16, cudaMemcpyDeviceToHost, s));
+  FFX_CUDA(cudaStreamSynchronize(s));
+  float ms = 0;
+  cudaEventElapsedTime(&ms, c->ev0, c->ev1);
+  R.seconds = ms * 1e-3;
+  R.bytes = reg.bytes;
+  R.first_bad_slice = c->result_host[0];
+  R.bad_slices = c->result_host[1];
+  c->stats.recovered_bytes += reg.bytes;
+  if (R.bad_slices)
+    return fail(FFX_ERESTORE, "weights source invalid: checksum mismatch in %llu slices",
+                (unsigned long long)R.bad_slices);
+  return FFX_OK;
+}
+
+extern "C" int ffx_ipc_export(void* dev_base, uint8_t handle[64]) {
+  if (!dev_base || !handle) return fail(FFX_EINVAL, "ipc_export: null argument");
+  cudaIpcMemHandle_t h;
+  FFX_CUDA(cudaIpcGetMemHandle(&h, dev_base));
+  std::memcpy(handle, &h, 64);
+  return FFX_OK;
+}
+
+extern "C" int ffx_ipc_open(const uint8_t handle[64], void** dev_base) {
+  if (!handle || !dev_base) return fail(FFX_EINVAL, "ipc_open: null argument");
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle, 64);
+  FFX_CUDA(cudaIpcOpenMemHandle(dev_base, h, cudaIpcMemLazyEnablePeerAccess));
+  return FFX_OK;
+}
+
+extern "C" int ffx_ipc_close(void* dev_base) {
+  if (!dev_base) return FFX_OK;
+  FFX_CUDA(cudaIpcCloseMemHandle(dev_base));
+  return FFX_OK;
+}
+
+// ---------------------------------------------------------------------------
+// failure injection + stats
+
+extern "C" int ffx_inject(ffx_ctx* c, int fault, ffx_replica* r, uint64_t arg) {
+  if (!c) return fail(FFX_EINVAL, "inject: null ctx");
+  DeviceGuard g(c->device);
+  switch (fault) {
+    case FFX_FAULT_POISON_STATE:
+      for (const auto& reg : c->regions)
+        if (reg.unique) FFX_CUDA(launch_fill(reg.dev, reg.bytes, 0xDEADBEEFu, nullptr));
+      FFX_CUDA(cudaDeviceSynchronize());
+      return FFX_OK;
+    case FFX_FAULT_CORRUPT_REPLICA: {
+      if (!r) return fail(FFX_EINVAL, "inject: replica required");
+      const uint32_t slot = static_cast<uint32_t>(arg >> 48);
+      const uint64_t off = arg & ((1ull << 48) - 1);
+      if (slot >= r->versions) return fail(FFX_ERANGE, "inject: slot %u", slot);
+      SlotMeta m;
+      int st = read_meta(r, slot, &m);
+      if (st) return st;
+      // logical offset -> physical (regions are 256-byte aligned in the slot)
+      uint64_t phys = 0, logical = off;
+      uint32_t i = 0;
+      for (; i < m.num_regions; ++i) {
+        if (logical < m.region_bytes[i]) break;
+        logical -= m.region_bytes[i];
+        phys = align_up(phys + m.region_bytes[i], kRegionAlign);
+      }
+      if (i >= m.num_regions) return fail(FFX_ERANGE, "inject: offset %llu beyond payload",
+                                          (unsigned long long)off);
+      FFX_CUDA(launch_xor_byte(r->payload(slot) + phys + logical, 0x01, nullptr));
+      FFX_CUDA(cudaDeviceSynchronize());
+      return FFX_OK;
+    }
+    case FFX_FAULT_TEAR_SLOT: {
+      if (!r) return fail(FFX_EINVAL, "inject: replica required");
+      if (arg >= r->versions) return fail(FFX_ERANGE, "inject: slot %llu", (unsigned long long)arg);
+      const uint32_t st = kSlotWriting;
+      FFX_CUDA(cudaMemcpy(r->slot(static_cast<uint32_t>(arg)) + offsetof(SlotMeta, state), &st, 4,
+                          cudaMemcpyHostToDevice));
+      r->cache[arg].state = kSlotWriting;
+      return FFX_OK;
+    }
+    case FFX_FAULT_CORRUPT_SUMS: {
+      if (!r) return fail(FFX_EINVAL, "inject: replica required");
+      const uint32_t slot = static_cast<uint32_t>(arg >> 48);
+      const uint64_t idx = arg & ((1ull << 48) - 1);
+      if (slot >= r->versions || idx >= r->layout.table_cap)
+        return fail(FFX_ERANGE, "inject: slot/index out of range");
+      FFX_CUDA(launch_xor_byte(reinterpret_cast<uint8_t*>(r->sums(slot) + idx), 0x80, nullptr));
+      FFX_CUDA(cudaDeviceSynchronize());
+      return FFX_OK;
+    }
+  }
+  return fail(FFX_EINVAL, "inject: unknown fault %d", fault);
+}
+
+extern "C" int ffx_get_stats(ffx_ctx* c, ffx_stats* out) {
+  if (!c || !out) return fail(FFX_EINVAL, "stats: null argument");
+  *out = c->stats;
+  return FFX_OK;
+}

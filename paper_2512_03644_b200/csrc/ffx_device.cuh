@@ -1,0 +1,76 @@
+// ffx_device.cuh -- device-side arithmetic shared by the ffx kernels.
+//
+// FNV-1a-64 (reference hash.cpp:102-110) and the splitmix64 finaliser
+// (reference evolution.cpp:43-48), restated for 32-bit integer datapaths.
+#pragma once
+
+#include <cstdint>
+
+namespace ffx {
+
+constexpr uint64_t kFnvBasis = 0xcbf29ce484222325ull;  // hash.cpp:104
+constexpr uint64_t kFnvPrime = 0x100000001b3ull;       // hash.cpp:107 (= 2^40 + 0x1b3)
+constexpr uint32_t kFnvQ = 0x1b3u;
+constexpr uint64_t kGolden = 0x9E3779B97F4A7C15ull;    // evolution.cpp:44, :76
+
+// FNV-1a-64 state split in 32-bit halves.  With h = hi:lo and x = lo ^ b,
+//   (h ^ b) * (2^40 + Q) mod 2^64  =  hi*Q*2^32 + x*2^40 + x*Q
+// so lo' = lo32(x*Q) and hi' = hi*Q + hi32(x*Q) + (x << 8): one wide
+// multiply, one multiply-add and one shift-add per byte.
+struct Fnv {
+  uint32_t lo, hi;
+
+  __device__ __forceinline__ void init() {
+    lo = static_cast<uint32_t>(kFnvBasis);
+    hi = static_cast<uint32_t>(kFnvBasis >> 32);
+  }
+  __device__ __forceinline__ void set(uint64_t h) {
+    lo = static_cast<uint32_t>(h);
+    hi = static_cast<uint32_t>(h >> 32);
+  }
+  __device__ __forceinline__ uint64_t value() const {
+    return (static_cast<uint64_t>(hi) << 32) | lo;
+  }
+  // Written as mul.lo/mul.hi/mad so ptxas folds hi32(x*Q) into the hi*Q
+  // multiply-add and splits the (x << 8) add between LEA (ALU pipe) and IMAD
+  // (FMA pipe): ~4.75 issue slots per byte, balanced across the two pipes.
+  __device__ __forceinline__ void byte(uint32_t b) {
+    const uint32_t x = lo ^ b;
+    uint32_t plo, phi, t;
+    asm("mul.lo.u32 %0, %2, 0x1b3;\n\tmul.hi.u32 %1, %2, 0x1b3;" : "=r"(plo), "=r"(phi) : "r"(x));
+    asm("mad.lo.u32 %0, %1, 0x1b3, %2;" : "=r"(t) : "r"(hi), "r"(phi));
+    hi = t + (x << 8);
+    lo = plo;
+  }
+  // Four bytes of a little-endian word, in memory order.
+  __device__ __forceinline__ void word(uint32_t w) {
+    byte(w & 0xffu);
+    byte(__byte_perm(w, 0u, 0x4441));
+    byte(__byte_perm(w, 0u, 0x4442));
+    byte(w >> 24);
+  }
+  __device__ __forceinline__ void vec(const uint4& v) {
+    word(v.x);
+    word(v.y);
+    word(v.z);
+    word(v.w);
+  }
+};
+
+// evo::mix64 including its leading golden-ratio add (evolution.cpp:43-48).
+__device__ __forceinline__ uint64_t mix64(uint64_t x) {
+  x += kGolden;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+  return x ^ (x >> 31);
+}
+
+// Streaming global accesses: every payload byte is touched once per pass.
+__device__ __forceinline__ uint4 ld_stream(const void* p) {
+  return __ldcs(reinterpret_cast<const uint4*>(p));
+}
+__device__ __forceinline__ void st_stream(void* p, const uint4& v) {
+  __stcs(reinterpret_cast<uint4*>(p), v);
+}
+
+}  // namespace ffx

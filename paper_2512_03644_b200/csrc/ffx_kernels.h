@@ -1,0 +1,77 @@
+// ffx_kernels.h -- host-side launchers for the sm_100a kernels in
+// ffx_kernels.cu.  Internal to libffx.so; the public boundary is include/ffx.h.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "ffx_layout.h"
+
+namespace ffx {
+
+// One contiguous range moved and/or hashed slice by slice.  Slices restart at
+// every region: slice s of region r covers [s*S, min((s+1)*S, bytes)).
+struct SliceRegion {
+  const uint8_t* src;
+  uint8_t* dst;          // null in hash-only mode
+  uint64_t bytes;
+  uint64_t slice_base;   // first checksum-table index of this region
+  uint64_t group_base;   // first 32-slice warp task of this region
+};
+
+// Optional slot commit fused into the snapshot kernel: every CTA marks the
+// slot WRITING before its first payload store; the last CTA to finish writes
+// the final meta + SNP1 header and flips the state to COMMITTED.
+struct SlotCommit {
+  uint8_t* slot;             // slot base (peer-mapped or local); null = no commit
+  unsigned int* done;        // local completion counter (zero between launches)
+  uint32_t finalize;         // this launch is the last batch of the snapshot
+  uint32_t pad_;
+  uint64_t payload_off;      // SNP1 header lives at slot + payload_off - 32
+  uint64_t iteration, seq;
+  uint4 meta[kMetaBytes / 16];  // final SlotMeta image (state field = COMMITTED)
+  uint4 snp1[2];                // SNP1 header image
+};
+
+struct SliceJob {
+  SliceRegion reg[kMaxRegions];
+  uint32_t nregions;
+  uint32_t pad_;
+  uint64_t total_groups;
+  uint64_t group_lo, group_hi;  // warp tasks this launch covers (a scheduler batch)
+  uint64_t slice_bytes;
+  uint64_t* sums_out;             // may be null
+  const uint64_t* sums_expected;  // verify mode
+  const uint64_t* init_state;     // per-slice FNV start (null = offset basis)
+  unsigned long long* result;     // verify mode: [first bad slice, bad count]
+  SlotCommit commit;
+};
+
+enum class SliceMode { Hash, Copy, CopyVerify, HashVerify };
+
+// Fill job.reg[*].group_base / slice_base, job.total_groups and the group
+// range [0, total_groups).
+void finalize_job(SliceJob& job);
+// Launch with at most max_ctas CTAs (0 = occupancy-sized full grid).
+cudaError_t launch_slices(const SliceJob& job, SliceMode mode, bool commit, uint32_t max_ctas,
+                          cudaStream_t stream);
+
+cudaError_t launch_expand(uint8_t* dst, uint64_t fold, uint64_t bytes, const uint8_t* prefix32,
+                          cudaStream_t stream);
+// result[0] <- min offset of a byte != materialize(prefix, bytes); must be
+// initialised to UINT64_MAX by the caller.
+cudaError_t launch_blob_check(const uint8_t* blob, uint64_t bytes, unsigned long long* result,
+                              cudaStream_t stream);
+
+// Whole-buffer FNV-1a-64 continuing from `h0` (kFnvBasis for checksum64).
+// Uses a scratch allocation internally; synchronises `stream`.
+cudaError_t whole_fnv(const uint8_t* data, uint64_t len, uint64_t h0, uint64_t* out,
+                      cudaStream_t stream);
+
+cudaError_t launch_fill(uint8_t* dst, uint64_t bytes, uint32_t pattern, cudaStream_t stream);
+cudaError_t launch_xor_byte(uint8_t* dst, uint8_t mask, cudaStream_t stream);
+
+int sm_count();
+
+}  // namespace ffx

@@ -1,0 +1,614 @@
+"""ctypes binding of libffx.so (include/ffx.h) -- plumbing for tests and bench.
+
+The product is the C ABI and the C++ facade over it; this module only lets
+Python (pytest, bench.py, torch.distributed for handle exchange) drive it.
+Device memory comes from torch tensors; every byte of payload work runs in the
+sm_100a kernels.  Status codes map 1:1 onto the reference's exception types
+(ckpt.hpp:58-68, storage.hpp:55-57), mirrored here as Python exceptions with
+the reference's names.
+
+There is deliberately no CPU fallback: importing this module without the
+built library raises immediately.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+from typing import Optional, Sequence
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libffx.so")
+ABI_VERSION = 1
+HANDLE_BYTES = 256
+MAX_REGIONS = 16
+
+# status codes (ffx.h)
+OK, ECONFIG, EVERSION, ERESTORE, ECORRUPT, EINVAL, ERANGE, ECUDA, ENOMEM, ESTATE = range(10)
+
+# region kinds
+REGION_MASTER, REGION_ADAM_M, REGION_ADAM_V, REGION_PARAMS, REGION_CURSOR, REGION_RNG, REGION_BLOB = range(7)
+# faults
+FAULT_POISON_STATE, FAULT_CORRUPT_REPLICA, FAULT_TEAR_SLOT, FAULT_CORRUPT_SUMS = range(4)
+SLOT_EMPTY, SLOT_WRITING, SLOT_COMMITTED = 0, 1, 2
+U64_MAX = (1 << 64) - 1
+
+
+class FfxError(RuntimeError):
+    status = -1
+
+
+class ConfigError(FfxError):       # ckpt::ConfigError (ckpt.hpp:58-60)
+    status = ECONFIG
+
+
+class VersionError(FfxError):      # ckpt::VersionError (ckpt.hpp:62-64)
+    status = EVERSION
+
+
+class RestoreError(FfxError):      # ckpt::RestoreError (ckpt.hpp:66-68)
+    status = ERESTORE
+
+
+class CorruptSnapshot(FfxError):   # store::CorruptSnapshot (storage.hpp:55-57)
+    status = ECORRUPT
+
+
+class InvalidArgument(FfxError, ValueError):  # std::invalid_argument
+    status = EINVAL
+
+
+class OutOfRange(FfxError, IndexError):       # std::out_of_range
+    status = ERANGE
+
+
+class CudaError(FfxError):
+    status = ECUDA
+
+
+class OutOfMemory(FfxError, MemoryError):
+    status = ENOMEM
+
+
+class StateError(FfxError):
+    status = ESTATE
+
+
+_EXC = {c.status: c for c in (ConfigError, VersionError, RestoreError, CorruptSnapshot,
+                              InvalidArgument, OutOfRange, CudaError, OutOfMemory, StateError)}
+
+
+class Role(ctypes.Structure):
+    _fields_ = [("dp", ctypes.c_uint16), ("pp", ctypes.c_uint16), ("tp", ctypes.c_uint16)]
+
+    def __repr__(self):
+        return "d%dp%dt%d" % (self.dp, self.pp, self.tp)
+
+    def __eq__(self, o):
+        return isinstance(o, Role) and (self.dp, self.pp, self.tp) == (o.dp, o.pp, o.tp)
+
+    def __hash__(self):
+        return hash((self.dp, self.pp, self.tp))
+
+    def tuple(self):
+        return (self.dp, self.pp, self.tp)
+
+
+class ClusterSpec(ctypes.Structure):
+    _fields_ = [("num_nodes", ctypes.c_uint32), ("gpus_per_node", ctypes.c_uint32),
+                ("data_parallel", ctypes.c_uint32), ("pipeline_parallel", ctypes.c_uint32),
+                ("tensor_parallel", ctypes.c_uint32), ("distributed_optimizer", ctypes.c_uint32),
+                ("params_per_device", ctypes.c_uint64)]
+
+
+def make_spec(d=1, p=1, t=1, phi=1_000_000_000, distributed=False, num_nodes=None, gpus_per_node=None):
+    world = d * p * t
+    if gpus_per_node is None:
+        gpus_per_node = world if num_nodes is None else world // num_nodes
+    if num_nodes is None:
+        num_nodes = max(1, world // gpus_per_node)
+    return ClusterSpec(num_nodes, gpus_per_node, d, p, t, int(bool(distributed)), phi)
+
+
+class UniquenessPlan(ctypes.Structure):
+    _fields_ = [("weights_redundant", ctypes.c_uint32), ("optimizer_redundant", ctypes.c_uint32),
+                ("unique_bytes_per_device", ctypes.c_uint64)]
+
+
+class BlobInfo(ctypes.Structure):
+    _fields_ = [("role", Role), ("kind", ctypes.c_uint8), ("pad_", ctypes.c_uint8 * 1),
+                ("payload_len", ctypes.c_uint32), ("iteration", ctypes.c_uint64),
+                ("checksum", ctypes.c_uint64)]
+
+
+class PlanInfo(ctypes.Structure):
+    _fields_ = [("razor", UniquenessPlan), ("registered_unique_bytes", ctypes.c_uint64),
+                ("registered_redundant_bytes", ctypes.c_uint64), ("slice_bytes", ctypes.c_uint64),
+                ("num_slices", ctypes.c_uint64), ("num_regions", ctypes.c_uint32),
+                ("num_unique_regions", ctypes.c_uint32)]
+
+
+class SlotInfo(ctypes.Structure):
+    _fields_ = [("state", ctypes.c_uint32), ("num_regions", ctypes.c_uint32), ("role", Role),
+                ("kind", ctypes.c_uint8), ("whole_checksum_valid", ctypes.c_uint8),
+                ("iteration", ctypes.c_uint64), ("payload_len", ctypes.c_uint64),
+                ("slice_bytes", ctypes.c_uint64), ("num_slices", ctypes.c_uint64),
+                ("whole_checksum", ctypes.c_uint64), ("seq", ctypes.c_uint64)]
+
+
+class SnapshotOpts(ctypes.Structure):
+    _fields_ = [("max_ctas", ctypes.c_uint32), ("batches", ctypes.c_uint32),
+                ("gate_events", ctypes.c_void_p), ("verify_on_store", ctypes.c_uint32),
+                ("weights_kind", ctypes.c_uint32)]
+
+
+class RecoverReport(ctypes.Structure):
+    _fields_ = [("bytes", ctypes.c_uint64), ("first_bad_slice", ctypes.c_uint64),
+                ("bad_slices", ctypes.c_uint64), ("slot", ctypes.c_uint32), ("pad_", ctypes.c_uint32),
+                ("seconds", ctypes.c_double)]
+
+
+class Stats(ctypes.Structure):
+    _fields_ = [("snapshots", ctypes.c_uint64), ("snapshot_bytes", ctypes.c_uint64),
+                ("recoveries", ctypes.c_uint64), ("recovered_bytes", ctypes.c_uint64),
+                ("verify_failures", ctypes.c_uint64), ("kernel_launches", ctypes.c_uint64)]
+
+
+class Forward(ctypes.Structure):
+    _fields_ = [("origin", Role), ("pad_", ctypes.c_uint16), ("holder_node", ctypes.c_uint32),
+                ("dest_node", ctypes.c_uint32), ("holder_dp", ctypes.c_uint32)]
+
+
+class RedundantSource(ctypes.Structure):
+    _fields_ = [("target", Role), ("source", Role)]
+
+
+class RecoveryPlanC(ctypes.Structure):
+    _fields_ = [("kind", ctypes.c_uint32), ("capacity", ctypes.c_uint32),
+                ("resume_iteration", ctypes.c_uint64),
+                ("failed_pods", ctypes.POINTER(ctypes.c_uint32)),
+                ("failed_roles", ctypes.POINTER(Role)),
+                ("lazy_backup_targets", ctypes.POINTER(Role)),
+                ("forwards", ctypes.POINTER(Forward)),
+                ("redundant_from", ctypes.POINTER(RedundantSource)),
+                ("n_failed_pods", ctypes.c_uint32), ("n_failed_roles", ctypes.c_uint32),
+                ("n_lazy", ctypes.c_uint32), ("n_forwards", ctypes.c_uint32),
+                ("n_redundant", ctypes.c_uint32)]
+
+
+_P = ctypes.c_void_p
+_U64 = ctypes.c_uint64
+_U32 = ctypes.c_uint32
+_I = ctypes.c_int
+_U8P = ctypes.c_char_p
+
+# name -> (restype, argtypes)
+SIGNATURES = {
+    "ffx_status_str": (ctypes.c_char_p, [_I]),
+    "ffx_last_error": (ctypes.c_char_p, []),
+    "ffx_abi_version": (_I, []),
+    "ffx_role_of": (_I, [ctypes.POINTER(ClusterSpec), _U32, ctypes.POINTER(Role)]),
+    "ffx_index_of": (_I, [ctypes.POINTER(ClusterSpec), Role, ctypes.POINTER(_U32)]),
+    "ffx_node_of": (_I, [ctypes.POINTER(ClusterSpec), Role, ctypes.POINTER(_U32)]),
+    "ffx_dp_neighbor": (_I, [ctypes.POINTER(ClusterSpec), Role, ctypes.POINTER(Role)]),
+    "ffx_dp_predecessor": (_I, [ctypes.POINTER(ClusterSpec), Role, ctypes.POINTER(Role)]),
+    "ffx_plan_recovery": (_I, [ctypes.POINTER(ClusterSpec), ctypes.POINTER(_U32), _U32,
+                               ctypes.POINTER(Role), _U32, _U64, _U64, _U32,
+                               ctypes.POINTER(RecoveryPlanC)]),
+    "ffx_razor": (_I, [ctypes.POINTER(ClusterSpec), ctypes.POINTER(UniquenessPlan)]),
+    "ffx_weights_bytes": (_U64, [ctypes.POINTER(ClusterSpec)]),
+    "ffx_optimizer_bytes": (_U64, [ctypes.POINTER(ClusterSpec)]),
+    "ffx_version_for_target": (_I, [_U64, _U64, ctypes.POINTER(_I)]),
+    "ffx_pack_header": (_I, [Role, _U64, ctypes.c_uint8, _U64, _U64, _P]),
+    "ffx_parse_header": (_I, [_P, _U64, ctypes.POINTER(BlobInfo)]),
+    "ffx_checksum64": (_I, [_P, _U64, ctypes.POINTER(_U64), _P]),
+    "ffx_slice_checksums": (_I, [_P, _U64, _U64, _P, _P]),
+    "ffx_copy_checksums": (_I, [_P, _P, _U64, _U64, _P, _P]),
+    "ffx_copy_verify": (_I, [_P, _P, _U64, _U64, _P, _P, _P]),
+    "ffx_expand": (_I, [_P, _P, _U64, _P]),
+    "ffx_materialize": (_I, [_P, _P, _U64, _P]),
+    "ffx_blob_check": (_I, [_P, _U64, ctypes.POINTER(_U64), _P]),
+    "ffx_open": (_I, [_I, ctypes.POINTER(ClusterSpec), Role, _U64, ctypes.POINTER(_P)]),
+    "ffx_close": (_I, [_P]),
+    "ffx_register_region": (_I, [_P, _I, _P, _U64, _I]),
+    "ffx_clear_regions": (_I, [_P]),
+    "ffx_plan": (_I, [_P, ctypes.POINTER(PlanInfo)]),
+    "ffx_replica_create": (_I, [_P, Role, _U64, _U32, ctypes.POINTER(_P)]),
+    "ffx_replica_export": (_I, [_P, _P]),
+    "ffx_replica_open": (_I, [_P, _P, ctypes.POINTER(_P)]),
+    "ffx_replica_destroy": (_I, [_P]),
+    "ffx_replica_slots": (_I, [_P, ctypes.POINTER(_U32)]),
+    "ffx_replica_slot_info": (_I, [_P, _U32, ctypes.POINTER(SlotInfo)]),
+    "ffx_replica_newest": (_I, [_P, ctypes.POINTER(_U64)]),
+    "ffx_replica_slot_ptrs": (_I, [_P, _U32, ctypes.POINTER(_P), ctypes.POINTER(_P)]),
+    "ffx_replica_clear": (_I, [_P]),
+    "ffx_replica_export_frame": (_I, [_P, _U64, _P, _U64, ctypes.POINTER(_U64), _P]),
+    "ffx_snapshot_target": (_I, [_P, _P]),
+    "ffx_snapshot": (_I, [_P, _U64, _P, ctypes.POINTER(SnapshotOpts)]),
+    "ffx_snapshot_read_sums": (_I, [_P, _P, _U64, ctypes.POINTER(_U64), _P]),
+    "ffx_recover": (_I, [_P, _P, _U64, _P, ctypes.POINTER(RecoverReport)]),
+    "ffx_recover_region": (_I, [_P, _U32, _P, _P, _P, ctypes.POINTER(RecoverReport)]),
+    "ffx_ipc_export": (_I, [_P, _P]),
+    "ffx_ipc_open": (_I, [_P, ctypes.POINTER(_P)]),
+    "ffx_ipc_close": (_I, [_P]),
+    "ffx_inject": (_I, [_P, _I, _P, _U64]),
+    "ffx_get_stats": (_I, [_P, ctypes.POINTER(Stats)]),
+}
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError("libffx.so not built at %s: run `python -c 'import __graft_entry__ as g; g.build()'`"
+                          " (no CPU fallback exists)" % LIB_PATH)
+    lib = ctypes.CDLL(LIB_PATH)
+    for name, (res, args) in SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    if lib.ffx_abi_version() != ABI_VERSION:
+        raise ImportError("libffx ABI %d != %d" % (lib.ffx_abi_version(), ABI_VERSION))
+    return lib
+
+
+lib = _load()
+
+
+def check(status: int, what: str = ""):
+    if status != OK:
+        msg = lib.ffx_last_error().decode(errors="replace")
+        raise _EXC.get(status, FfxError)("%s: %s" % (what or lib.ffx_status_str(status).decode(), msg))
+
+
+def _stream_ptr(stream) -> Optional[int]:
+    if stream is None:
+        return None
+    if isinstance(stream, int):
+        return stream
+    return stream.cuda_stream  # torch.cuda.Stream
+
+
+def _ptr(t) -> int:
+    if t is None:
+        return 0
+    if isinstance(t, int):
+        return t
+    return t.data_ptr()
+
+
+# ---- host-side functions (no GPU needed) -----------------------------------
+
+def razor(spec: ClusterSpec) -> UniquenessPlan:
+    p = UniquenessPlan()
+    check(lib.ffx_razor(ctypes.byref(spec), ctypes.byref(p)), "razor")
+    return p
+
+
+def weights_bytes(spec: ClusterSpec) -> int:
+    return lib.ffx_weights_bytes(ctypes.byref(spec))
+
+
+def optimizer_bytes(spec: ClusterSpec) -> int:
+    return lib.ffx_optimizer_bytes(ctypes.byref(spec))
+
+
+def version_for_target(held: int, target: int) -> int:
+    out = ctypes.c_int()
+    check(lib.ffx_version_for_target(held, target, ctypes.byref(out)), "version_for_target")
+    return out.value
+
+
+def role_of(spec, idx) -> Role:
+    r = Role()
+    check(lib.ffx_role_of(ctypes.byref(spec), idx, ctypes.byref(r)), "role_of")
+    return r
+
+
+def index_of(spec, role) -> int:
+    o = ctypes.c_uint32()
+    check(lib.ffx_index_of(ctypes.byref(spec), role, ctypes.byref(o)), "index_of")
+    return o.value
+
+
+def node_of(spec, role) -> int:
+    o = ctypes.c_uint32()
+    check(lib.ffx_node_of(ctypes.byref(spec), role, ctypes.byref(o)), "node_of")
+    return o.value
+
+
+def dp_neighbor(spec, role) -> Role:
+    r = Role()
+    check(lib.ffx_dp_neighbor(ctypes.byref(spec), role, ctypes.byref(r)), "dp_neighbor")
+    return r
+
+
+def dp_predecessor(spec, role) -> Role:
+    r = Role()
+    check(lib.ffx_dp_predecessor(ctypes.byref(spec), role, ctypes.byref(r)), "dp_predecessor")
+    return r
+
+
+def pack_header(role: Role, iteration: int, kind: int, length: int, checksum: int) -> bytes:
+    out = ctypes.create_string_buffer(32)
+    check(lib.ffx_pack_header(role, iteration, kind, length, checksum, out), "pack_header")
+    return out.raw
+
+
+def parse_header(header: bytes, framed_len: int = 0) -> BlobInfo:
+    info = BlobInfo()
+    buf = ctypes.create_string_buffer(bytes(header[:32]).ljust(32, b"\0"), 32)
+    check(lib.ffx_parse_header(buf, framed_len, ctypes.byref(info)), "parse_header")
+    return info
+
+
+@dataclass
+class RecoveryPlan:
+    kind: str
+    resume_iteration: int
+    failed_pods: list
+    failed_roles: list
+    lazy_backup_targets: list
+    forwards: list       # (origin Role, holder_node, dest_node, holder_dp)
+    redundant_from: list  # (target Role, source Role)
+
+
+def plan_recovery(spec, failed_pods: Sequence[int], failed_roles: Sequence, global_consistent: int,
+                  latest_fallback_round: int, replicas: int = 1) -> RecoveryPlan:
+    cap = max(spec.num_nodes * spec.gpus_per_node, len(failed_roles) + 1, 1) + len(failed_pods) * spec.gpus_per_node
+    pods = (ctypes.c_uint32 * cap)()
+    roles_out = (Role * cap)()
+    lazy = (Role * cap)()
+    fwd = (Forward * cap)()
+    red = (RedundantSource * cap)()
+    p = RecoveryPlanC()
+    p.capacity = cap
+    p.failed_pods = pods
+    p.failed_roles = roles_out
+    p.lazy_backup_targets = lazy
+    p.forwards = fwd
+    p.redundant_from = red
+    in_pods = (ctypes.c_uint32 * max(1, len(failed_pods)))(*failed_pods)
+    rl = [r if isinstance(r, Role) else Role(*r) for r in failed_roles]
+    in_roles = (Role * max(1, len(rl)))(*rl)
+    check(lib.ffx_plan_recovery(ctypes.byref(spec), in_pods, len(failed_pods), in_roles, len(rl),
+                                global_consistent, latest_fallback_round, replicas, ctypes.byref(p)),
+          "plan_recovery")
+    cp = lambda r: Role(r.dp, r.pp, r.tp)
+    return RecoveryPlan(
+        kind="neighbor" if p.kind == 0 else "fallback",
+        resume_iteration=p.resume_iteration,
+        failed_pods=[pods[i] for i in range(p.n_failed_pods)],
+        failed_roles=[cp(roles_out[i]) for i in range(p.n_failed_roles)],
+        lazy_backup_targets=[cp(lazy[i]) for i in range(p.n_lazy)],
+        forwards=[(cp(fwd[i].origin), fwd[i].holder_node, fwd[i].dest_node, fwd[i].holder_dp)
+                  for i in range(p.n_forwards)],
+        redundant_from=[(cp(red[i].target), cp(red[i].source)) for i in range(p.n_redundant)],
+    )
+
+
+# ---- device primitives ------------------------------------------------------
+
+def checksum64(dev_tensor, nbytes: Optional[int] = None, stream=None) -> int:
+    n = dev_tensor.numel() * dev_tensor.element_size() if nbytes is None else nbytes
+    out = ctypes.c_uint64()
+    check(lib.ffx_checksum64(_ptr(dev_tensor), n, ctypes.byref(out), _stream_ptr(stream)), "checksum64")
+    return out.value
+
+
+def slice_checksums(dev_tensor, slice_bytes: int, out_tensor, nbytes=None, stream=None):
+    n = dev_tensor.numel() * dev_tensor.element_size() if nbytes is None else nbytes
+    check(lib.ffx_slice_checksums(_ptr(dev_tensor), n, slice_bytes, _ptr(out_tensor),
+                                  _stream_ptr(stream)), "slice_checksums")
+
+
+def copy_checksums(dst, src, slice_bytes: int, out_tensor, nbytes=None, stream=None):
+    n = src.numel() * src.element_size() if nbytes is None else nbytes
+    check(lib.ffx_copy_checksums(_ptr(dst), _ptr(src), n, slice_bytes, _ptr(out_tensor),
+                                 _stream_ptr(stream)), "copy_checksums")
+
+
+def copy_verify(dst, src, slice_bytes: int, expected, result, nbytes=None, stream=None):
+    n = src.numel() * src.element_size() if nbytes is None else nbytes
+    check(lib.ffx_copy_verify(_ptr(dst), _ptr(src), n, slice_bytes, _ptr(expected), _ptr(result),
+                              _stream_ptr(stream)), "copy_verify")
+
+
+def materialize(dst, digest: bytes, nbytes: Optional[int] = None, stream=None):
+    n = dst.numel() * dst.element_size() if nbytes is None else nbytes
+    check(lib.ffx_materialize(_ptr(dst), bytes(digest), n, _stream_ptr(stream)), "materialize")
+
+
+def expand(dst, digest: bytes, nbytes: Optional[int] = None, stream=None):
+    n = dst.numel() * dst.element_size() if nbytes is None else nbytes
+    check(lib.ffx_expand(_ptr(dst), bytes(digest), n, _stream_ptr(stream)), "expand")
+
+
+def blob_first_bad(dev, nbytes: Optional[int] = None, stream=None) -> int:
+    n = dev.numel() * dev.element_size() if nbytes is None else nbytes
+    out = ctypes.c_uint64()
+    check(lib.ffx_blob_check(_ptr(dev), n, ctypes.byref(out), _stream_ptr(stream)), "blob_check")
+    return out.value
+
+
+def blob_is_sound(dev, nbytes=None, stream=None) -> bool:
+    n = dev.numel() * dev.element_size() if nbytes is None else nbytes
+    return n >= 32 and blob_first_bad(dev, n, stream) == U64_MAX
+
+
+def ipc_export(ptr: int) -> bytes:
+    h = ctypes.create_string_buffer(64)
+    check(lib.ffx_ipc_export(ptr, h), "ipc_export")
+    return h.raw
+
+
+def ipc_open(handle: bytes) -> int:
+    p = ctypes.c_void_p()
+    check(lib.ffx_ipc_open(ctypes.create_string_buffer(bytes(handle), 64), ctypes.byref(p)), "ipc_open")
+    return p.value
+
+
+def ipc_close(ptr: int):
+    check(lib.ffx_ipc_close(ptr), "ipc_close")
+
+
+# ---- context / replica objects -------------------------------------------------
+
+class Replica:
+    """A neighbour replica (holder-side NeighborBuffer, ckpt.hpp:105-120)."""
+
+    def __init__(self, handle_ptr: int, owner: "Context"):
+        self._h = ctypes.c_void_p(handle_ptr)
+        self._owner = owner
+
+    @property
+    def ptr(self):
+        return self._h
+
+    def export(self) -> bytes:
+        buf = ctypes.create_string_buffer(HANDLE_BYTES)
+        check(lib.ffx_replica_export(self._h, buf), "replica_export")
+        return buf.raw
+
+    def versions(self) -> int:
+        v = ctypes.c_uint32()
+        check(lib.ffx_replica_slots(self._h, ctypes.byref(v)), "replica_slots")
+        return v.value
+
+    def slot_info(self, slot: int) -> SlotInfo:
+        s = SlotInfo()
+        check(lib.ffx_replica_slot_info(self._h, slot, ctypes.byref(s)), "slot_info")
+        return s
+
+    def newest(self) -> Optional[int]:
+        it = ctypes.c_uint64()
+        st = lib.ffx_replica_newest(self._h, ctypes.byref(it))
+        if st == ERESTORE:
+            return None
+        check(st, "replica_newest")
+        return it.value
+
+    def held(self) -> dict:
+        """{iteration: slot} for committed slots."""
+        out = {}
+        for v in range(self.versions()):
+            s = self.slot_info(v)
+            if s.state == SLOT_COMMITTED:
+                out[s.iteration] = v
+        return out
+
+    def slot_ptrs(self, slot: int):
+        pay, sums = ctypes.c_void_p(), ctypes.c_void_p()
+        check(lib.ffx_replica_slot_ptrs(self._h, slot, ctypes.byref(pay), ctypes.byref(sums)), "slot_ptrs")
+        return pay.value, sums.value
+
+    def clear(self):
+        check(lib.ffx_replica_clear(self._h), "replica_clear")
+
+    def export_frame(self, iteration: int, stream=None) -> bytes:
+        n = ctypes.c_uint64()
+        check(lib.ffx_replica_export_frame(self._h, iteration, None, 0, ctypes.byref(n),
+                                           _stream_ptr(stream)), "export_frame")
+        buf = ctypes.create_string_buffer(n.value)
+        check(lib.ffx_replica_export_frame(self._h, iteration, buf, n.value, ctypes.byref(n),
+                                           _stream_ptr(stream)), "export_frame")
+        return buf.raw
+
+    def destroy(self):
+        if self._h:
+            check(lib.ffx_replica_destroy(self._h), "replica_destroy")
+            self._h = ctypes.c_void_p(0)
+
+
+class Context:
+    """One rank's ffx context: state registry, snapshot issue, recovery."""
+
+    def __init__(self, device: int, spec: ClusterSpec, role, slice_bytes: int = 4096):
+        self.spec = spec
+        self.role = role if isinstance(role, Role) else Role(*role)
+        self.device = device
+        self._c = ctypes.c_void_p()
+        self._keep = []  # tensors whose memory is registered
+        check(lib.ffx_open(device, ctypes.byref(spec), self.role, slice_bytes, ctypes.byref(self._c)), "open")
+
+    @property
+    def ptr(self):
+        return self._c
+
+    def close(self):
+        if self._c:
+            check(lib.ffx_close(self._c), "close")
+            self._c = ctypes.c_void_p(0)
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    def register(self, kind: int, tensor, unique: bool = True, nbytes: Optional[int] = None):
+        n = tensor.numel() * tensor.element_size() if nbytes is None else nbytes
+        check(lib.ffx_register_region(self._c, kind, _ptr(tensor), n, int(unique)), "register_region")
+        self._keep.append(tensor)
+
+    def clear_regions(self):
+        check(lib.ffx_clear_regions(self._c), "clear_regions")
+        self._keep.clear()
+
+    def plan(self) -> PlanInfo:
+        p = PlanInfo()
+        check(lib.ffx_plan(self._c, ctypes.byref(p)), "plan")
+        return p
+
+    def create_replica(self, origin, capacity: int, versions: int = 2) -> Replica:
+        origin = origin if isinstance(origin, Role) else Role(*origin)
+        h = ctypes.c_void_p()
+        check(lib.ffx_replica_create(self._c, origin, capacity, versions, ctypes.byref(h)), "replica_create")
+        return Replica(h.value, self)
+
+    def open_replica(self, handle: bytes) -> Replica:
+        h = ctypes.c_void_p()
+        check(lib.ffx_replica_open(self._c, ctypes.create_string_buffer(bytes(handle), HANDLE_BYTES),
+                                   ctypes.byref(h)), "replica_open")
+        return Replica(h.value, self)
+
+    def set_target(self, replica: Optional[Replica]):
+        check(lib.ffx_snapshot_target(self._c, replica.ptr if replica else None), "snapshot_target")
+
+    def snapshot(self, iteration: int, stream=None, max_ctas: int = 0, batches: int = 1,
+                 gate_events=None, verify_on_store: bool = False, weights_kind: bool = False):
+        o = SnapshotOpts()
+        o.max_ctas = max_ctas
+        o.batches = batches
+        o.verify_on_store = int(verify_on_store)
+        o.weights_kind = int(weights_kind)
+        arr = None
+        if gate_events:
+            arr = (ctypes.c_void_p * len(gate_events))(*[e.cuda_event if hasattr(e, "cuda_event") else e
+                                                          for e in gate_events])
+            o.gate_events = ctypes.cast(arr, ctypes.c_void_p)
+        check(lib.ffx_snapshot(self._c, iteration, _stream_ptr(stream), ctypes.byref(o)), "snapshot")
+
+    def read_sums(self, host_tensor, stream=None) -> int:
+        """D2H of the last snapshot's checksum table into a (pinned) int64 tensor."""
+        n = ctypes.c_uint64()
+        check(lib.ffx_snapshot_read_sums(self._c, _ptr(host_tensor), host_tensor.numel(), ctypes.byref(n),
+                                         _stream_ptr(stream)), "snapshot_read_sums")
+        return n.value
+
+    def recover(self, replica: Replica, target: int, stream=None) -> RecoverReport:
+        rep = RecoverReport()
+        check(lib.ffx_recover(self._c, replica.ptr, target, _stream_ptr(stream), ctypes.byref(rep)), "recover")
+        return rep
+
+    def recover_region(self, index: int, peer_src: int, peer_sums: int, stream=None) -> RecoverReport:
+        rep = RecoverReport()
+        check(lib.ffx_recover_region(self._c, index, peer_src, peer_sums, _stream_ptr(stream),
+                                     ctypes.byref(rep)), "recover_region")
+        return rep
+
+    def inject(self, fault: int, replica: Optional[Replica] = None, arg: int = 0):
+        check(lib.ffx_inject(self._c, fault, replica.ptr if replica else None, arg), "inject")
+
+    def stats(self) -> Stats:
+        s = Stats()
+        check(lib.ffx_get_stats(self._c, ctypes.byref(s)), "stats")
+        return s

@@ -1,0 +1,309 @@
+"""GPU parity of the replica manager, snapshot and recovery (single process).
+
+Restates the hot-path cases of proj/tests/test_ckpt.cpp against the B200
+path: two-version retention and replace-in-place (:198-263), capacity
+ConfigError (:220-221), header-only frames (:222-226), SNP1 frame bytes
+(:50-72), and ring restore with its failure modes (:278-330) -- missing,
+stale, wrong origin, flipped byte -- plus the B200-specific faults (torn slot,
+corrupted checksum table).  Frames are compared byte for byte with the
+oracle's pack_blob; restored state with the oracle's materialize.
+"""
+import os
+
+import pytest
+
+import pyoracle as orc
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def ffx():
+    from paper_2512_03644_b200 import ffx as m
+    return m
+
+
+def host(t):
+    return bytes(t.cpu().numpy().tobytes())
+
+
+def spec2(ffx, phi=64, d=2):
+    return ffx.make_spec(d=d, phi=phi, distributed=True)
+
+
+def blob_for(ffx, dp, nbytes, seed=42):
+    d = orc.optimizer_init(seed, dp, 0, 0, True)
+    t = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+    ffx.materialize(t, d)
+    return t, orc.materialize(d, nbytes)
+
+
+def ring_pair(ffx, nbytes, slice_bytes=4096, versions=2):
+    """origin d1 snapshots into a replica held by d0's context (one GPU)."""
+    spec = spec2(ffx)
+    holder = ffx.Context(0, spec, (0, 0, 0), slice_bytes)
+    origin = ffx.Context(0, spec, (1, 0, 0), slice_bytes)
+    rep = holder.create_replica((1, 0, 0), max(nbytes, 1), versions)
+    view = origin.open_replica(rep.export())
+    origin.set_target(view)
+    return spec, holder, origin, rep, view
+
+
+def test_snapshot_roundtrip_frame_is_reference_bytes(ffx):
+    n = 100_003
+    spec, holder, origin, rep, view = ring_pair(ffx, n)
+    state, want = blob_for(ffx, 1, n)
+    origin.register(ffx.REGION_BLOB, state)
+    origin.snapshot(9)
+    torch.cuda.synchronize()
+    s = rep.slot_info(0)
+    assert s.state == ffx.SLOT_COMMITTED and s.iteration == 9 and s.payload_len == n
+    assert s.role.tuple() == (1, 0, 0) and s.kind == 1
+    pay, sums = rep.slot_ptrs(0)
+    # payload bytes and slice table
+    frame = rep.export_frame(9)
+    assert frame == orc.pack_blob((1, 0, 0), 9, 1, want)
+    assert rep.slot_info(0).whole_checksum == orc.fnv1a64(want)
+    # second export is served from the cached checksum
+    assert rep.export_frame(9) == frame
+
+
+def test_two_version_rule_and_replace_in_place(ffx):
+    # proj/tests/test_ckpt.cpp:198-216, :229-263
+    n = 8192
+    spec, holder, origin, rep, view = ring_pair(ffx, n)
+    state = torch.zeros(n, dtype=torch.uint8, device="cuda")
+    origin.register(ffx.REGION_BLOB, state)
+    payloads = {}
+    for it in (1, 2, 3, 4, 5):
+        state.fill_(it)
+        payloads[it] = bytes([it]) * n
+        origin.snapshot(it)
+    torch.cuda.synchronize()
+    assert rep.newest() == 5
+    assert sorted(rep.held()) == [4, 5]
+    assert rep.export_frame(4)[32:] == payloads[4]
+    with pytest.raises(ffx.RestoreError):
+        rep.export_frame(3)
+    slot5 = rep.held()[5]
+    state.fill_(55)
+    origin.snapshot(5)  # replace-in-place keeps iteration 4
+    torch.cuda.synchronize()
+    assert rep.held() == {4: 1 - slot5, 5: slot5}
+    assert rep.export_frame(5)[32:] == bytes([55]) * n
+    assert rep.export_frame(4)[32:] == payloads[4]
+
+
+def test_capacity_config_error(ffx):
+    # proj/tests/test_ckpt.cpp:220-221
+    spec, holder, origin, rep, view = ring_pair(ffx, 16)
+    big = torch.zeros(17, dtype=torch.uint8, device="cuda")
+    origin.register(ffx.REGION_BLOB, big)
+    with pytest.raises(ffx.ConfigError):
+        origin.snapshot(7)
+
+
+def test_header_only_snapshot(ffx):
+    # proj/tests/test_ckpt.cpp:222-226: a zero-byte plan produces header-only frames
+    spec = ffx.make_spec(d=2, phi=64, distributed=False)
+    holder = ffx.Context(0, spec, (0, 0, 0))
+    origin = ffx.Context(0, spec, (1, 0, 0))
+    rep = holder.create_replica((1, 0, 0), 0, 2)
+    origin.set_target(origin.open_replica(rep.export()))
+    origin.snapshot(1)
+    torch.cuda.synchronize()
+    fr = rep.export_frame(1)
+    assert fr == orc.pack_blob((1, 0, 0), 1, 1, b"")
+    assert len(fr) == 32
+
+
+def test_multi_region_state_roundtrip(ffx):
+    # fp32 master + Adam m/v shards + cursor + RNG state, ragged sizes
+    spec, holder, origin, rep, view = ring_pair(ffx, 1 << 20)
+    g = torch.Generator(device="cuda").manual_seed(1)
+    master = torch.randn(40_001, device="cuda", generator=g)
+    m = torch.randn(40_001, device="cuda", generator=g)
+    v = torch.rand(40_001, device="cuda", generator=g)
+    cursor = torch.tensor([1234, 5678], dtype=torch.int64, device="cuda")
+    rng = torch.randint(0, 2**31, (4,), dtype=torch.int32, device="cuda", generator=g)
+    regions = [(ffx.REGION_MASTER, master), (ffx.REGION_ADAM_M, m), (ffx.REGION_ADAM_V, v),
+               (ffx.REGION_CURSOR, cursor), (ffx.REGION_RNG, rng)]
+    for k, t in regions:
+        origin.register(k, t)
+    weights = torch.randn(1000, device="cuda", generator=g).to(torch.bfloat16)
+    origin.register(ffx.REGION_PARAMS, weights, unique=False)
+    plan = origin.plan()
+    concat = b"".join(host(t) for _, t in regions)
+    assert plan.registered_unique_bytes == len(concat)
+    assert plan.registered_redundant_bytes == 2000
+    assert plan.num_unique_regions == 5 and plan.num_regions == 6
+    origin.snapshot(3)
+    torch.cuda.synchronize()
+    assert rep.export_frame(3) == orc.pack_blob((1, 0, 0), 3, 1, concat)
+    saved = [t.clone() for _, t in regions]
+    origin.inject(ffx.FAULT_POISON_STATE)
+    assert not torch.equal(master, saved[0])
+    rpt = origin.recover(view, 3)
+    assert rpt.bad_slices == 0 and rpt.bytes == len(concat)
+    for (_, t), s in zip(regions, saved):
+        assert torch.equal(t, s)
+
+
+def test_recover_bit_exact_and_failure_modes(ffx):
+    # proj/tests/test_ckpt.cpp:278-330
+    n = 3 * (1 << 20) + 1001
+    spec, holder, origin, rep, view = ring_pair(ffx, n)
+    state, want = blob_for(ffx, 1, n)
+    origin.register(ffx.REGION_BLOB, state)
+    origin.snapshot(8)
+    origin.snapshot(9)
+    torch.cuda.synchronize()
+    origin.inject(ffx.FAULT_POISON_STATE)
+    assert not ffx.blob_is_sound(state)
+    rpt = origin.recover(view, 9)
+    assert host(state) == want and ffx.blob_is_sound(state)
+    assert rpt.bytes == n and rpt.bad_slices == 0 and rpt.seconds > 0
+
+    # missing iteration
+    with pytest.raises(ffx.RestoreError, match="missing"):
+        origin.recover(view, 7)
+    # wrong worker: a context for d0 must not accept d1's snapshot
+    other = ffx.Context(0, spec, (0, 0, 0))
+    t0 = torch.empty(n, dtype=torch.uint8, device="cuda")
+    other.register(ffx.REGION_BLOB, t0)
+    with pytest.raises(ffx.RestoreError, match="d1p0t0"):
+        other.recover(view, 9)
+    # layout mismatch
+    other2 = ffx.Context(0, spec, (1, 0, 0))
+    t1 = torch.empty(n - 1, dtype=torch.uint8, device="cuda")
+    other2.register(ffx.REGION_BLOB, t1)
+    with pytest.raises(ffx.RestoreError):
+        other2.recover(view, 9)
+    # flipped payload byte -> the slice that holds it is named
+    slot9 = rep.held()[9]
+    off = 4096 * 300 + 17
+    origin.inject(ffx.FAULT_CORRUPT_REPLICA, view, (slot9 << 48) | off)
+    with pytest.raises(ffx.RestoreError, match="checksum mismatch"):
+        origin.recover(view, 9)
+    origin.inject(ffx.FAULT_CORRUPT_REPLICA, view, (slot9 << 48) | off)  # flip back
+    origin.recover(view, 9)
+    # corrupted checksum table entry
+    origin.inject(ffx.FAULT_CORRUPT_SUMS, view, (slot9 << 48) | 5)
+    with pytest.raises(ffx.RestoreError):
+        origin.recover(view, 9)
+    origin.inject(ffx.FAULT_CORRUPT_SUMS, view, (slot9 << 48) | 5)
+    # torn slot (origin died mid-snapshot): iteration 8 still recoverable
+    slot8 = rep.held()[8]
+    origin.inject(ffx.FAULT_TEAR_SLOT, view, slot9)
+    with pytest.raises(ffx.RestoreError, match="torn"):
+        origin.recover(view, 9)
+    assert rep.newest() == 8
+    origin.recover(view, 8)
+    assert ffx.blob_is_sound(state)
+
+
+def test_recover_reports_first_bad_slice(ffx):
+    n = 1 << 20
+    spec, holder, origin, rep, view = ring_pair(ffx, n, slice_bytes=4096)
+    state, want = blob_for(ffx, 1, n)
+    origin.register(ffx.REGION_BLOB, state)
+    origin.snapshot(1)
+    torch.cuda.synchronize()
+    origin.inject(ffx.FAULT_CORRUPT_REPLICA, view, (0 << 48) | (4096 * 100 + 1))
+    origin.inject(ffx.FAULT_CORRUPT_REPLICA, view, (0 << 48) | (4096 * 40))
+    rep_c = ffx.RecoverReport()
+    st = ffx.lib.ffx_recover(origin.ptr, view.ptr, 1, None, ffx.ctypes.byref(rep_c))
+    assert st == ffx.ERESTORE
+    assert rep_c.first_bad_slice == 40 and rep_c.bad_slices == 2
+
+
+def test_batched_gated_snapshot_equals_single(ffx):
+    n = (1 << 22) + 77
+    spec, holder, origin, rep, view = ring_pair(ffx, n)
+    state, want = blob_for(ffx, 1, n)
+    origin.register(ffx.REGION_BLOB, state)
+    side = torch.cuda.Stream(priority=0)
+    low = torch.cuda.Stream(priority=0)
+    events = [torch.cuda.Event() for _ in range(4)]
+    for e in events:
+        e.record(side)
+    origin.snapshot(21, stream=low, batches=4, gate_events=events, max_ctas=16)
+    low.synchronize()
+    assert rep.export_frame(21) == orc.pack_blob((1, 0, 0), 21, 1, want)
+
+
+def test_verify_on_store(ffx):
+    n = 500_000
+    spec, holder, origin, rep, view = ring_pair(ffx, n)
+    state, want = blob_for(ffx, 1, n)
+    origin.register(ffx.REGION_BLOB, state)
+    origin.snapshot(2, verify_on_store=True)
+    assert origin.stats().verify_failures == 0
+
+
+def test_recover_redundant_region_from_peer(ffx):
+    # ckpt.cpp:150-152: weights come from a live DP peer, checksum-verified.
+    n = 2 * 50_000
+    spec = spec2(ffx)
+    peer_w = torch.randn(50_000, device="cuda").to(torch.bfloat16)
+    sums = torch.zeros((n + 4095) // 4096, dtype=torch.int64, device="cuda")
+    ffx.slice_checksums(peer_w, 4096, sums)
+    me = ffx.Context(0, spec, (1, 0, 0))
+    mine = torch.zeros_like(peer_w)
+    me.register(ffx.REGION_PARAMS, mine, unique=False)
+    r = me.recover_region(0, peer_w.data_ptr(), sums.data_ptr())
+    assert torch.equal(mine, peer_w) and r.bytes == n
+    peer_w.view(torch.uint8)[12345] ^= 1
+    with pytest.raises(ffx.RestoreError):
+        me.recover_region(0, peer_w.data_ptr(), sums.data_ptr())
+
+
+def test_stats_count_backup_bytes(ffx):
+    n = 65536
+    spec, holder, origin, rep, view = ring_pair(ffx, n)
+    state, _ = blob_for(ffx, 1, n)
+    origin.register(ffx.REGION_BLOB, state)
+    for it in range(5):
+        origin.snapshot(it)
+    torch.cuda.synchronize()
+    s = origin.stats()
+    assert s.snapshots == 5 and s.snapshot_bytes == 5 * n
+
+
+@pytest.mark.skipif(os.environ.get("FFX_FULL_SIZE", "1") == "0", reason="full-size disabled")
+def test_full_size_gpt2xl_shard_roundtrip(ffx):
+    # BASELINE configs[1]: GPT-2 XL ZeRO-1 d=8 shard, N = ceil(12*1,557,611,200/8).
+    spec = ffx.make_spec(d=8, phi=1_557_611_200, distributed=True)
+    n = ffx.razor(spec).unique_bytes_per_device
+    assert n == 2_336_416_800
+    holder = ffx.Context(0, spec, (0, 0, 0))
+    origin = ffx.Context(0, spec, (7, 0, 0))
+    rep = holder.create_replica((7, 0, 0), n, 2)
+    view = origin.open_replica(rep.export())
+    origin.set_target(view)
+    d = orc.optimizer_init(42, 7, 0, 0, True)
+    state = torch.empty(n, dtype=torch.uint8, device="cuda")
+    ffx.materialize(state, d)
+    origin.register(ffx.REGION_BLOB, state)
+    origin.snapshot(10)
+    origin.snapshot(11)
+    torch.cuda.synchronize()
+    # size-independent properties: the restored blob is sound, and sampled
+    # slices (bytes and table entries) equal the oracle's.
+    pay, sums = rep.slot_ptrs(rep.held()[11])
+    nsl = (n + 4095) // 4096
+    table = torch.empty(nsl, dtype=torch.int64, device="cuda")
+    scratch = torch.empty((nsl * 8 + 4095) // 4096, dtype=torch.int64, device="cuda")
+    ffx.copy_checksums(table, sums, 4096, scratch, nbytes=nsl * 8)  # device copy of the table
+    tab = [v & ffx.U64_MAX for v in table.cpu().tolist()]
+    origin.inject(ffx.FAULT_POISON_STATE)
+    rpt = origin.recover(view, 11)
+    assert rpt.bad_slices == 0 and rpt.bytes == n
+    assert ffx.blob_is_sound(state)
+    for s in (0, 1, 12345, nsl // 2, nsl - 2, nsl - 1):
+        lo = s * 4096
+        ln = min(4096, n - lo)
+        want = orc.materialize_range(d, n, lo, ln)
+        assert host(state[lo:lo + ln]) == want
+        assert tab[s] == orc.fnv1a64(want)
