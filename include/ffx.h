@@ -168,6 +168,17 @@ int ffx_materialize(void* dst, const uint8_t digest[32], uint64_t bytes, void* s
  * first byte that differs from materialize(prefix), UINT64_MAX if sound. */
 int ffx_blob_check(const void* dev, uint64_t bytes, uint64_t* host_first_bad, void* stream);
 
+/* ---- buffer plumbing (for hosts without their own CUDA runtime, e.g. the
+ * C++ facade over the reference API) ---------------------------------------- */
+
+int ffx_device_alloc(int device, uint64_t bytes, void** dev);
+int ffx_device_free(int device, void* dev);
+/* cudaMemcpyAsync(kind = default) on `stream`; blocks when sync != 0. */
+int ffx_memcpy(void* dst, const void* src, uint64_t bytes, void* stream, int sync);
+/* *is_device = 1 when p is device (or managed) memory visible to CUDA. */
+int ffx_pointer_is_device(const void* p, int* is_device);
+int ffx_stream_sync(void* stream);
+
 /* ---- contexts and the state registry -------------------------------------- */
 
 typedef struct ffx_ctx ffx_ctx;

@@ -548,6 +548,54 @@ extern "C" int ffx_blob_check(const void* dev, uint64_t bytes, uint64_t* host_fi
 }
 
 // ---------------------------------------------------------------------------
+// buffer plumbing
+
+extern "C" int ffx_device_alloc(int device, uint64_t bytes, void** dev) {
+  if (!dev) return fail(FFX_EINVAL, "device_alloc: null out");
+  DeviceGuard g(device);
+  cudaError_t e = cudaMalloc(dev, bytes ? bytes : 1);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail(FFX_ENOMEM, "device_alloc(%llu): %s", (unsigned long long)bytes, cudaGetErrorString(e));
+  }
+  return FFX_OK;
+}
+
+extern "C" int ffx_device_free(int device, void* dev) {
+  if (!dev) return FFX_OK;
+  DeviceGuard g(device);
+  FFX_CUDA(cudaFree(dev));
+  return FFX_OK;
+}
+
+extern "C" int ffx_memcpy(void* dst, const void* src, uint64_t bytes, void* stream, int sync) {
+  if (!bytes) return FFX_OK;
+  if (!dst || !src) return fail(FFX_EINVAL, "memcpy: null pointer");
+  FFX_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, as_stream(stream)));
+  if (sync) FFX_CUDA(cudaStreamSynchronize(as_stream(stream)));
+  return FFX_OK;
+}
+
+extern "C" int ffx_pointer_is_device(const void* p, int* is_device) {
+  if (!is_device) return fail(FFX_EINVAL, "pointer_is_device: null out");
+  *is_device = 0;
+  if (!p) return FFX_OK;
+  cudaPointerAttributes a{};
+  cudaError_t e = cudaPointerGetAttributes(&a, p);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return FFX_OK;
+  }
+  *is_device = (a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged) ? 1 : 0;
+  return FFX_OK;
+}
+
+extern "C" int ffx_stream_sync(void* stream) {
+  FFX_CUDA(cudaStreamSynchronize(as_stream(stream)));
+  return FFX_OK;
+}
+
+// ---------------------------------------------------------------------------
 // context + registry
 
 extern "C" int ffx_open(int device, const ffx_cluster_spec* spec, ffx_role self,
@@ -958,6 +1006,7 @@ extern "C" int ffx_snapshot(ffx_ctx* c, uint64_t iteration, void* stream, const 
     job.reg[i] = SliceRegion{pm.regs[i]->dev, t->payload(slot) + pm.offs[i], pm.regs[i]->bytes, 0, 0};
   job.slice_bytes = c->slice_bytes;
   job.sums_out = t->sums(slot);
+  job.sched = c->done + 8;  // dynamic task counter (words 8-9 of the ctx scratch)
   finalize_job(job);
 
   SlotMeta m{};
@@ -1022,6 +1071,7 @@ extern "C" int ffx_snapshot(ffx_ctx* c, uint64_t iteration, void* stream, const 
     vj.sums_out = nullptr;
     vj.sums_expected = t->sums(slot);
     vj.result = c->result;
+    vj.sched = c->done + 12;
     vj.commit = SlotCommit{};
     FFX_CUDA(launch_slices(vj, SliceMode::HashVerify, false, opts.max_ctas, s));
     c->stats.kernel_launches++;
@@ -1093,6 +1143,7 @@ extern "C" int ffx_recover(ffx_ctx* c, ffx_replica* src, uint64_t target, void* 
   job.slice_bytes = m.slice_bytes;
   job.sums_expected = src->sums(R.slot);
   job.result = c->result;
+  job.sched = c->done + 12;
   finalize_job(job);
   const unsigned long long init[2] = {~0ull, 0ull};
   FFX_CUDA(cudaMemcpyAsync(c->result, init, sizeof init, cudaMemcpyHostToDevice, s));
@@ -1132,6 +1183,7 @@ extern "C" int ffx_recover_region(ffx_ctx* c, uint32_t idx, const void* peer_src
   SliceJob job = single_job(peer_src, reg.dev, reg.bytes, c->slice_bytes);
   job.sums_expected = peer_sums;
   job.result = c->result;
+  job.sched = c->done + 12;
   const unsigned long long init[2] = {~0ull, 0ull};
   FFX_CUDA(cudaMemcpyAsync(c->result, init, sizeof init, cudaMemcpyHostToDevice, s));
   FFX_CUDA(cudaEventRecord(c->ev0, s));

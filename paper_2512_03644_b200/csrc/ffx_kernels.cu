@@ -1,16 +1,12 @@
 // ffx_kernels.cu -- sm_100a kernels of the state-backup / recovery path.
 //
-//  slice_kernel   fused copy + per-slice FNV-1a-64 (+ verify, + slot commit):
-//                 the snapshot kernel (local or NVLink-peer destination) and
-//                 the recovery gather/verify kernel (peer source).
+//  (the snapshot / recovery slice kernel lives in ffx_slice.cu)
 //  expand_kernel  evo::expand / evo::materialize (evolution.cpp:71-97).
 //  check_kernel   evo::blob_is_sound (evolution.cpp:106-110).
 //  fnv_spec_kernel + helpers: whole-buffer checksum64 (hash.cpp:102-110) by
 //                 low-byte speculation and an affine combine.
 //
-// The path is HBM/NVLink-bound integer work: no tensor cores.  Global traffic
-// is 16-byte vectorised and fully coalesced; the byte-serial FNV chains run
-// one lane per slice out of a padded (conflict-free) shared-memory transpose.
+// HBM-bound integer work: 16-byte vectorised, coalesced, grid-stride.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -23,35 +19,20 @@ namespace ffx {
 
 namespace {
 
-constexpr int kThreads = 256;
-constexpr int kWarps = kThreads / 32;
-constexpr int kChunk = 128;  // bytes of each slice staged per warp step
-
-template <int C>
-struct Stage {
-  static constexpr int VPL = C / 16;   // 16-byte vectors per slice chunk (= per lane per step)
-  static constexpr int ROW = VPL + 1;  // padded shared-memory row, in uint4
-  static constexpr int SMEM = kWarps * 32 * ROW * 16;
-};
-
 __device__ __forceinline__ uint64_t umin64(uint64_t a, uint64_t b) { return a < b ? a : b; }
 
 __device__ __forceinline__ bool aligned16(const void* p) {
   return (reinterpret_cast<uintptr_t>(p) & 15u) == 0;
 }
 
-// Load 16 bytes at base+o, zero beyond `bytes`; byte loads when unaligned or
-// at a ragged tail.
 __device__ __forceinline__ uint4 load16(const uint8_t* base, uint64_t o, uint64_t bytes, bool al) {
   if (al && o + 16 <= bytes) return ld_stream(base + o);
-  uint4 v = make_uint4(0, 0, 0, 0);
+  uint32_t w[4] = {0, 0, 0, 0};
   if (o < bytes) {
-    uint32_t w[4] = {0, 0, 0, 0};
-    const uint64_t n = bytes - o < 16 ? bytes - o : 16;
+    const uint64_t n = umin64(bytes - o, 16);
     for (uint64_t b = 0; b < n; ++b) w[b >> 2] |= static_cast<uint32_t>(base[o + b]) << (8 * (b & 3));
-    v = make_uint4(w[0], w[1], w[2], w[3]);
   }
-  return v;
+  return make_uint4(w[0], w[1], w[2], w[3]);
 }
 
 __device__ __forceinline__ void store16(uint8_t* base, uint64_t o, uint64_t bytes, bool al,
@@ -62,170 +43,9 @@ __device__ __forceinline__ void store16(uint8_t* base, uint64_t o, uint64_t byte
   }
   if (o < bytes) {
     const uint32_t w[4] = {v.x, v.y, v.z, v.w};
-    const uint64_t n = bytes - o < 16 ? bytes - o : 16;
+    const uint64_t n = umin64(bytes - o, 16);
     for (uint64_t b = 0; b < n; ++b) base[o + b] = static_cast<uint8_t>(w[b >> 2] >> (8 * (b & 3)));
   }
-}
-
-__device__ __forceinline__ void commit_begin(const SlotCommit& c) {
-  if (threadIdx.x == 0) {
-    volatile SlotMeta* m = reinterpret_cast<volatile SlotMeta*>(c.slot);
-    m->magic = kSlotMagic;
-    m->iteration = c.iteration;
-    m->seq = c.seq;
-    m->state = kSlotWriting;
-    __threadfence_system();
-  }
-  __syncthreads();
-}
-
-__device__ __forceinline__ void commit_end(const SlotCommit& c) {
-  __syncthreads();
-  if (threadIdx.x != 0 || !c.finalize) return;
-  __threadfence_system();
-  const unsigned prev = atomicAdd(c.done, 1u);
-  if (prev != gridDim.x - 1) return;
-  __threadfence_system();
-  volatile uint4* m = reinterpret_cast<volatile uint4*>(c.slot);
-  for (int i = 1; i < static_cast<int>(kMetaBytes / 16); ++i) {
-    const uint4 v = c.meta[i];
-    m[i].x = v.x; m[i].y = v.y; m[i].z = v.z; m[i].w = v.w;
-  }
-  volatile uint4* h = reinterpret_cast<volatile uint4*>(c.slot + c.payload_off - 32);
-  for (int i = 0; i < 2; ++i) {
-    const uint4 v = c.snp1[i];
-    h[i].x = v.x; h[i].y = v.y; h[i].z = v.z; h[i].w = v.w;
-  }
-  __threadfence_system();
-  volatile SlotMeta* sm = reinterpret_cast<volatile SlotMeta*>(c.slot);
-  sm->state = kSlotCommitted;
-  __threadfence_system();
-  *c.done = 0;
-}
-
-// One warp task = 32 consecutive slices of one region, one lane per slice.
-// Per step the warp stages C bytes of each of its 32 slices: coalesced
-// 16-byte loads (VPL per lane) -> optional 16-byte stores to the destination
-// -> padded shared-memory rows -> each lane hashes its own row.  The next
-// step's loads are issued before hashing, so HBM/NVLink latency overlaps the
-// byte-serial FNV chains.
-template <int C, SliceMode M, bool kCommit>
-__global__ void __launch_bounds__(kThreads, 2) slice_kernel(const __grid_constant__ SliceJob job) {
-  constexpr int VPL = Stage<C>::VPL;
-  constexpr int ROW = Stage<C>::ROW;
-  constexpr bool kCopy = (M == SliceMode::Copy || M == SliceMode::CopyVerify);
-  constexpr bool kVerify = (M == SliceMode::CopyVerify || M == SliceMode::HashVerify);
-  extern __shared__ uint4 smem[];
-  const int lane = threadIdx.x & 31;
-  const int warp = threadIdx.x >> 5;
-  uint4* wsm = smem + warp * 32 * ROW;
-
-  if constexpr (kCommit) commit_begin(job.commit);
-
-  const uint64_t S = job.slice_bytes;
-  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * kWarps;
-  for (uint64_t g = job.group_lo + static_cast<uint64_t>(blockIdx.x) * kWarps + warp;
-       g < job.group_hi; g += stride) {
-    SliceRegion R = job.reg[0];
-#pragma unroll
-    for (int i = 1; i < static_cast<int>(kMaxRegions); ++i)
-      if (i < static_cast<int>(job.nregions) && g >= job.reg[i].group_base) R = job.reg[i];
-    const bool al = aligned16(R.src) && (!kCopy || aligned16(R.dst));
-    const uint64_t s0 = (g - R.group_base) * 32;
-    const uint64_t base0 = s0 * S;
-    const uint64_t my_off = base0 + static_cast<uint64_t>(lane) * S;
-    const uint64_t my_len = my_off < R.bytes ? min(S, R.bytes - my_off) : 0;
-    const uint64_t max_len = min(S, R.bytes - base0);
-    const int nsteps = static_cast<int>((max_len + C - 1) / C);
-
-    Fnv h;
-    h.init();
-    if (job.init_state != nullptr && my_len) h.set(job.init_state[R.slice_base + s0 + lane]);
-
-    uint4 buf[VPL];
-    auto voff = [&](int i, int k) -> uint64_t {
-      const int q = i * 32 + lane;
-      return base0 + static_cast<uint64_t>(q / VPL) * S + static_cast<uint64_t>(k) * C +
-             static_cast<uint64_t>(q % VPL) * 16;
-    };
-    // Fast path: the whole task is 32 full, aligned slices.
-    const bool full = al && base0 + 32 * S <= R.bytes;
-    auto load_step = [&](int k) {
-      if (full) {
-#pragma unroll
-        for (int i = 0; i < VPL; ++i) buf[i] = ld_stream(R.src + voff(i, k));
-      } else {
-#pragma unroll
-        for (int i = 0; i < VPL; ++i) buf[i] = load16(R.src, voff(i, k), R.bytes, al);
-      }
-    };
-    load_step(0);
-
-    for (int k = 0; k < nsteps; ++k) {
-      __syncwarp();
-#pragma unroll
-      for (int i = 0; i < VPL; ++i) {
-        const int q = i * 32 + lane;
-        wsm[(q / VPL) * ROW + (q % VPL)] = buf[i];
-      }
-      if constexpr (kCopy) {
-        if (full) {
-#pragma unroll
-          for (int i = 0; i < VPL; ++i) st_stream(R.dst + voff(i, k), buf[i]);
-        } else {
-#pragma unroll
-          for (int i = 0; i < VPL; ++i) store16(R.dst, voff(i, k), R.bytes, al, buf[i]);
-        }
-      }
-      __syncwarp();
-      if (k + 1 < nsteps) load_step(k + 1);
-      const int64_t rem = static_cast<int64_t>(my_len) - static_cast<int64_t>(k) * C;
-      if (rem >= C) {
-#pragma unroll
-        for (int w = 0; w < VPL; ++w) h.vec(wsm[lane * ROW + w]);
-      } else if (rem > 0) {
-        const uint8_t* row = reinterpret_cast<const uint8_t*>(wsm + lane * ROW);
-        for (int b = 0; b < rem; ++b) h.byte(row[b]);
-      }
-    }
-    if (my_len) {
-      const uint64_t idx = R.slice_base + s0 + lane;
-      const uint64_t v = h.value();
-      if (job.sums_out != nullptr) job.sums_out[idx] = v;
-      if constexpr (kVerify) {
-        if (v != job.sums_expected[idx]) {
-          atomicMin(&job.result[0], static_cast<unsigned long long>(idx));
-          atomicAdd(&job.result[1], 1ull);
-        }
-      }
-    }
-  }
-
-  if constexpr (kCommit) commit_end(job.commit);
-}
-
-int g_sms = 0;
-
-template <int C, SliceMode M, bool kCommit>
-cudaError_t launch_t(const SliceJob& job, uint32_t max_ctas, cudaStream_t stream) {
-  auto kern = slice_kernel<C, M, kCommit>;
-  constexpr int smem = Stage<C>::SMEM;
-  static int occ = 0;
-  if (occ == 0) {
-    if (smem > 48 * 1024) {
-      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-      if (e != cudaSuccess) return e;
-    }
-    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kThreads, smem);
-    if (e != cudaSuccess) return e;
-    if (occ < 1) occ = 1;
-  }
-  uint64_t want = (job.group_hi - job.group_lo + kWarps - 1) / kWarps;
-  uint64_t cap = static_cast<uint64_t>(occ) * sm_count();
-  if (max_ctas) cap = std::min<uint64_t>(cap, max_ctas);
-  uint64_t grid = std::max<uint64_t>(1, std::min(want, cap));
-  kern<<<static_cast<unsigned>(grid), kThreads, smem, stream>>>(job);
-  return cudaGetLastError();
 }
 
 // ---- synthetic state ----------------------------------------------------------
@@ -428,49 +248,6 @@ unsigned grid_for(uint64_t work_items, int threads) {
 }
 
 }  // namespace
-
-int sm_count() {
-  if (g_sms == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev);
-    if (g_sms <= 0) g_sms = 148;
-  }
-  return g_sms;
-}
-
-void finalize_job(SliceJob& job) {
-  uint64_t groups = 0, slices = 0;
-  for (uint32_t r = 0; r < job.nregions; ++r) {
-    const uint64_t ns = (job.reg[r].bytes + job.slice_bytes - 1) / job.slice_bytes;
-    job.reg[r].slice_base = slices;
-    job.reg[r].group_base = groups;
-    slices += ns;
-    groups += (ns + 31) / 32;
-  }
-  for (uint32_t r = job.nregions; r < kMaxRegions; ++r) {
-    job.reg[r] = SliceRegion{nullptr, nullptr, 0, slices, ~0ull};
-  }
-  job.total_groups = groups;
-  job.group_lo = 0;
-  job.group_hi = groups;
-}
-
-cudaError_t launch_slices(const SliceJob& job, SliceMode mode, bool commit, uint32_t max_ctas,
-                          cudaStream_t stream) {
-  switch (mode) {
-    case SliceMode::Hash:
-      return launch_t<kChunk, SliceMode::Hash, false>(job, max_ctas, stream);
-    case SliceMode::Copy:
-      return commit ? launch_t<kChunk, SliceMode::Copy, true>(job, max_ctas, stream)
-                    : launch_t<kChunk, SliceMode::Copy, false>(job, max_ctas, stream);
-    case SliceMode::CopyVerify:
-      return launch_t<kChunk, SliceMode::CopyVerify, false>(job, max_ctas, stream);
-    case SliceMode::HashVerify:
-      return launch_t<kChunk, SliceMode::HashVerify, false>(job, max_ctas, stream);
-  }
-  return cudaErrorInvalidValue;
-}
 
 cudaError_t launch_expand(uint8_t* dst, uint64_t fold, uint64_t bytes, const uint8_t* prefix32,
                           cudaStream_t stream) {

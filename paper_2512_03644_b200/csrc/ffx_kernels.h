@@ -45,6 +45,8 @@ struct SliceJob {
   const uint64_t* sums_expected;  // verify mode
   const uint64_t* init_state;     // per-slice FNV start (null = offset basis)
   unsigned long long* result;     // verify mode: [first bad slice, bad count]
+  unsigned int* sched;            // [next task, CTAs done]: dynamic scheduling
+                                  // (zero between launches; null = static)
   SlotCommit commit;
 };
 

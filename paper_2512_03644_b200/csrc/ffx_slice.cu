@@ -1,0 +1,395 @@
+// ffx_slice.cu -- the snapshot / recovery kernel: fused copy + per-slice
+// FNV-1a-64 (+ verify against a checksum table, + slot commit).
+//
+// Work unit: one warp task = 32 consecutive slices of one region, one lane
+// per slice (FNV-1a is byte-serial, hash.cpp:102-110, so parallelism comes
+// from independent slice chains).  Each step moves C bytes of every slice:
+//
+//   full, aligned task (the bulk of any payload) -- TMA bulk-copy pipeline:
+//     cp.async.bulk global->smem (one C-byte row per lane, S stages, mbarrier
+//     complete_tx) -> cp.async.bulk smem->global to the destination (local
+//     HBM or an NVLink peer's replica) -> each lane hashes its row from
+//     shared memory.  No payload byte passes through registers on the copy
+//     path; loads run S steps ahead of the hash.
+//   ragged task (region tail, unaligned pointers) -- register path: 16-byte
+//     loads, stores and a padded shared-memory transpose.
+//
+// Rows are padded by 16 bytes so the eight lanes of each LDS.128 phase hit
+// distinct banks.  Tasks are handed out dynamically (one atomic per task) so
+// the last wave does not idle SMs.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdlib>
+
+#include "ffx_device.cuh"
+#include "ffx_kernels.h"
+
+namespace ffx {
+
+namespace {
+
+__device__ __forceinline__ uint64_t umin64(uint64_t a, uint64_t b) { return a < b ? a : b; }
+
+__device__ __forceinline__ bool aligned16(const void* p) {
+  return (reinterpret_cast<uintptr_t>(p) & 15u) == 0;
+}
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+// 16 bytes at base+o, zero past `bytes`; byte loads when unaligned / ragged.
+__device__ __forceinline__ uint4 load16(const uint8_t* base, uint64_t o, uint64_t bytes, bool al) {
+  if (al && o + 16 <= bytes) return ld_stream(base + o);
+  uint32_t w[4] = {0, 0, 0, 0};
+  if (o < bytes) {
+    const uint64_t n = umin64(bytes - o, 16);
+    for (uint64_t b = 0; b < n; ++b) w[b >> 2] |= static_cast<uint32_t>(base[o + b]) << (8 * (b & 3));
+  }
+  return make_uint4(w[0], w[1], w[2], w[3]);
+}
+
+__device__ __forceinline__ void store16(uint8_t* base, uint64_t o, uint64_t bytes, bool al,
+                                        const uint4& v) {
+  if (al && o + 16 <= bytes) {
+    st_stream(base + o, v);
+    return;
+  }
+  if (o < bytes) {
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+    const uint64_t n = umin64(bytes - o, 16);
+    for (uint64_t b = 0; b < n; ++b) base[o + b] = static_cast<uint8_t>(w[b >> 2] >> (8 * (b & 3)));
+  }
+}
+
+// ---- TMA bulk copies + mbarriers (PTX) ------------------------------------------
+
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_init_fence() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "FFX_WAIT:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra FFX_WAIT;\n\t}" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_load(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+      "l"(src), "r"(bytes), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_store(void* dst, uint32_t src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(src), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read_all() {
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void fence_async_global() {
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
+// ---- slot commit ------------------------------------------------------------------
+
+__device__ __forceinline__ void commit_begin(const SlotCommit& c) {
+  if (threadIdx.x == 0) {
+    volatile SlotMeta* m = reinterpret_cast<volatile SlotMeta*>(c.slot);
+    m->magic = kSlotMagic;
+    m->iteration = c.iteration;
+    m->seq = c.seq;
+    m->state = kSlotWriting;
+    __threadfence_system();
+  }
+  __syncthreads();
+}
+
+// Called by thread 0 after the whole CTA finished (and its bulk stores landed).
+__device__ __forceinline__ void commit_end(const SlotCommit& c) {
+  if (!c.finalize) return;
+  __threadfence_system();
+  const unsigned prev = atomicAdd(c.done, 1u);
+  if (prev != gridDim.x - 1) return;
+  __threadfence_system();
+  volatile uint4* m = reinterpret_cast<volatile uint4*>(c.slot);
+  for (int i = 1; i < static_cast<int>(kMetaBytes / 16); ++i) {
+    const uint4 v = c.meta[i];
+    m[i].x = v.x;
+    m[i].y = v.y;
+    m[i].z = v.z;
+    m[i].w = v.w;
+  }
+  volatile uint4* h = reinterpret_cast<volatile uint4*>(c.slot + c.payload_off - 32);
+  for (int i = 0; i < 2; ++i) {
+    const uint4 v = c.snp1[i];
+    h[i].x = v.x;
+    h[i].y = v.y;
+    h[i].z = v.z;
+    h[i].w = v.w;
+  }
+  __threadfence_system();
+  reinterpret_cast<volatile SlotMeta*>(c.slot)->state = kSlotCommitted;
+  __threadfence_system();
+  *c.done = 0;
+}
+
+template <int C, int S, int W>
+struct Cfg {
+  static constexpr int VPL = C / 16;        // 16-byte vectors per row
+  static constexpr int ROWB = C + 16;       // padded row (bytes)
+  static constexpr int STAGE = 32 * ROWB;   // one step of one warp
+  static constexpr int WARPB = S * STAGE;
+  static constexpr int BARB = ((W * S * 8 + 127) / 128) * 128;
+  static constexpr int SMEM = BARB + W * WARPB;
+};
+
+template <int C, int S, int W, SliceMode M, bool kCommit>
+__global__ void __launch_bounds__(W * 32) slice_kernel(const __grid_constant__ SliceJob job) {
+  using K = Cfg<C, S, W>;
+  constexpr bool kCopy = (M == SliceMode::Copy || M == SliceMode::CopyVerify);
+  constexpr bool kVerify = (M == SliceMode::CopyVerify || M == SliceMode::HashVerify);
+  extern __shared__ __align__(128) uint8_t smem[];
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  uint8_t* wbase = smem + K::BARB + warp * K::WARPB;
+  const uint32_t bar0 = smem_u32(smem) + warp * S * 8;
+  const uint32_t stage0 = smem_u32(wbase);
+
+  if (lane == 0) {
+    for (int s = 0; s < S; ++s) mbar_init(bar0 + 8 * s, 1);
+    mbar_init_fence();
+  }
+  __syncwarp();
+  uint32_t phase = 0;  // bit s: parity of the next completion of stage s
+
+  if constexpr (kCommit) commit_begin(job.commit);
+
+  const uint64_t Sl = job.slice_bytes;
+  uint64_t g_next = job.group_lo + static_cast<uint64_t>(blockIdx.x) * W + warp;
+  const uint64_t g_stride = static_cast<uint64_t>(gridDim.x) * W;
+  for (;;) {
+    uint64_t g;
+    if (job.sched != nullptr) {
+      unsigned t = 0;
+      if (lane == 0) t = atomicAdd(&job.sched[0], 1u);
+      g = job.group_lo + __shfl_sync(0xffffffffu, t, 0);
+    } else {
+      g = g_next;
+      g_next += g_stride;
+    }
+    if (g >= job.group_hi) break;
+
+    SliceRegion R = job.reg[0];
+#pragma unroll
+    for (int i = 1; i < static_cast<int>(kMaxRegions); ++i)
+      if (i < static_cast<int>(job.nregions) && g >= job.reg[i].group_base) R = job.reg[i];
+    const bool al = aligned16(R.src) && (!kCopy || aligned16(R.dst));
+    const uint64_t s0 = (g - R.group_base) * 32;
+    const uint64_t base0 = s0 * Sl;
+    const uint64_t my_off = base0 + static_cast<uint64_t>(lane) * Sl;
+    const uint64_t my_len = my_off < R.bytes ? umin64(Sl, R.bytes - my_off) : 0;
+
+    Fnv h;
+    h.init();
+    if (job.init_state != nullptr && my_len) h.set(job.init_state[R.slice_base + s0 + lane]);
+
+    // Stages are free once this lane's earlier bulk stores finished reading
+    // them and every lane is past its previous hash.
+    if constexpr (kCopy) bulk_wait_read_all();
+    __syncwarp();
+
+    if (al && base0 + 32 * Sl <= R.bytes) {
+      // ---- TMA pipeline: 32 full slices --------------------------------------------
+      const int nsteps = static_cast<int>(Sl / C);
+      const uint8_t* src = R.src + my_off;
+      uint8_t* dst = kCopy ? R.dst + my_off : nullptr;
+      fence_async_smem();
+      const int pro = nsteps < S ? nsteps : S;
+      for (int k = 0; k < pro; ++k) {
+        if (lane == 0) mbar_expect_tx(bar0 + 8 * k, 32 * C);
+        __syncwarp();
+        bulk_load(stage0 + k * K::STAGE + lane * K::ROWB, src + static_cast<uint64_t>(k) * C, C,
+                  bar0 + 8 * k);
+      }
+      for (int k = 0; k < nsteps; ++k) {
+        const int s = k % S;
+        mbar_wait(bar0 + 8 * s, (phase >> s) & 1u);
+        phase ^= 1u << s;
+        const uint32_t row = stage0 + s * K::STAGE + lane * K::ROWB;
+        if constexpr (kCopy) {
+          bulk_store(dst + static_cast<uint64_t>(k) * C, row, C);
+          bulk_commit();
+        }
+        const uint4* rp = reinterpret_cast<const uint4*>(wbase + s * K::STAGE + lane * K::ROWB);
+#pragma unroll
+        for (int w = 0; w < K::VPL; ++w) h.vec(rp[w]);
+        if (k + S < nsteps) {
+          if constexpr (kCopy) bulk_wait_read_all();
+          __syncwarp();
+          fence_async_smem();
+          if (lane == 0) mbar_expect_tx(bar0 + 8 * s, 32 * C);
+          __syncwarp();
+          bulk_load(row, src + static_cast<uint64_t>(k + S) * C, C, bar0 + 8 * s);
+        }
+      }
+    } else {
+      // ---- register path: ragged tail or unaligned pointers ------------------------
+      const uint64_t max_len = umin64(Sl, R.bytes - base0);
+      const int nsteps = static_cast<int>((max_len + C - 1) / C);
+      uint4* rows = reinterpret_cast<uint4*>(wbase);
+      for (int k = 0; k < nsteps; ++k) {
+        uint4 buf[K::VPL];
+#pragma unroll
+        for (int i = 0; i < K::VPL; ++i) {
+          const int q = i * 32 + lane;
+          const uint64_t o = base0 + static_cast<uint64_t>(q / K::VPL) * Sl + static_cast<uint64_t>(k) * C +
+                             static_cast<uint64_t>(q % K::VPL) * 16;
+          buf[i] = load16(R.src, o, R.bytes, al);
+          if constexpr (kCopy) store16(R.dst, o, R.bytes, al, buf[i]);
+        }
+        __syncwarp();
+#pragma unroll
+        for (int i = 0; i < K::VPL; ++i) {
+          const int q = i * 32 + lane;
+          rows[(q / K::VPL) * (K::ROWB / 16) + (q % K::VPL)] = buf[i];
+        }
+        __syncwarp();
+        const int64_t rem = static_cast<int64_t>(my_len) - static_cast<int64_t>(k) * C;
+        const uint4* rp = rows + lane * (K::ROWB / 16);
+        if (rem >= C) {
+#pragma unroll
+          for (int w = 0; w < K::VPL; ++w) h.vec(rp[w]);
+        } else if (rem > 0) {
+          const uint8_t* rb = reinterpret_cast<const uint8_t*>(rp);
+          for (int b = 0; b < rem; ++b) h.byte(rb[b]);
+        }
+      }
+    }
+
+    if (my_len) {
+      const uint64_t idx = R.slice_base + s0 + lane;
+      const uint64_t v = h.value();
+      if (job.sums_out != nullptr) job.sums_out[idx] = v;
+      if constexpr (kVerify) {
+        if (v != job.sums_expected[idx]) {
+          atomicMin(&job.result[0], static_cast<unsigned long long>(idx));
+          atomicAdd(&job.result[1], 1ull);
+        }
+      }
+    }
+  }
+
+  if constexpr (kCopy) {
+    bulk_wait_all();  // this lane's stores have landed
+    fence_async_global();
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (job.sched != nullptr) {
+      __threadfence();
+      if (atomicAdd(&job.sched[1], 1u) == gridDim.x - 1) {
+        job.sched[0] = 0;
+        job.sched[1] = 0;
+      }
+    }
+    if constexpr (kCommit) commit_end(job.commit);
+  }
+}
+
+int g_sms = 0;
+
+template <int C, int S, int W, SliceMode M, bool kCommit>
+cudaError_t launch_t(const SliceJob& job, uint32_t max_ctas, cudaStream_t stream) {
+  auto kern = slice_kernel<C, S, W, M, kCommit>;
+  constexpr int smem = Cfg<C, S, W>::SMEM;
+  static int occ = 0;
+  if (occ == 0) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, W * 32, smem);
+    if (e != cudaSuccess) return e;
+    if (occ < 1) occ = 1;
+  }
+  const uint64_t want = (job.group_hi - job.group_lo + W - 1) / W;
+  uint64_t cap = static_cast<uint64_t>(occ) * sm_count();
+  if (max_ctas) cap = std::min<uint64_t>(cap, max_ctas);
+  const uint64_t grid = std::max<uint64_t>(1, std::min(want, cap));
+  kern<<<static_cast<unsigned>(grid), W * 32, smem, stream>>>(job);
+  return cudaGetLastError();
+}
+
+// Kernel variants for tuning: FFX_SLICE_VARIANT selects chunk/stages/warps.
+int variant() {
+  static const int v = [] {
+    const char* e = std::getenv("FFX_SLICE_VARIANT");
+    return e ? std::atoi(e) : 0;
+  }();
+  return v;
+}
+
+template <SliceMode M, bool kCommit>
+cudaError_t launch_mode(const SliceJob& job, uint32_t max_ctas, cudaStream_t stream) {
+  switch (variant()) {
+    case 1: return launch_t<128, 3, 4, M, kCommit>(job, max_ctas, stream);
+    case 2: return launch_t<256, 3, 2, M, kCommit>(job, max_ctas, stream);
+    case 3: return launch_t<64, 6, 4, M, kCommit>(job, max_ctas, stream);
+    default: return launch_t<128, 4, 4, M, kCommit>(job, max_ctas, stream);
+  }
+}
+
+}  // namespace
+
+int sm_count() {
+  if (g_sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev);
+    if (g_sms <= 0) g_sms = 148;
+  }
+  return g_sms;
+}
+
+void finalize_job(SliceJob& job) {
+  uint64_t groups = 0, slices = 0;
+  for (uint32_t r = 0; r < job.nregions; ++r) {
+    const uint64_t ns = (job.reg[r].bytes + job.slice_bytes - 1) / job.slice_bytes;
+    job.reg[r].slice_base = slices;
+    job.reg[r].group_base = groups;
+    slices += ns;
+    groups += (ns + 31) / 32;
+  }
+  for (uint32_t r = job.nregions; r < kMaxRegions; ++r) job.reg[r] = SliceRegion{nullptr, nullptr, 0, slices, ~0ull};
+  job.total_groups = groups;
+  job.group_lo = 0;
+  job.group_hi = groups;
+}
+
+cudaError_t launch_slices(const SliceJob& job, SliceMode mode, bool commit, uint32_t max_ctas,
+                          cudaStream_t stream) {
+  switch (mode) {
+    case SliceMode::Hash: return launch_mode<SliceMode::Hash, false>(job, max_ctas, stream);
+    case SliceMode::Copy:
+      return commit ? launch_mode<SliceMode::Copy, true>(job, max_ctas, stream)
+                    : launch_mode<SliceMode::Copy, false>(job, max_ctas, stream);
+    case SliceMode::CopyVerify: return launch_mode<SliceMode::CopyVerify, false>(job, max_ctas, stream);
+    case SliceMode::HashVerify: return launch_mode<SliceMode::HashVerify, false>(job, max_ctas, stream);
+  }
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace ffx

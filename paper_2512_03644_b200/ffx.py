@@ -208,6 +208,11 @@ SIGNATURES = {
     "ffx_expand": (_I, [_P, _P, _U64, _P]),
     "ffx_materialize": (_I, [_P, _P, _U64, _P]),
     "ffx_blob_check": (_I, [_P, _U64, ctypes.POINTER(_U64), _P]),
+    "ffx_device_alloc": (_I, [_I, _U64, ctypes.POINTER(_P)]),
+    "ffx_device_free": (_I, [_I, _P]),
+    "ffx_memcpy": (_I, [_P, _P, _U64, _P, _I]),
+    "ffx_pointer_is_device": (_I, [_P, ctypes.POINTER(_I)]),
+    "ffx_stream_sync": (_I, [_P]),
     "ffx_open": (_I, [_I, ctypes.POINTER(ClusterSpec), Role, _U64, ctypes.POINTER(_P)]),
     "ffx_close": (_I, [_P]),
     "ffx_register_region": (_I, [_P, _I, _P, _U64, _I]),

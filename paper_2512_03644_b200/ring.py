@@ -1,0 +1,70 @@
+"""Host-side wiring of the DP-ring replicas across ranks (plumbing).
+
+One process per GPU.  Every rank holds the replica of its ring predecessor
+(reference SPEC.md:516-517, controller.cpp:179-180: the replica of
+(dp, pp, tp) lives on (dp+1 mod d, pp, tp)) and snapshots into the replica
+its successor holds.  Replica memory is exported as an opaque handle
+(ffx_replica_export: CUDA IPC + layout) and exchanged with
+torch.distributed's object collectives; the data path itself never touches
+the host.
+
+The functions take the export / open / all-gather operations as arguments so
+the wiring is testable on CPU with gloo (tests/test_ring_wiring.py).
+"""
+from __future__ import annotations
+
+from typing import Callable, List, Sequence
+
+
+def ring_roles(world: int, p: int = 1, t: int = 1):
+    """Global index -> (dp, pp, tp), tensor fastest, then pipeline, then data
+    parallel (reference domain.cpp:18-30)."""
+    return [(i // (t * p), (i // t) % p, i % t) for i in range(world)]
+
+
+def successor(rank: int, world: int, p: int = 1, t: int = 1, k: int = 1) -> int:
+    """Rank holding this rank's k-th replica: (dp+k mod d, pp, tp)."""
+    d = world // (p * t)
+    dp, pp, tp = ring_roles(world, p, t)[rank]
+    return (((dp + k) % d) * p + pp) * t + tp
+
+
+def predecessor(rank: int, world: int, p: int = 1, t: int = 1, k: int = 1) -> int:
+    d = world // (p * t)
+    dp, pp, tp = ring_roles(world, p, t)[rank]
+    return (((dp - k) % d) * p + pp) * t + tp
+
+
+def wire_ring(rank: int, world: int, create_for: Callable[[int], object], export: Callable[[object], bytes],
+              open_handle: Callable[[bytes], object], all_gather: Callable[[bytes], List[bytes]],
+              p: int = 1, t: int = 1, replicas: int = 1):
+    """Create the replicas this rank holds, exchange handles, open the ones
+    this rank writes into.
+
+    Returns (held, targets, handles):
+      held[k]    replica this rank holds for predecessor k+1 steps back
+      targets[k] opened view of the replica that successor k+1 holds for us
+      handles[r][k] every rank's exported handle (needed again for recovery)
+    """
+    held = [create_for(predecessor(rank, world, p, t, k + 1)) for k in range(replicas)]
+    mine = b"".join(export(h) for h in held)
+    gathered = all_gather(mine)
+    hb = len(mine) // replicas if replicas else 0
+    handles = [[g[i * hb:(i + 1) * hb] for i in range(replicas)] for g in gathered]
+    targets = [open_handle(handles[successor(rank, world, p, t, k + 1)][k]) for k in range(replicas)]
+    return held, targets, handles
+
+
+def recovery_sources(plan_forwards: Sequence, world: int, p: int = 1, t: int = 1):
+    """Map plan_recovery forwards (origin Role, holder_node, dest_node,
+    holder_dp) to (origin rank, holder rank, replica index k) so the
+    replacement knows which exported handle to open."""
+    out = []
+    d = world // (p * t)
+    for origin, _hn, _dn, holder_dp in plan_forwards:
+        o = origin.tuple() if hasattr(origin, "tuple") else tuple(origin)
+        origin_rank = (o[0] * p + o[1]) * t + o[2]
+        holder_rank = (holder_dp * p + o[1]) * t + o[2]
+        k = (holder_dp - o[0]) % d - 1
+        out.append((origin_rank, holder_rank, k))
+    return out

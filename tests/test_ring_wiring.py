@@ -1,0 +1,97 @@
+"""Multi-process host logic of the DP ring on CPU (gloo, world_size 2 and 4).
+
+The replica handles are stand-in byte strings; what is checked is that every
+rank writes into exactly the replica its ring successor holds for it, and
+that recovery sources derived from plan_recovery point at the right holder
+(reference controller.cpp:177-189, domain.cpp:51-62).
+"""
+import os
+import socket
+
+import pytest
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2512_03644_b200 import ring
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _worker(rank, world, port, replicas, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        created = []
+
+        def create_for(origin):
+            created.append(origin)
+            return origin
+
+        def export(origin):
+            return b"H%02d<%02d" % (rank, origin)  # "held by rank, for origin"
+
+        opened = []
+
+        def open_handle(h):
+            opened.append(h)
+            return h
+
+        def all_gather(b):
+            out = [None] * world
+            dist.all_gather_object(out, b)
+            return out
+
+        held, targets, handles = ring.wire_ring(rank, world, create_for, export, open_handle, all_gather,
+                                                replicas=replicas)
+        q.put((rank, created, [bytes(t) for t in targets], [[bytes(x) for x in h] for h in handles]))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,replicas", [(2, 1), (4, 1), (4, 2)])
+def test_ring_wiring_gloo(world, replicas):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, replicas, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = {}
+    for _ in range(world):
+        rank, created, targets, handles = q.get(timeout=120)
+        res[rank] = (created, targets, handles)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for r in range(world):
+        created, targets, handles = res[r]
+        assert created == [(r - k) % world for k in range(1, replicas + 1)]
+        for k in range(replicas):
+            holder = (r + k + 1) % world
+            assert targets[k] == b"H%02d<%02d" % (holder, r)  # my snapshots land at my k-th successor
+        assert handles == res[0][2]
+
+
+def test_recovery_sources_follow_plan():
+    from paper_2512_03644_b200 import ffx
+    spec = ffx.make_spec(d=8, phi=1000, distributed=True, num_nodes=8, gpus_per_node=1)
+    plan = ffx.plan_recovery(spec, [3], [], 10, 0)
+    assert ring.recovery_sources(plan.forwards, 8) == [(3, 4, 0)]
+    plan2 = ffx.plan_recovery(spec, [3, 4], [], 10, 0, replicas=2)
+    assert sorted(ring.recovery_sources(plan2.forwards, 8)) == [(3, 5, 1), (4, 5, 0)]
+
+
+def test_successor_predecessor_with_pp_tp():
+    # d=2, p=2, t=2: ring successor keeps (pp, tp) and moves dp.
+    w = 8
+    for r in range(w):
+        s = ring.successor(r, w, 2, 2)
+        assert ring.ring_roles(w, 2, 2)[s][1:] == ring.ring_roles(w, 2, 2)[r][1:]
+        assert ring.predecessor(s, w, 2, 2) == r
