@@ -280,6 +280,16 @@ typedef struct ffx_snapshot_opts {
  * exceed the target capacity (ckpt.cpp:40-43). */
 int ffx_snapshot(ffx_ctx* ctx, uint64_t iteration, void* stream, const ffx_snapshot_opts* opts);
 
+/* The slice scheduler, step by step: begin() fixes the slot, layout and the
+ * split into opts->batches batches (no GPU work); each next() launches one
+ * batch on `stream` after `gate_event` (a cudaEvent_t the training step
+ * records when a gap opens -- e.g. right after an all-gather completes; NULL
+ * = no gate).  The last batch commits the slot.  ffx_snapshot() is
+ * begin + next for every batch with opts->gate_events[b]. */
+int ffx_snapshot_begin(ffx_ctx* ctx, uint64_t iteration, const ffx_snapshot_opts* opts,
+                       uint32_t* batches);
+int ffx_snapshot_next(ffx_ctx* ctx, void* stream, void* gate_event, uint32_t* remaining);
+
 /* Copy the checksum table written by this ctx's most recent snapshot into
  * host memory (async on `stream`; pinned memory for true overlap).
  * *n_out = entries copied (min(table, max_entries)). */

@@ -115,7 +115,17 @@ struct ffx_replica {
   uint64_t* sums(uint32_t v) const { return reinterpret_cast<uint64_t*>(slot(v) + kMetaBytes); }
 };
 
+// A snapshot split by the slice scheduler into batches still to be issued.
+struct PendingSnapshot {
+  bool active = false;
+  SliceJob job{};
+  uint32_t batches = 1, next = 0, max_ctas = 0, slot = 0;
+  uint64_t iteration = 0, seq = 0, nslices = 0, logical = 0;
+  bool verify = false;
+};
+
 struct ffx_ctx {
+  PendingSnapshot pending;
   int device = 0;
   ffx_cluster_spec spec{};
   ffx_role self{};
@@ -962,10 +972,14 @@ extern "C" int ffx_snapshot_target(ffx_ctx* c, ffx_replica* t) {
   return FFX_OK;
 }
 
-extern "C" int ffx_snapshot(ffx_ctx* c, uint64_t iteration, void* stream, const ffx_snapshot_opts* o) {
+extern "C" int ffx_snapshot_begin(ffx_ctx* c, uint64_t iteration, const ffx_snapshot_opts* o,
+                                  uint32_t* batches_out) {
   if (!c) return fail(FFX_EINVAL, "snapshot: null ctx");
   ffx_replica* t = c->target;
   if (!t) return fail(FFX_ESTATE, "snapshot: no target replica (ffx_snapshot_target)");
+  if (c->pending.active)
+    return fail(FFX_ESTATE, "snapshot of iteration %llu still has %u batches to issue",
+                (unsigned long long)c->pending.iteration, c->pending.batches - c->pending.next);
   ffx_snapshot_opts opts{};
   if (o) opts = *o;
   const PayloadMap pm = payload_map(c);
@@ -980,10 +994,8 @@ extern "C" int ffx_snapshot(ffx_ctx* c, uint64_t iteration, void* stream, const 
   if (nslices > t->layout.table_cap)
     return fail(FFX_ECONFIG, "snapshot needs %llu checksum entries, slot has %llu",
                 (unsigned long long)nslices, (unsigned long long)t->layout.table_cap);
-  if (c->slice_bytes != t->slice_bytes && t->layout.table_cap < nslices)
-    return fail(FFX_ECONFIG, "slice size mismatch");
 
-  // Two-version rule (ckpt.cpp:46-52): replace the slot holding this
+  // Two-version rule (ckpt.cpp:46-52, :86-92): replace the slot holding this
   // iteration, else an empty slot, else the oldest.
   int v = -1;
   for (uint32_t i = 0; i < t->versions; ++i)
@@ -999,8 +1011,9 @@ extern "C" int ffx_snapshot(ffx_ctx* c, uint64_t iteration, void* stream, const 
   const uint32_t slot = static_cast<uint32_t>(v);
   const uint64_t seq = ++c->seq;
 
-  DeviceGuard g(c->device);
-  SliceJob job{};
+  PendingSnapshot& P = c->pending;
+  P = PendingSnapshot{};
+  SliceJob& job = P.job;
   job.nregions = static_cast<uint32_t>(pm.regs.size());
   for (size_t i = 0; i < pm.regs.size(); ++i)
     job.reg[i] = SliceRegion{pm.regs[i]->dev, t->payload(slot) + pm.offs[i], pm.regs[i]->bytes, 0, 0};
@@ -1035,52 +1048,94 @@ extern "C" int ffx_snapshot(ffx_ctx* c, uint64_t iteration, void* stream, const 
   std::memcpy(cm.meta, &m, sizeof m);
   std::memcpy(cm.snp1, hdr, 32);
 
-  // Slice scheduler: split the warp tasks into `batches` launches, each
-  // optionally gated on a caller event (a measured gap in the step's own
-  // collectives), all on the caller's (low-priority) stream.
+  P.active = true;
+  P.batches = std::max<uint32_t>(1, opts.batches);
+  P.max_ctas = opts.max_ctas;
+  P.slot = slot;
+  P.iteration = iteration;
+  P.seq = seq;
+  P.nslices = nslices;
+  P.logical = pm.logical;
+  P.verify = opts.verify_on_store != 0;
+  if (batches_out) *batches_out = P.batches;
+  return FFX_OK;
+}
+
+namespace {
+
+// Holder-side re-verification of a landed slot (NeighborBuffer::store
+// validates before accepting, ckpt.cpp:78): one HBM read of the replica.
+int verify_landed(ffx_ctx* c, const PendingSnapshot& P, cudaStream_t s) {
+  const unsigned long long init[2] = {~0ull, 0ull};
+  FFX_CUDA(cudaMemcpyAsync(c->result, init, sizeof init, cudaMemcpyHostToDevice, s));
+  SliceJob vj = P.job;
+  for (uint32_t i = 0; i < vj.nregions; ++i) {
+    vj.reg[i].src = vj.reg[i].dst;
+    vj.reg[i].dst = nullptr;
+  }
+  vj.sums_out = nullptr;
+  vj.sums_expected = P.job.sums_out;
+  vj.result = c->result;
+  vj.sched = c->done + 12;
+  vj.commit = SlotCommit{};
+  vj.group_lo = 0;
+  vj.group_hi = vj.total_groups;
+  FFX_CUDA(launch_slices(vj, SliceMode::HashVerify, false, P.max_ctas, s));
+  c->stats.kernel_launches++;
+  FFX_CUDA(cudaMemcpyAsync(c->result_host, c->result, 16, cudaMemcpyDeviceToHost, s));
+  FFX_CUDA(cudaStreamSynchronize(s));
+  if (c->result_host[1]) {
+    c->stats.verify_failures++;
+    return fail(FFX_ECORRUPT, "snapshot verify-on-store: %llu bad slices (first %llu)",
+                c->result_host[1], c->result_host[0]);
+  }
+  return FFX_OK;
+}
+
+}  // namespace
+
+extern "C" int ffx_snapshot_next(ffx_ctx* c, void* stream, void* gate_event, uint32_t* remaining) {
+  if (!c) return fail(FFX_EINVAL, "snapshot_next: null ctx");
+  PendingSnapshot& P = c->pending;
+  if (!P.active) return fail(FFX_ESTATE, "snapshot_next: no snapshot in progress (ffx_snapshot_begin)");
+  DeviceGuard g(c->device);
   cudaStream_t s = as_stream(stream);
-  const uint32_t batches = std::max<uint32_t>(1, opts.batches);
-  const uint64_t G = job.total_groups;
-  auto* gates = static_cast<cudaEvent_t*>(opts.gate_events);
-  for (uint32_t b = 0; b < batches; ++b) {
-    SliceJob bj = job;
-    bj.group_lo = G * b / batches;
-    bj.group_hi = G * (b + 1) / batches;
-    bj.commit.finalize = (b + 1 == batches);
-    if (gates && gates[b]) FFX_CUDA(cudaStreamWaitEvent(s, gates[b], 0));
-    if (bj.group_lo == bj.group_hi && !bj.commit.finalize) continue;
-    FFX_CUDA(launch_slices(bj, SliceMode::Copy, true, opts.max_ctas, s));
+  // Batch b covers warp tasks [G*b/B, G*(b+1)/B); the last batch commits.
+  const uint32_t b = P.next++;
+  const uint64_t G = P.job.total_groups;
+  SliceJob bj = P.job;
+  bj.group_lo = G * b / P.batches;
+  bj.group_hi = G * (b + 1) / P.batches;
+  bj.commit.finalize = (b + 1 == P.batches);
+  if (gate_event) FFX_CUDA(cudaStreamWaitEvent(s, static_cast<cudaEvent_t>(gate_event), 0));
+  if (bj.group_lo != bj.group_hi || bj.commit.finalize) {
+    FFX_CUDA(launch_slices(bj, SliceMode::Copy, true, P.max_ctas, s));
     c->stats.kernel_launches++;
   }
-  t->cache[slot] = SlotCache{true, kSlotCommitted, iteration, seq};
-  c->last_slot = slot;
-  c->last_nslices = nslices;
-  c->stats.snapshots++;
-  c->stats.snapshot_bytes += pm.logical;
+  if (remaining) *remaining = P.batches - P.next;
+  if (P.next < P.batches) return FFX_OK;
 
-  if (opts.verify_on_store) {
-    // Holder-side re-verification of the landed slot (NeighborBuffer::store
-    // validates before accepting, ckpt.cpp:78): HBM read of the replica.
-    const unsigned long long init[2] = {~0ull, 0ull};
-    FFX_CUDA(cudaMemcpyAsync(c->result, init, sizeof init, cudaMemcpyHostToDevice, s));
-    SliceJob vj = job;
-    for (size_t i = 0; i < pm.regs.size(); ++i) {
-      vj.reg[i].src = t->payload(slot) + pm.offs[i];
-      vj.reg[i].dst = nullptr;
-    }
-    vj.sums_out = nullptr;
-    vj.sums_expected = t->sums(slot);
-    vj.result = c->result;
-    vj.sched = c->done + 12;
-    vj.commit = SlotCommit{};
-    FFX_CUDA(launch_slices(vj, SliceMode::HashVerify, false, opts.max_ctas, s));
-    c->stats.kernel_launches++;
-    FFX_CUDA(cudaMemcpyAsync(c->result_host, c->result, 16, cudaMemcpyDeviceToHost, s));
-    FFX_CUDA(cudaStreamSynchronize(s));
-    if (c->result_host[1]) {
-      c->stats.verify_failures++;
-      return fail(FFX_ECORRUPT, "snapshot verify-on-store: %llu bad slices (first %llu)",
-                  c->result_host[1], c->result_host[0]);
+  P.active = false;
+  ffx_replica* t = c->target;
+  t->cache[P.slot] = SlotCache{true, kSlotCommitted, P.iteration, P.seq};
+  c->last_slot = P.slot;
+  c->last_nslices = P.nslices;
+  c->stats.snapshots++;
+  c->stats.snapshot_bytes += P.logical;
+  return P.verify ? verify_landed(c, P, s) : FFX_OK;
+}
+
+extern "C" int ffx_snapshot(ffx_ctx* c, uint64_t iteration, void* stream, const ffx_snapshot_opts* o) {
+  uint32_t batches = 1;
+  int st = ffx_snapshot_begin(c, iteration, o, &batches);
+  if (st) return st;
+  auto* gates = o ? static_cast<void**>(o->gate_events) : nullptr;
+  for (uint32_t b = 0; b < batches; ++b) {
+    uint32_t left = 0;
+    st = ffx_snapshot_next(c, stream, gates ? gates[b] : nullptr, &left);
+    if (st) {
+      c->pending.active = false;
+      return st;
     }
   }
   return FFX_OK;

@@ -2,6 +2,7 @@
 // ffx_kernels.cu.  Internal to libffx.so; the public boundary is include/ffx.h.
 #pragma once
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -18,7 +19,12 @@ struct SliceRegion {
   uint64_t bytes;
   uint64_t slice_base;   // first checksum-table index of this region
   uint64_t group_base;   // first 32-slice warp task of this region
+  int32_t tmap;          // index of this region's src/dst tensor-map pair, -1 = none
+  uint32_t pad_;
+  uint64_t nfull;        // full-length slices (the tensor maps' outer extent)
 };
+
+constexpr int kTmaRegions = 4;  // regions that get 2-D TMA tensor maps per launch
 
 // Optional slot commit fused into the snapshot kernel: every CTA marks the
 // slot WRITING before its first payload store; the last CTA to finish writes
@@ -35,6 +41,10 @@ struct SlotCommit {
 };
 
 struct SliceJob {
+  // [2*i] = source, [2*i+1] = destination of tensor-mapped region i: a 2-D
+  // view {slice_bytes, nfull} with row pitch slice_bytes, 128 x 32 boxes,
+  // 128-byte swizzle (conflict-free per-lane row reads).
+  CUtensorMap maps[2 * kTmaRegions];
   SliceRegion reg[kMaxRegions];
   uint32_t nregions;
   uint32_t pad_;

@@ -22,6 +22,8 @@
 #include <algorithm>
 #include <cstdlib>
 
+#include <cudaTypedefs.h>
+
 #include "ffx_device.cuh"
 #include "ffx_kernels.h"
 
@@ -93,6 +95,18 @@ __device__ __forceinline__ void bulk_store(void* dst, uint32_t src, uint32_t byt
   asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(src), "r"(bytes)
                : "memory");
 }
+// 2-D tensor TMA (tile mode): one op moves a 128 x 32 box = 4 KB.
+__device__ __forceinline__ void tensor_load(uint32_t dst, const CUtensorMap* map, int x, int y, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+      ::"r"(dst), "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void tensor_store(const CUtensorMap* map, int x, int y, uint32_t src) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.tile.bulk_group [%0, {%1, %2}], [%3];"
+               ::"l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(src)
+               : "memory");
+}
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_read_all() {
   asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
@@ -148,22 +162,27 @@ __device__ __forceinline__ void commit_end(const SlotCommit& c) {
   *c.done = 0;
 }
 
-template <int C, int S, int W>
+template <int C, int S, int W, bool kTensor>
 struct Cfg {
-  static constexpr int VPL = C / 16;        // 16-byte vectors per row
-  static constexpr int ROWB = C + 16;       // padded row (bytes)
-  static constexpr int STAGE = 32 * ROWB;   // one step of one warp
-  static constexpr int WARPB = S * STAGE;
-  static constexpr int BARB = ((W * S * 8 + 127) / 128) * 128;
-  static constexpr int SMEM = BARB + W * WARPB;
+  static constexpr int VPL = C / 16;  // 16-byte vectors per row
+  // Row-copy stages pad each row by 16 bytes; tensor-TMA stages are dense
+  // 4 KB tiles whose 128-byte swizzle does the bank spreading instead.
+  static constexpr int ROWB = kTensor ? C : C + 16;
+  static constexpr int STAGE = 32 * ROWB;
+  static constexpr int WARPB = S * STAGE > 32 * (C + 16) ? S * STAGE : 32 * (C + 16);
+  static constexpr int ALIGN = kTensor ? 1024 : 128;
+  static constexpr int BARB = ((W * S * 8 + ALIGN - 1) / ALIGN) * ALIGN;
+  static constexpr int SMEM = BARB + W * WARPB + ALIGN;  // + slack to align the base
 };
 
-template <int C, int S, int W, SliceMode M, bool kCommit>
+template <int C, int S, int W, bool kTensor, SliceMode M, bool kCommit>
 __global__ void __launch_bounds__(W * 32) slice_kernel(const __grid_constant__ SliceJob job) {
-  using K = Cfg<C, S, W>;
+  using K = Cfg<C, S, W, kTensor>;
+  static_assert(!kTensor || C == 128, "tensor tiles are 128-byte rows");
   constexpr bool kCopy = (M == SliceMode::Copy || M == SliceMode::CopyVerify);
   constexpr bool kVerify = (M == SliceMode::CopyVerify || M == SliceMode::HashVerify);
-  extern __shared__ __align__(128) uint8_t smem[];
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((K::ALIGN - (smem_u32(smem_raw) & (K::ALIGN - 1))) & (K::ALIGN - 1));
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   uint8_t* wbase = smem + K::BARB + warp * K::WARPB;
@@ -213,7 +232,46 @@ __global__ void __launch_bounds__(W * 32) slice_kernel(const __grid_constant__ S
     if constexpr (kCopy) bulk_wait_read_all();
     __syncwarp();
 
-    if (al && base0 + 32 * Sl <= R.bytes) {
+    if (kTensor && R.tmap >= 0 && s0 + 32 <= R.nfull) {
+      // ---- 2-D tensor TMA: one 128 x 32 box per step (4 KB), swizzled ---------------
+      const CUtensorMap* msrc = &job.maps[2 * R.tmap];
+      const CUtensorMap* mdst = &job.maps[2 * R.tmap + 1];
+      const int nsteps = static_cast<int>(Sl / C);
+      const int y = static_cast<int>(s0);
+      const int pro = nsteps < S ? nsteps : S;
+      if (lane == 0) {
+        fence_async_smem();
+        for (int k = 0; k < pro; ++k) {
+          mbar_expect_tx(bar0 + 8 * k, 32 * C);
+          tensor_load(stage0 + k * K::STAGE, msrc, k * C, y, bar0 + 8 * k);
+        }
+      }
+      const int sw = lane & 7;
+      for (int k = 0; k < nsteps; ++k) {
+        const int s = k % S;
+        mbar_wait(bar0 + 8 * s, (phase >> s) & 1u);
+        phase ^= 1u << s;
+        const uint32_t tile = stage0 + s * K::STAGE;
+        if constexpr (kCopy) {
+          if (lane == 0) {
+            tensor_store(mdst, k * C, y, tile);
+            bulk_commit();
+          }
+        }
+        const uint8_t* row = wbase + s * K::STAGE + lane * C;
+#pragma unroll
+        for (int w = 0; w < K::VPL; ++w) h.vec(*reinterpret_cast<const uint4*>(row + ((w ^ sw) << 4)));
+        if (k + S < nsteps) {
+          __syncwarp();
+          if (lane == 0) {
+            if constexpr (kCopy) bulk_wait_read_all();
+            fence_async_smem();
+            mbar_expect_tx(bar0 + 8 * s, 32 * C);
+            tensor_load(tile, msrc, (k + S) * C, y, bar0 + 8 * s);
+          }
+        }
+      }
+    } else if (!kTensor && al && base0 + 32 * Sl <= R.bytes) {
       // ---- TMA pipeline: 32 full slices --------------------------------------------
       const int nsteps = static_cast<int>(Sl / C);
       const uint8_t* src = R.src + my_off;
@@ -266,11 +324,11 @@ __global__ void __launch_bounds__(W * 32) slice_kernel(const __grid_constant__ S
 #pragma unroll
         for (int i = 0; i < K::VPL; ++i) {
           const int q = i * 32 + lane;
-          rows[(q / K::VPL) * (K::ROWB / 16) + (q % K::VPL)] = buf[i];
+          rows[(q / K::VPL) * (K::VPL + 1) + (q % K::VPL)] = buf[i];
         }
         __syncwarp();
         const int64_t rem = static_cast<int64_t>(my_len) - static_cast<int64_t>(k) * C;
-        const uint4* rp = rows + lane * (K::ROWB / 16);
+        const uint4* rp = rows + lane * (K::VPL + 1);
         if (rem >= C) {
 #pragma unroll
           for (int w = 0; w < K::VPL; ++w) h.vec(rp[w]);
@@ -313,10 +371,10 @@ __global__ void __launch_bounds__(W * 32) slice_kernel(const __grid_constant__ S
 
 int g_sms = 0;
 
-template <int C, int S, int W, SliceMode M, bool kCommit>
+template <int C, int S, int W, bool kTensor, SliceMode M, bool kCommit>
 cudaError_t launch_t(const SliceJob& job, uint32_t max_ctas, cudaStream_t stream) {
-  auto kern = slice_kernel<C, S, W, M, kCommit>;
-  constexpr int smem = Cfg<C, S, W>::SMEM;
+  auto kern = slice_kernel<C, S, W, kTensor, M, kCommit>;
+  constexpr int smem = Cfg<C, S, W, kTensor>::SMEM;
   static int occ = 0;
   if (occ == 0) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -345,10 +403,11 @@ int variant() {
 template <SliceMode M, bool kCommit>
 cudaError_t launch_mode(const SliceJob& job, uint32_t max_ctas, cudaStream_t stream) {
   switch (variant()) {
-    case 1: return launch_t<128, 3, 4, M, kCommit>(job, max_ctas, stream);
-    case 2: return launch_t<256, 3, 2, M, kCommit>(job, max_ctas, stream);
-    case 3: return launch_t<64, 6, 4, M, kCommit>(job, max_ctas, stream);
-    default: return launch_t<128, 4, 4, M, kCommit>(job, max_ctas, stream);
+    case 1: return launch_t<128, 3, 4, false, M, kCommit>(job, max_ctas, stream);
+    case 2: return launch_t<128, 4, 4, false, M, kCommit>(job, max_ctas, stream);
+    case 3: return launch_t<128, 6, 4, true, M, kCommit>(job, max_ctas, stream);
+    case 4: return launch_t<128, 8, 4, true, M, kCommit>(job, max_ctas, stream);
+    default: return launch_t<128, 4, 4, true, M, kCommit>(job, max_ctas, stream);
   }
 }
 
@@ -373,14 +432,64 @@ void finalize_job(SliceJob& job) {
     slices += ns;
     groups += (ns + 31) / 32;
   }
-  for (uint32_t r = job.nregions; r < kMaxRegions; ++r) job.reg[r] = SliceRegion{nullptr, nullptr, 0, slices, ~0ull};
+  for (uint32_t r = job.nregions; r < kMaxRegions; ++r)
+    job.reg[r] = SliceRegion{nullptr, nullptr, 0, slices, ~0ull, -1, 0, 0};
+  for (uint32_t r = 0; r < kMaxRegions; ++r) job.reg[r].tmap = -1;
   job.total_groups = groups;
   job.group_lo = 0;
   job.group_hi = groups;
 }
 
-cudaError_t launch_slices(const SliceJob& job, SliceMode mode, bool commit, uint32_t max_ctas,
+namespace {
+
+PFN_cuTensorMapEncodeTiled_v12000 encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      p = nullptr;
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }();
+  return fn;
+}
+
+bool encode_rows(CUtensorMap* map, const void* base, uint64_t slice_bytes, uint64_t nfull) {
+  auto enc = encoder();
+  if (!enc) return false;
+  const cuuint64_t dims[2] = {slice_bytes, nfull};
+  const cuuint64_t strides[1] = {slice_bytes};
+  const cuuint32_t box[2] = {128, 32};
+  const cuuint32_t estr[2] = {1, 1};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+}  // namespace
+
+// Give the (up to kTmaRegions) largest eligible regions 2-D tensor maps.
+void attach_tensor_maps(SliceJob& job, bool copy) {
+  for (uint32_t r = 0; r < kMaxRegions; ++r) job.reg[r].tmap = -1;
+  if (job.slice_bytes % 128 != 0 || job.slice_bytes > (1ull << 31)) return;
+  int used = 0;
+  for (uint32_t r = 0; r < job.nregions && used < kTmaRegions; ++r) {
+    SliceRegion& R = job.reg[r];
+    R.nfull = R.bytes / job.slice_bytes;
+    const bool al = (reinterpret_cast<uintptr_t>(R.src) % 16 == 0) &&
+                    (!copy || reinterpret_cast<uintptr_t>(R.dst) % 16 == 0);
+    if (!al || R.nfull < 32 || R.nfull > (1ull << 31)) continue;
+    if (!encode_rows(&job.maps[2 * used], R.src, job.slice_bytes, R.nfull)) continue;
+    if (copy && !encode_rows(&job.maps[2 * used + 1], R.dst, job.slice_bytes, R.nfull)) continue;
+    R.tmap = used++;
+  }
+}
+
+cudaError_t launch_slices(const SliceJob& job_in, SliceMode mode, bool commit, uint32_t max_ctas,
                           cudaStream_t stream) {
+  SliceJob job = job_in;
+  const int v = variant();
+  if (v == 0 || v >= 3) attach_tensor_maps(job, mode == SliceMode::Copy || mode == SliceMode::CopyVerify);
   switch (mode) {
     case SliceMode::Hash: return launch_mode<SliceMode::Hash, false>(job, max_ctas, stream);
     case SliceMode::Copy:

@@ -230,6 +230,8 @@ SIGNATURES = {
     "ffx_replica_export_frame": (_I, [_P, _U64, _P, _U64, ctypes.POINTER(_U64), _P]),
     "ffx_snapshot_target": (_I, [_P, _P]),
     "ffx_snapshot": (_I, [_P, _U64, _P, ctypes.POINTER(SnapshotOpts)]),
+    "ffx_snapshot_begin": (_I, [_P, _U64, ctypes.POINTER(SnapshotOpts), ctypes.POINTER(_U32)]),
+    "ffx_snapshot_next": (_I, [_P, _P, _P, ctypes.POINTER(_U32)]),
     "ffx_snapshot_read_sums": (_I, [_P, _P, _U64, ctypes.POINTER(_U64), _P]),
     "ffx_recover": (_I, [_P, _P, _U64, _P, ctypes.POINTER(RecoverReport)]),
     "ffx_recover_region": (_I, [_P, _U32, _P, _P, _P, ctypes.POINTER(RecoverReport)]),
@@ -591,6 +593,25 @@ class Context:
                                                           for e in gate_events])
             o.gate_events = ctypes.cast(arr, ctypes.c_void_p)
         check(lib.ffx_snapshot(self._c, iteration, _stream_ptr(stream), ctypes.byref(o)), "snapshot")
+
+    def snapshot_begin(self, iteration: int, batches: int = 1, max_ctas: int = 0,
+                       verify_on_store: bool = False) -> int:
+        o = SnapshotOpts()
+        o.max_ctas = max_ctas
+        o.batches = batches
+        o.verify_on_store = int(verify_on_store)
+        n = ctypes.c_uint32()
+        check(lib.ffx_snapshot_begin(self._c, iteration, ctypes.byref(o), ctypes.byref(n)), "snapshot_begin")
+        return n.value
+
+    def snapshot_next(self, stream=None, gate_event=None) -> int:
+        """Issue the next batch; returns how many remain."""
+        left = ctypes.c_uint32()
+        ev = None
+        if gate_event is not None:
+            ev = gate_event.cuda_event if hasattr(gate_event, "cuda_event") else gate_event
+        check(lib.ffx_snapshot_next(self._c, _stream_ptr(stream), ev, ctypes.byref(left)), "snapshot_next")
+        return left.value
 
     def read_sums(self, host_tensor, stream=None) -> int:
         """D2H of the last snapshot's checksum table into a (pinned) int64 tensor."""

@@ -307,3 +307,29 @@ def test_full_size_gpt2xl_shard_roundtrip(ffx):
         want = orc.materialize_range(d, n, lo, ln)
         assert host(state[lo:lo + ln]) == want
         assert tab[s] == orc.fnv1a64(want)
+
+
+def test_scheduler_begin_next_gated(ffx):
+    # The slice scheduler driven step by step from a training loop: each batch
+    # waits on an event the "train" stream records when a gap opens.
+    n = (1 << 23) + 4097
+    spec, holder, origin, rep, view = ring_pair(ffx, n)
+    state, want = blob_for(ffx, 1, n)
+    origin.register(ffx.REGION_BLOB, state)
+    train = torch.cuda.Stream()
+    low = torch.cuda.Stream(priority=0)
+    nb = origin.snapshot_begin(30, batches=5, max_ctas=8)
+    assert nb == 5
+    x = torch.randn(1024, 1024, device="cuda")
+    left = nb
+    while left:
+        with torch.cuda.stream(train):
+            x = x @ x.T / 1024.0  # a "compute phase"
+            ev = torch.cuda.Event()
+            ev.record(train)
+        left = origin.snapshot_next(stream=low, gate_event=ev)
+    low.synchronize()
+    assert rep.newest() == 30
+    assert rep.export_frame(30) == orc.pack_blob((1, 0, 0), 30, 1, want)
+    with pytest.raises(ffx.StateError):
+        origin.snapshot_next(stream=low)
