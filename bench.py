@@ -1,25 +1,33 @@
 #!/usr/bin/env python3
-"""bench.py -- per-iteration neighbour snapshot (+ recovery) throughput.
+"""bench.py -- per-iteration neighbour snapshot (+ recovery, + step overhead).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ffx|reference]
+    (N > 1: python -m torch.distributed.run --nproc-per-node N bench.py --gpus N)
 
-Workload (BASELINE.json configs[1]): the GPT-2 XL ZeRO-1 shard a DP rank
-owns at d=8 -- N = ceil(12 * 1,557,611,200 / 8) = 2,336,416,800 bytes of
+Headline workload (BASELINE.json configs[1]): the GPT-2 XL ZeRO-1 shard a DP
+rank owns at d=8 -- N = ceil(12 * 1,557,611,200 / 8) = 2,336,416,800 bytes of
 unique Adam state (evo::optimizer_bytes, reference evolution.cpp:15-19),
 synthesised on the device as evo::materialize(optimizer_init(42, role), N).
 
-One step = one per-iteration snapshot of every rank's N bytes into its
-replica slot with fused per-slice FNV-1a-64 (the reference's
-HostSnapshots::take + ring stream + NeighborBuffer::store):
-  N = 1: into a local replica on the same B200 (HBM-bound: 2N bytes).
+One step = one per-iteration snapshot of every rank's N bytes into its replica
+slot with fused per-slice FNV-1a-64 (the reference's HostSnapshots::take +
+ring stream + NeighborBuffer::store):
+  N = 1: into a local replica on the same B200 (HBM-bound: 2N bytes moved).
   N > 1: into the ring successor's replica over NVLink (weak scaling: every
-         rank moves its own N bytes; one process per GPU, torchrun).
+         rank moves its own N bytes; one process per GPU).
 Inputs (2.3 GB per rank) exceed the 126 MB L2, so no flush is needed.
 
-Also reported on the same line: recovery (pull + verify of a failed rank's
-N bytes from its holder), the end-to-end path through the reference-facing
-call with host buffers (e2e), the dominant kernel's roofline, the reference
-CPU path timed on this host (cpu_baseline), and clocks under load.
+Also on the same JSON line:
+  recovery       rank 1 loses its state and pulls + verifies it from its holder;
+  llama3_8b      (N > 1) configs[2]/[3]: single-rank recovery of a Llama-3 8B
+                 ZeRO-3 shard (12phi/8 fp32 Adam + 2phi/8 bf16 params) and the
+                 step-time overhead of snapshotting it inside a synthetic
+                 ZeRO-3 step's gaps (slice scheduler);
+  e2e            the same snapshot through the reference-facing call with host
+                 buffers (H2D of the state + D2H of the checksum table);
+  roofline       the snapshot kernel against measured HBM / NVLink peaks;
+  cpu_baseline   the reference's own C++ (oracle/_ref) on this host's cores;
+  clocks         nvidia-smi during the timed region.
 """
 import argparse
 import ctypes
@@ -33,11 +41,13 @@ import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "oracle"))
 
 PHI_GPT2_XL = 1_557_611_200
+PHI_LLAMA3_8B = 8_030_261_248
 D_REF = 8
-PEAKS_FALLBACK = {"hbm_gbs": 6650.0}
 NVLINK_MEASURED_GBS = 770.0  # B200_PROFILING.md: measured peer copy per direction (900 nominal)
+PEAKS_FALLBACK = {"hbm_gbs": 6650.0}
 
 
 def parse():
@@ -51,22 +61,16 @@ def parse():
     ap.add_argument("--bytes", type=int, default=0, help="override bytes per rank (debug)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-llama", action="store_true", help="skip the Llama-3 8B recovery/overhead legs")
+    ap.add_argument("--sched-ctas", type=int, default=32, help="SM budget of scheduled snapshot batches")
     return ap.parse_args()
-
-
-def workload_bytes(args):
-    if args.bytes:
-        return args.bytes
-    full = 12 * PHI_GPT2_XL
-    return (full + D_REF - 1) // D_REF
 
 
 def measured_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
         with open(p) as f:
-            d = json.load(f)
-        return d, "MEASURED_PEAKS.json"
+            return json.load(f), "MEASURED_PEAKS.json"
     return PEAKS_FALLBACK, "fallback (B200_PROFILING.md)"
 
 
@@ -78,9 +82,7 @@ class ClockSampler:
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
     def __init__(self, index):
-        self.index = index
-        self.proc = None
-        self.lines = []
+        self.index, self.proc, self.lines = index, None, []
 
     def start(self):
         try:
@@ -88,8 +90,7 @@ class ClockSampler:
                 ["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.FIELDS,
                  "--format=csv,noheader,nounits", "-lms", "100"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
-            self.t.start()
+            threading.Thread(target=self._read, daemon=True).start()
         except Exception:
             self.proc = None
 
@@ -128,7 +129,6 @@ class ClockSampler:
 # reference CPU path (oracle/_ref: the reference's own C++ compiled here)
 
 def cpu_ring(threads, bytes_per_thread, iters):
-    sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import pyoracle
     ref = pyoracle.ref_lib()
     if ref is None:
@@ -136,12 +136,13 @@ def cpu_ring(threads, bytes_per_thread, iters):
     h = ref.ref_ring_setup(threads, bytes_per_thread)
     secs = (ctypes.c_double * 4)()
     out = []
-    for i in range(iters):
-        rc = ref.ref_ring_run(h, i + 1, secs)
-        if rc != 0:
-            raise RuntimeError("reference ring iteration failed")
-        out.append(tuple(secs[k] for k in range(4)))
-    ref.ref_ring_free(h)
+    try:
+        for i in range(iters):
+            if ref.ref_ring_run(h, i + 1, secs) != 0:
+                raise RuntimeError("reference ring iteration failed")
+            out.append(tuple(secs[k] for k in range(4)))
+    finally:
+        ref.ref_ring_free(h)
     return out
 
 
@@ -154,47 +155,104 @@ def cpu_baseline_line(threads, bytes_per_thread, iters=2):
     restore = min(r[2] for r in res)
     agg = threads * bytes_per_thread
     return {
-        "value": round(agg / (take + store) / 1e9, 3), "unit": "GB/s",
-        "cores": threads, "kind": "reference",
-        "sample": "%d threads x %d MiB: HostSnapshots::take + NeighborBuffer::store (snapshot), "
-                  "assemble_restore timed separately; reference proj/src compiled -O3 into oracle/_ref"
-                  % (threads, bytes_per_thread >> 20),
+        "value": round(agg / (take + store) / 1e9, 3), "unit": "GB/s", "cores": threads, "kind": "reference",
+        "sample": "%d threads x %d MiB per rank: HostSnapshots::take + NeighborBuffer::store (the snapshot); "
+                  "reference proj/src compiled -O3 into oracle/_ref" % (threads, bytes_per_thread >> 20),
         "stages_gbs": {"take": round(agg / take / 1e9, 3), "store": round(agg / store / 1e9, 3),
                        "restore": round(agg / restore / 1e9, 3)},
     }
 
 
 def run_reference(args):
-    rank = int(os.environ.get("RANK", "0"))
-    if rank != 0:
+    if int(os.environ.get("RANK", "0")) != 0:
         return
     threads = os.cpu_count() or 1
     per = 256 << 20
-    steps, warmup = args.steps, args.warmup
-    # bounded sample: each step is one ring iteration over `threads` ranks of `per` bytes
-    res = cpu_ring(threads, per, max(1, warmup) + steps)
-    res = res[max(1, warmup):]
+    res = cpu_ring(threads, per, max(1, args.warmup) + args.steps)
+    if res is None:
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built (needs the reference checkout)"}))
+        return
+    res = res[max(1, args.warmup):]
     agg = threads * per
-    snap_s = [r[0] + r[1] for r in res]
-    t = sum(snap_s)
+    t = sum(r[0] + r[1] for r in res)
     value = agg * len(res) / t / 1e9
-    line = {
+    print(json.dumps({
         "impl": "reference", "metric": "snapshot GB/s (per-iteration neighbour backup, all ranks)",
-        "value": round(value, 3), "unit": "GB/s", "n_gpus": args.gpus, "steps": steps, "warmup": warmup,
-        "ms_per_step": round(1e3 * t / len(res), 3), "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "u8", "data": "synthetic (evo::materialize, seed 42)",
-        "config": {"workload": "reference CPU path on a bounded sample of the GPT-2 XL ZeRO-1 d=8 shard",
+        "value": round(value, 3), "unit": "GB/s", "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(1e3 * t / len(res), 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic (evo::materialize, seed 42)",
+        "config": {"workload": "reference CPU path (HostSnapshots::take + NeighborBuffer::store) on a bounded "
+                               "sample of the GPT-2 XL ZeRO-1 d=8 shard, one thread per ring rank",
                    "bytes_per_rank_sample": per, "ranks": threads},
         "cpu_baseline": {"value": round(value, 3), "unit": "GB/s", "cores": threads, "kind": "reference",
-                         "sample": "%d threads x 256 MiB per step (HostSnapshots::take + NeighborBuffer::store)" % threads},
+                         "sample": "%d threads x 256 MiB per step" % threads},
         "e2e": {"value": round(value, 3), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "restore_gbs": round(agg * len(res) / sum(r[2] for r in res) / 1e9, 3),
-    }
-    print(json.dumps(line), flush=True)
+    }), flush=True)
 
 
 # ---------------------------------------------------------------------------
 # B200 path
+
+class Ring:
+    """This rank's ffx context, its state, the replica it holds for its ring
+    predecessor and the view of the replica its successor holds for it."""
+
+    def __init__(self, ffx, torch, dist, world, rank, local, n, spec, slice_bytes, regions):
+        from paper_2512_03644_b200 import ring
+        import pyoracle
+        self.ffx, self.n = ffx, n
+        self.ctx = ffx.Context(local, spec, ffx.Role(rank, 0, 0), slice_bytes)
+        self.holder = None
+        if world == 1:
+            # the ring collapses onto one GPU: a second context plays the holder
+            self.holder = ffx.Context(local, spec, ffx.Role(1, 0, 0), slice_bytes)
+            self.held = self.holder.create_replica(ffx.Role(rank, 0, 0), n, 2)
+            self.target = self.ctx.open_replica(self.held.export())
+            self.handles = None
+        else:
+            def all_gather(b):
+                out = [None] * world
+                dist.all_gather_object(out, b)
+                return out
+            held, targets, handles = ring.wire_ring(
+                rank, world, lambda origin: self.ctx.create_replica(ffx.Role(origin, 0, 0), n, 2),
+                lambda r: r.export(), self.ctx.open_replica, all_gather)
+            self.held, self.target, self.handles = held[0], targets[0], handles
+        self.ctx.set_target(self.target)
+        self.state = []
+        for kind, nbytes, digest in regions(rank):
+            t = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+            ffx.materialize(t, digest)
+            self.ctx.register(kind, t)
+            self.state.append(t)
+        del pyoracle
+
+    def close(self):
+        for r in (self.target, self.held):
+            try:
+                r.destroy()
+            except Exception:
+                pass
+        self.ctx.close()
+        if self.holder:
+            self.holder.close()
+
+
+def gpt2xl_regions(n):
+    import pyoracle
+    ffx = __import__("paper_2512_03644_b200.ffx", fromlist=["ffx"])
+    return lambda rank: [(ffx.REGION_BLOB, n, pyoracle.optimizer_init(42, rank, 0, 0, True))]
+
+
+def llama_regions(world):
+    import pyoracle
+    ffx = __import__("paper_2512_03644_b200.ffx", fromlist=["ffx"])
+    adam = (12 * PHI_LLAMA3_8B + D_REF - 1) // D_REF     # fp32 master + m + v shard (ZeRO-3, d=8)
+    params = (2 * PHI_LLAMA3_8B + D_REF - 1) // D_REF    # bf16 param shard: unique under ZeRO-3
+    return (lambda rank: [(ffx.REGION_BLOB, adam, pyoracle.optimizer_init(42, rank, 0, 0, True)),
+                          (ffx.REGION_PARAMS, params, pyoracle.weights_init(42 + rank, 0, 0))]), adam + params
+
 
 def main():
     args = parse()
@@ -203,8 +261,6 @@ def main():
 
     import torch
     import torch.distributed as dist
-
-    sys.path.insert(0, os.path.join(ROOT, "oracle"))
     from paper_2512_03644_b200 import ffx
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -214,50 +270,29 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
-    n = workload_bytes(args)
-    d = max(world, 2)
-    spec = ffx.make_spec(d=d, phi=PHI_GPT2_XL, distributed=True)
-    me = ffx.Role(rank, 0, 0)
-    pred = (rank - 1) % world if world > 1 else rank
-    ctx = ffx.Context(local, spec, me, args.slice_bytes)
-    if world == 1:
-        holder = ffx.Context(local, spec, ffx.Role(1, 0, 0), args.slice_bytes)
-        replica = holder.create_replica(me, n, 2)
-        target = ctx.open_replica(replica.export())
-        succ_replica = target
-    else:
-        holder = None
-        replica = ctx.create_replica(ffx.Role(pred, 0, 0), n, 2)  # I hold my predecessor's snapshots
-        handles = [None] * world
-        dist.all_gather_object(handles, replica.export())
-        target = ctx.open_replica(handles[(rank + 1) % world])  # my successor holds mine
-        succ_replica = target
-    ctx.set_target(target)
-
-    import hashlib
-    digest = hashlib.sha256(b"O0-%d" % rank).digest()
-    sys.path.insert(0, os.path.join(ROOT, "oracle"))
-    try:
-        import pyoracle
-        digest = pyoracle.optimizer_init(42, rank, 0, 0, True)
-    except Exception:
-        pass
-    state = torch.empty(n, dtype=torch.uint8, device="cuda")
-    ffx.materialize(state, digest)
-    ctx.register(ffx.REGION_BLOB, state)
-    stream = torch.cuda.Stream()
-    torch.cuda.synchronize()
-
     def barrier():
         if world > 1:
             dist.barrier()
 
+    def max_over_ranks(x):
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    n = args.bytes or (12 * PHI_GPT2_XL + D_REF - 1) // D_REF
+    spec = ffx.make_spec(d=max(world, 2), phi=PHI_GPT2_XL, distributed=True)
+    R = Ring(ffx, torch, dist, world, rank, local, n, spec, args.slice_bytes, gpt2xl_regions(n))
+    stream = torch.cuda.Stream()
+    torch.cuda.synchronize()
+
+    # ---- timed snapshot loop ------------------------------------------------
     it = 0
     for _ in range(args.warmup):
         it += 1
-        ctx.snapshot(it, stream=stream, max_ctas=args.max_ctas)
+        R.ctx.snapshot(it, stream=stream, max_ctas=args.max_ctas)
     stream.synchronize()
-    launches0 = ctx.stats().kernel_launches
+    launches0 = R.ctx.stats().kernel_launches
     barrier()
     torch.cuda.synchronize()
     clocks = ClockSampler(local)
@@ -267,47 +302,38 @@ def main():
     e0.record(stream)
     for _ in range(args.steps):
         it += 1
-        ctx.snapshot(it, stream=stream, max_ctas=args.max_ctas)
+        R.ctx.snapshot(it, stream=stream, max_ctas=args.max_ctas)
     e1.record(stream)
     stream.synchronize()
-    torch.cuda.synchronize()
     ck = clocks.stop()
     barrier()
-    ms = e0.elapsed_time(e1)
-    launches = ctx.stats().kernel_launches - launches0
-    t_max = torch.tensor([ms], dtype=torch.float64, device="cuda")
-    if world > 1:
-        dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
-    ms_max = float(t_max.item())
+    launches = R.ctx.stats().kernel_launches - launches0
+    ms_max = max_over_ranks(e0.elapsed_time(e1))
     per_step_ms = ms_max / args.steps
     value = world * n * args.steps / (ms_max * 1e-3) / 1e9
-
-    # correctness of the last snapshot: holder-side slot committed at `it`
-    ok_commit = target.newest() == it
+    commit_ok = R.target.newest() == it
 
     # ---- recovery: rank (1 % world) loses its state and pulls it back --------
     fail_rank = 1 % world
     rec = {}
     barrier()
     if rank == fail_rank:
-        ctx.inject(ffx.FAULT_POISON_STATE)
-        src = target  # holder of my snapshots = my successor (or the local holder)
-        rpt = ctx.recover(src, it, stream=stream)
-        sound = ffx.blob_is_sound(state)
-        rec = {"recovery_s": rpt.seconds, "recovery_gbs": n / rpt.seconds / 1e9,
-               "recovery_verified": bool(sound and rpt.bad_slices == 0)}
+        R.ctx.inject(ffx.FAULT_POISON_STATE)
+        rpt = R.ctx.recover(R.target, it, stream=stream)
+        rec = {"recovery_s": rpt.seconds, "recovery_gbs": round(n / rpt.seconds / 1e9, 2),
+               "recovery_verified": bool(ffx.blob_is_sound(R.state[0]) and rpt.bad_slices == 0),
+               "source": "local replica" if world == 1 else "ring successor over NVLink"}
     barrier()
-    recs = [rec]
     if world > 1:
         recs = [None] * world
         dist.all_gather_object(recs, rec)
-    rec = recs[fail_rank]
+        rec = recs[fail_rank]
 
-    # ---- e2e: the reference-facing call with host buffers --------------------
+    # ---- e2e: the reference-facing call with host buffers ---------------------
     e2e = None
     if not args.no_e2e:
         host = torch.empty(n, dtype=torch.uint8, pin_memory=True)
-        host.copy_(state, non_blocking=False)
+        host.copy_(R.state[0])
         nsl = (n + args.slice_bytes - 1) // args.slice_bytes
         table_host = torch.empty(nsl, dtype=torch.int64, pin_memory=True)
         k = max(2, min(args.steps, 6))
@@ -319,29 +345,28 @@ def main():
                 if j == 1:
                     f0.record(stream)
                 it += 1
-                state.copy_(host, non_blocking=True)               # H2D: take(it, host_ptr, len)
-                ctx.snapshot(it, stream=stream, max_ctas=args.max_ctas)
-                ctx.read_sums(table_host, stream=stream)           # D2H of the step's result
+                R.state[0].copy_(host, non_blocking=True)        # take(it, host_ptr, len): H2D
+                R.ctx.snapshot(it, stream=stream, max_ctas=args.max_ctas)
+                R.ctx.read_sums(table_host, stream=stream)       # D2H of the step's result
             f1.record(stream)
         stream.synchronize()
-        ems = f0.elapsed_time(f1)
-        t = torch.tensor([ems], dtype=torch.float64, device="cuda")
-        if world > 1:
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e = {"value": round(world * n * k / (float(t.item()) * 1e-3) / 1e9, 3), "unit": "GB/s",
+        ems = max_over_ranks(f0.elapsed_time(f1))
+        e2e = {"value": round(world * n * k / (ems * 1e-3) / 1e9, 3), "unit": "GB/s",
                "h2d_bytes_per_step": n, "d2h_bytes_per_step": nsl * 8,
-               "path": "pinned host state -> H2D -> ffx_snapshot -> D2H checksum table (HostSnapshots::take semantics)"}
+               "path": "pinned host state -> H2D -> ffx_snapshot -> D2H checksum table "
+                       "(HostSnapshots::take(it, host_ptr, len) semantics)"}
+        del host, table_host
 
     peaks, peak_src = measured_peaks()
     if world == 1:
         roof = {"bound": "hbm", "achieved": round(2 * n / (per_step_ms * 1e-3) / 1e9, 1),
-                "peak": peaks.get("hbm_gbs"), "unit": "GB/s",
-                "traffic": None, "kernel": "slice_kernel<Copy,commit> (copy + per-slice FNV-1a)",
-                "algorithmic_bytes_per_launch": 2 * n, "peak_source": peak_src}
+                "peak": peaks.get("hbm_gbs"), "unit": "GB/s", "traffic": None,
+                "kernel": "slice_kernel<Copy,commit>: TMA copy + per-slice FNV-1a",
+                "algorithmic_bytes_per_launch": 2 * n, "peak_source": peak_src + " (copy read+write)"}
     else:
         roof = {"bound": "nvlink", "achieved": round(n / (per_step_ms * 1e-3) / 1e9, 1),
                 "peak": NVLINK_MEASURED_GBS, "unit": "GB/s", "traffic": None,
-                "kernel": "slice_kernel<Copy,commit> (peer stores + per-slice FNV-1a)",
+                "kernel": "slice_kernel<Copy,commit>: TMA stores to the peer replica + per-slice FNV-1a",
                 "algorithmic_bytes_per_launch": n,
                 "peak_source": "B200_PROFILING.md measured peer copy per direction (900 nominal)"}
     roof["frac"] = round(roof["achieved"] / roof["peak"], 4) if roof["peak"] else None
@@ -352,6 +377,14 @@ def main():
         except Exception:
             pass
 
+    R.close()
+    torch.cuda.empty_cache()
+
+    # ---- Llama-3 8B ZeRO-3 (configs[2], [3]): recovery + step overhead -----------
+    llama = None
+    if world > 1 and not args.no_llama:
+        llama = llama_leg(args, ffx, torch, dist, world, rank, local, barrier)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
@@ -360,32 +393,68 @@ def main():
             cpu = {"error": str(ex)}
 
     if rank == 0:
-        line = {
+        print(json.dumps({
             "metric": "snapshot GB/s (per-iteration neighbour backup, all ranks)",
             "value": round(value, 3), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(per_step_ms, 4), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "u8",
             "data": "synthetic (evo::materialize(optimizer_init(42, role)), device-generated)",
-            "config": {"workload": "GPT-2 XL ZeRO-1 d=8 shard (BASELINE configs[1]): %d B/rank unique Adam state, "
-                                   "%s" % (n, "1-GPU local replica" if world == 1 else "ring-neighbour replica over NVLink"),
+            "config": {"workload": "GPT-2 XL ZeRO-1 d=8 shard (BASELINE configs[1]): %d B/rank unique Adam state, %s"
+                                   % (n, "1-GPU local replica" if world == 1 else "ring-neighbour replica over NVLink"),
                        "bytes_per_rank": n, "slice_bytes": args.slice_bytes, "replica_versions": 2,
                        "l2": "inputs 2.3 GB/rank > 126 MB L2; no flush needed",
                        "parallelism": "dp%d ring" % world if world > 1 else "single GPU"},
             "per_gpu_gbs": round(value / world, 3),
             "nvlink_frac_per_gpu": round(value / world / NVLINK_MEASURED_GBS, 4) if world > 1 else None,
-            "roofline": roof,
-            "recovery": rec,
-            "cpu_baseline": cpu,
-            "e2e": e2e,
-            "gpu_launches": int(launches),
-            "clocks": ck,
-            "commit_ok": bool(ok_commit),
-        }
-        print(json.dumps(line), flush=True)
+            "roofline": roof, "recovery": rec, "llama3_8b": llama, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": int(launches), "clocks": ck, "commit_ok": bool(commit_ok),
+        }), flush=True)
 
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def llama_leg(args, ffx, torch, dist, world, rank, local, barrier):
+    from paper_2512_03644_b200.step import SliceScheduler, SyntheticStep, measure_overhead
+    regions, nbytes = llama_regions(world)
+    spec = ffx.make_spec(d=world, phi=PHI_LLAMA3_8B, distributed=True)
+    R = Ring(ffx, torch, dist, world, rank, local, nbytes, spec, args.slice_bytes, regions)
+    s = torch.cuda.Stream()
+    R.ctx.snapshot(1, stream=s)
+    R.ctx.snapshot(2, stream=s)
+    s.synchronize()
+    barrier()
+    out = {"bytes_per_rank": nbytes, "state": "12phi/8 fp32 master+Adam m,v + 2phi/8 bf16 params (ZeRO-3, d=8 shard)"}
+    # single-rank failure (configs[3]): rank 1 pulls both regions back from its holder
+    fail_rank = 1 % world
+    rec = {}
+    if rank == fail_rank:
+        R.ctx.inject(ffx.FAULT_POISON_STATE)
+        t0 = time.perf_counter()
+        rpt = R.ctx.recover(R.target, 2, stream=s)
+        wall = time.perf_counter() - t0
+        ok = rpt.bad_slices == 0 and all(ffx.blob_is_sound(t) for t in R.state)
+        rec = {"recovery_s": round(rpt.seconds, 5), "recovery_wall_s": round(wall, 5),
+               "recovery_gbs": round(nbytes / rpt.seconds / 1e9, 2),
+               "nvlink_frac": round(nbytes / rpt.seconds / 1e9 / NVLINK_MEASURED_GBS, 4),
+               "verified_bit_exact": bool(ok)}
+    barrier()
+    recs = [None] * world
+    dist.all_gather_object(recs, rec)
+    out["recovery"] = recs[fail_rank]
+    # step overhead (configs[2])
+    try:
+        step = SyntheticStep(world)
+        sched = SliceScheduler(R.ctx, step, max_ctas=args.sched_ctas)
+        out["step_overhead"] = measure_overhead(step, sched, steps=6, warmup=2)
+        out["step_overhead"]["sched_ctas"] = args.sched_ctas
+        del step, sched
+    except Exception as ex:
+        out["step_overhead"] = {"error": repr(ex)}
+    R.close()
+    torch.cuda.empty_cache()
+    return out
 
 
 if __name__ == "__main__":
