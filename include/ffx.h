@@ -271,7 +271,18 @@ typedef struct ffx_snapshot_opts {
   void* gate_events;       /* cudaEvent_t[batches] each batch waits on (NULL = none) */
   uint32_t verify_on_store;/* holder-side re-verify after landing (ckpt.cpp:78 semantics) */
   uint32_t weights_kind;   /* nonzero: frame as BlobKind::Weights (0), else Optimizer (1) */
+  /* Split policy: copy and checksum are scheduled separately -- copy batches
+   * (TMA copy-only kernel, max_ctas CTAs, or the copy engines) for the gaps
+   * where NVLink is idle, hash batches (local state -> the slot's checksum
+   * table) for the gaps where SMs are idle.  The slot commits once both
+   * queues drain.  0 = fused copy+checksum batches. */
+  uint32_t split;
+  uint32_t hash_batches;   /* split: hash batches (0 = batches) */
+  uint32_t hash_ctas;      /* split: SM budget of hash batches (0 = whole GPU) */
+  uint32_t copy_engine;    /* split: copy batches by cudaMemcpyAsync (no SMs) */
 } ffx_snapshot_opts;
+
+enum ffx_batch_kind { FFX_BATCH_COPY = 0, FFX_BATCH_HASH = 1 };
 
 /* Snapshot all unique regions into the target replica at `iteration`, async
  * on `stream`.  Slot choice follows the two-version rule: replace the slot
@@ -289,6 +300,9 @@ int ffx_snapshot(ffx_ctx* ctx, uint64_t iteration, void* stream, const ffx_snaps
 int ffx_snapshot_begin(ffx_ctx* ctx, uint64_t iteration, const ffx_snapshot_opts* opts,
                        uint32_t* batches);
 int ffx_snapshot_next(ffx_ctx* ctx, void* stream, void* gate_event, uint32_t* remaining);
+/* Issue the next batch of one kind (split policy: FFX_BATCH_COPY or
+ * FFX_BATCH_HASH; fused snapshots only have copy batches). */
+int ffx_snapshot_next_kind(ffx_ctx* ctx, int kind, void* stream, void* gate_event, uint32_t* remaining);
 
 /* Copy the checksum table written by this ctx's most recent snapshot into
  * host memory (async on `stream`; pinned memory for true overlap).

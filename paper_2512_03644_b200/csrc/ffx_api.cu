@@ -118,10 +118,14 @@ struct ffx_replica {
 // A snapshot split by the slice scheduler into batches still to be issued.
 struct PendingSnapshot {
   bool active = false;
-  SliceJob job{};
+  SliceJob job{};  // fused: copy + hash (+ commit); split: the hash-only job
   uint32_t batches = 1, next = 0, max_ctas = 0, slot = 0;
   uint64_t iteration = 0, seq = 0, nslices = 0, logical = 0;
   bool verify = false;
+  // split policy: copy batches and hash batches drain independently
+  bool split = false, copy_engine = false;
+  CopyJob copy{};
+  uint32_t hbatches = 0, hnext = 0, hash_ctas = 0;
 };
 
 struct ffx_ctx {
@@ -136,6 +140,7 @@ struct ffx_ctx {
   unsigned long long* result = nullptr;    // verify result (device, 2 words)
   unsigned long long* result_host = nullptr;  // pinned mirror
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  cudaEvent_t copy_done = nullptr, hash_done = nullptr;  // split-policy joins
   uint64_t seq = 0;
   uint32_t last_slot = 0;
   uint64_t last_nslices = 0;
@@ -628,6 +633,8 @@ extern "C" int ffx_open(int device, const ffx_cluster_spec* spec, ffx_role self,
   if (e == cudaSuccess) e = cudaMallocHost(&c->result_host, 16);
   if (e == cudaSuccess) e = cudaEventCreate(&c->ev0);
   if (e == cudaSuccess) e = cudaEventCreate(&c->ev1);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->copy_done, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->hash_done, cudaEventDisableTiming);
   if (e != cudaSuccess) {
     ffx_close(c);
     return cuda_fail(e, "open");
@@ -644,6 +651,8 @@ extern "C" int ffx_close(ffx_ctx* c) {
   if (c->result_host) cudaFreeHost(c->result_host);
   if (c->ev0) cudaEventDestroy(c->ev0);
   if (c->ev1) cudaEventDestroy(c->ev1);
+  if (c->copy_done) cudaEventDestroy(c->copy_done);
+  if (c->hash_done) cudaEventDestroy(c->hash_done);
   delete c;
   return FFX_OK;
 }
@@ -1057,6 +1066,21 @@ extern "C" int ffx_snapshot_begin(ffx_ctx* c, uint64_t iteration, const ffx_snap
   P.nslices = nslices;
   P.logical = pm.logical;
   P.verify = opts.verify_on_store != 0;
+  P.split = opts.split != 0;
+  if (P.split) {
+    // Copy batches: TMA copy-only (or copy engines) into the slot payload.
+    P.copy_engine = opts.copy_engine != 0;
+    CopyJob& cj = P.copy;
+    cj.nregions = job.nregions;
+    for (uint32_t i = 0; i < job.nregions; ++i)
+      cj.reg[i] = CopyRegion{job.reg[i].src, job.reg[i].dst, job.reg[i].bytes, 0, 0};
+    finalize_copy_job(cj);
+    cj.mark = SlotMark{t->slot(slot), iteration, seq};
+    // Hash batches: the local state hashed straight into the slot's table.
+    for (uint32_t i = 0; i < job.nregions; ++i) job.reg[i].dst = nullptr;
+    P.hbatches = std::max<uint32_t>(1, opts.hash_batches ? opts.hash_batches : P.batches);
+    P.hash_ctas = opts.hash_ctas;
+  }
   if (batches_out) *batches_out = P.batches;
   return FFX_OK;
 }
@@ -1070,7 +1094,7 @@ int verify_landed(ffx_ctx* c, const PendingSnapshot& P, cudaStream_t s) {
   FFX_CUDA(cudaMemcpyAsync(c->result, init, sizeof init, cudaMemcpyHostToDevice, s));
   SliceJob vj = P.job;
   for (uint32_t i = 0; i < vj.nregions; ++i) {
-    vj.reg[i].src = vj.reg[i].dst;
+    vj.reg[i].src = P.split ? P.copy.reg[i].dst : vj.reg[i].dst;  // the landed payload
     vj.reg[i].dst = nullptr;
   }
   vj.sums_out = nullptr;
@@ -1094,27 +1118,52 @@ int verify_landed(ffx_ctx* c, const PendingSnapshot& P, cudaStream_t s) {
 
 }  // namespace
 
-extern "C" int ffx_snapshot_next(ffx_ctx* c, void* stream, void* gate_event, uint32_t* remaining) {
-  if (!c) return fail(FFX_EINVAL, "snapshot_next: null ctx");
-  PendingSnapshot& P = c->pending;
-  if (!P.active) return fail(FFX_ESTATE, "snapshot_next: no snapshot in progress (ffx_snapshot_begin)");
-  DeviceGuard g(c->device);
-  cudaStream_t s = as_stream(stream);
-  // Batch b covers warp tasks [G*b/B, G*(b+1)/B); the last batch commits.
-  const uint32_t b = P.next++;
-  const uint64_t G = P.job.total_groups;
-  SliceJob bj = P.job;
-  bj.group_lo = G * b / P.batches;
-  bj.group_hi = G * (b + 1) / P.batches;
-  bj.commit.finalize = (b + 1 == P.batches);
-  if (gate_event) FFX_CUDA(cudaStreamWaitEvent(s, static_cast<cudaEvent_t>(gate_event), 0));
-  if (bj.group_lo != bj.group_hi || bj.commit.finalize) {
-    FFX_CUDA(launch_slices(bj, SliceMode::Copy, true, P.max_ctas, s));
-    c->stats.kernel_launches++;
-  }
-  if (remaining) *remaining = P.batches - P.next;
-  if (P.next < P.batches) return FFX_OK;
+namespace {
 
+// Split policy: one copy batch (TMA copy-only kernel, or copy engines).
+int issue_copy_batch(ffx_ctx* c, PendingSnapshot& P, uint32_t b, cudaStream_t s) {
+  CopyJob bj = P.copy;
+  const uint64_t n = P.copy.total_chunks;
+  bj.chunk_lo = n * b / P.batches;
+  bj.chunk_hi = n * (b + 1) / P.batches;
+  if (bj.chunk_lo == bj.chunk_hi) return FFX_OK;
+  if (!P.copy_engine) {
+    FFX_CUDA(launch_copy(bj, P.max_ctas, s));
+    c->stats.kernel_launches++;
+    return FFX_OK;
+  }
+  // Copy engines: no SMs at all.  Mark WRITING first with a (tiny) copy
+  // kernel over zero chunks, then one cudaMemcpyAsync per region piece.
+  CopyJob mark = bj;
+  mark.chunk_lo = mark.chunk_hi = 0;
+  FFX_CUDA(launch_copy(mark, 1, s));
+  for (uint32_t r = 0; r < bj.nregions; ++r) {
+    const uint64_t c0 = std::max(bj.chunk_lo, bj.chunk_base[r]);
+    const uint64_t cend = (r + 1 < bj.nregions) ? bj.chunk_base[r + 1] : bj.total_chunks;
+    const uint64_t c1 = std::min(bj.chunk_hi, cend);
+    if (c0 >= c1) continue;
+    const uint64_t off = (c0 - bj.chunk_base[r]) * (32 * 1024);
+    const uint64_t end = std::min(bj.reg[r].bytes, (c1 - bj.chunk_base[r]) * (32 * 1024));
+    FFX_CUDA(cudaMemcpyAsync(bj.reg[r].dst + off, bj.reg[r].src + off, end - off, cudaMemcpyDefault, s));
+  }
+  return FFX_OK;
+}
+
+// Split policy: one hash batch (local state -> checksum table in the slot).
+int issue_hash_batch(ffx_ctx* c, PendingSnapshot& P, uint32_t b, cudaStream_t s) {
+  SliceJob hj = P.job;
+  const uint64_t G = P.job.total_groups;
+  hj.group_lo = G * b / P.hbatches;
+  hj.group_hi = G * (b + 1) / P.hbatches;
+  hj.commit.finalize = 0;
+  hj.sched = c->done + 16;
+  if (hj.group_lo == hj.group_hi) return FFX_OK;
+  FFX_CUDA(launch_slices(hj, SliceMode::Hash, true, P.hash_ctas, s));
+  c->stats.kernel_launches++;
+  return FFX_OK;
+}
+
+int finish_snapshot(ffx_ctx* c, PendingSnapshot& P, cudaStream_t s) {
   P.active = false;
   ffx_replica* t = c->target;
   t->cache[P.slot] = SlotCache{true, kSlotCommitted, P.iteration, P.seq};
@@ -1125,14 +1174,74 @@ extern "C" int ffx_snapshot_next(ffx_ctx* c, void* stream, void* gate_event, uin
   return P.verify ? verify_landed(c, P, s) : FFX_OK;
 }
 
+}  // namespace
+
+extern "C" int ffx_snapshot_next_kind(ffx_ctx* c, int kind, void* stream, void* gate_event,
+                                      uint32_t* remaining) {
+  if (!c) return fail(FFX_EINVAL, "snapshot_next: null ctx");
+  PendingSnapshot& P = c->pending;
+  if (!P.active) return fail(FFX_ESTATE, "snapshot_next: no snapshot in progress (ffx_snapshot_begin)");
+  if (kind != FFX_BATCH_COPY && kind != FFX_BATCH_HASH) return fail(FFX_EINVAL, "snapshot_next: kind %d", kind);
+  if (kind == FFX_BATCH_HASH && !P.split) return fail(FFX_ESTATE, "snapshot_next: hash batches need opts.split");
+  DeviceGuard g(c->device);
+  cudaStream_t s = as_stream(stream);
+  uint32_t* next = kind == FFX_BATCH_COPY ? &P.next : &P.hnext;
+  const uint32_t total = kind == FFX_BATCH_COPY ? P.batches : P.hbatches;
+  if (*next >= total) return fail(FFX_ESTATE, "snapshot_next: no %s batches left", kind ? "hash" : "copy");
+  if (gate_event) FFX_CUDA(cudaStreamWaitEvent(s, static_cast<cudaEvent_t>(gate_event), 0));
+  const uint32_t b = (*next)++;
+
+  if (!P.split) {
+    // Fused: batch b covers warp tasks [G*b/B, G*(b+1)/B); the last commits.
+    const uint64_t G = P.job.total_groups;
+    SliceJob bj = P.job;
+    bj.group_lo = G * b / P.batches;
+    bj.group_hi = G * (b + 1) / P.batches;
+    bj.commit.finalize = (b + 1 == P.batches);
+    if (bj.group_lo != bj.group_hi || bj.commit.finalize) {
+      FFX_CUDA(launch_slices(bj, SliceMode::Copy, true, P.max_ctas, s));
+      c->stats.kernel_launches++;
+    }
+    if (remaining) *remaining = P.batches - P.next;
+    return P.next < P.batches ? FFX_OK : finish_snapshot(c, P, s);
+  }
+
+  int st = kind == FFX_BATCH_COPY ? issue_copy_batch(c, P, b, s) : issue_hash_batch(c, P, b, s);
+  if (st) return st;
+  if (remaining) *remaining = total - *next;
+  if (*next == total) FFX_CUDA(cudaEventRecord(kind == FFX_BATCH_COPY ? c->copy_done : c->hash_done, s));
+  if (P.next < P.batches || P.hnext < P.hbatches) return FFX_OK;
+  // Both queues drained: join the other queue's stream, then commit.
+  FFX_CUDA(cudaStreamWaitEvent(s, kind == FFX_BATCH_COPY ? c->hash_done : c->copy_done, 0));
+  FFX_CUDA(launch_commit(P.job.commit, s));
+  c->stats.kernel_launches++;
+  return finish_snapshot(c, P, s);
+}
+
+extern "C" int ffx_snapshot_next(ffx_ctx* c, void* stream, void* gate_event, uint32_t* remaining) {
+  if (!c) return fail(FFX_EINVAL, "snapshot_next: null ctx");
+  PendingSnapshot& P = c->pending;
+  if (!P.active) return fail(FFX_ESTATE, "snapshot_next: no snapshot in progress (ffx_snapshot_begin)");
+  // Split mode: copy batches first, then hash batches.
+  const int kind = (P.split && P.next >= P.batches) ? FFX_BATCH_HASH : FFX_BATCH_COPY;
+  uint32_t left = 0;
+  int st = ffx_snapshot_next_kind(c, kind, stream, gate_event, &left);
+  if (remaining) *remaining = (P.batches - P.next) + (P.split ? P.hbatches - P.hnext : 0);
+  return st;
+}
+
 extern "C" int ffx_snapshot(ffx_ctx* c, uint64_t iteration, void* stream, const ffx_snapshot_opts* o) {
   uint32_t batches = 1;
   int st = ffx_snapshot_begin(c, iteration, o, &batches);
   if (st) return st;
   auto* gates = o ? static_cast<void**>(o->gate_events) : nullptr;
-  for (uint32_t b = 0; b < batches; ++b) {
+  // Copy (or fused) batches on their gates, then -- split policy -- the hash
+  // batches on the same stream.
+  const uint32_t hb = c->pending.split ? c->pending.hbatches : 0;
+  for (uint32_t b = 0; b < batches + hb; ++b) {
     uint32_t left = 0;
-    st = ffx_snapshot_next(c, stream, gates ? gates[b] : nullptr, &left);
+    st = ffx_snapshot_next_kind(c, b < batches ? FFX_BATCH_COPY : FFX_BATCH_HASH, stream,
+                                (gates && b < batches) ? gates[b] : nullptr, &left);
     if (st) {
       c->pending.active = false;
       return st;

@@ -57,10 +57,41 @@ struct SliceJob {
   unsigned long long* result;     // verify mode: [first bad slice, bad count]
   unsigned int* sched;            // [next task, CTAs done]: dynamic scheduling
                                   // (zero between launches; null = static)
+  uint32_t proxy_fence;           // tensor path: generic->async proxy fence before each refill
   SlotCommit commit;
 };
 
 enum class SliceMode { Hash, Copy, CopyVerify, HashVerify };
+
+// ---- copy-only TMA batches (split scheduling policy, ffx_copy.cu) ----------
+
+struct CopyRegion {
+  const uint8_t* src;
+  uint8_t* dst;
+  uint64_t bytes;
+  uint32_t aligned;  // both pointers 16-byte aligned (set by finalize_copy_job)
+  uint32_t pad_;
+};
+
+struct SlotMark {  // every copy CTA marks the slot WRITING first
+  uint8_t* slot;   // null = no mark
+  uint64_t iteration, seq;
+};
+
+struct CopyJob {
+  CopyRegion reg[kMaxRegions];
+  uint64_t chunk_base[kMaxRegions];
+  uint32_t nregions;
+  uint32_t pad_;
+  uint64_t total_chunks;
+  uint64_t chunk_lo, chunk_hi;  // this launch's 32 KB chunks
+  SlotMark mark;
+};
+
+void finalize_copy_job(CopyJob& job);
+cudaError_t launch_copy(const CopyJob& job, uint32_t ctas, cudaStream_t stream);
+// One-thread kernel writing the final meta + SNP1 header, then COMMITTED.
+cudaError_t launch_commit(const SlotCommit& c, cudaStream_t stream);
 
 // Fill job.reg[*].group_base / slice_base, job.total_groups and the group
 // range [0, total_groups).

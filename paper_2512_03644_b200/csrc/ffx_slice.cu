@@ -265,7 +265,7 @@ __global__ void __launch_bounds__(W * 32) slice_kernel(const __grid_constant__ S
           __syncwarp();
           if (lane == 0) {
             if constexpr (kCopy) bulk_wait_read_all();
-            fence_async_smem();
+            if (job.proxy_fence) fence_async_smem();
             mbar_expect_tx(bar0 + 8 * s, 32 * C);
             tensor_load(tile, msrc, (k + S) * C, y, bar0 + 8 * s);
           }
@@ -407,6 +407,9 @@ cudaError_t launch_mode(const SliceJob& job, uint32_t max_ctas, cudaStream_t str
     case 2: return launch_t<128, 4, 4, false, M, kCommit>(job, max_ctas, stream);
     case 3: return launch_t<128, 6, 4, true, M, kCommit>(job, max_ctas, stream);
     case 4: return launch_t<128, 8, 4, true, M, kCommit>(job, max_ctas, stream);
+    case 5: return launch_t<128, 3, 4, true, M, kCommit>(job, max_ctas, stream);
+    case 6: return launch_t<128, 2, 4, true, M, kCommit>(job, max_ctas, stream);
+    case 7: return launch_t<128, 2, 8, true, M, kCommit>(job, max_ctas, stream);
     default: return launch_t<128, 4, 4, true, M, kCommit>(job, max_ctas, stream);
   }
 }
@@ -490,8 +493,12 @@ cudaError_t launch_slices(const SliceJob& job_in, SliceMode mode, bool commit, u
   SliceJob job = job_in;
   const int v = variant();
   if (v == 0 || v >= 3) attach_tensor_maps(job, mode == SliceMode::Copy || mode == SliceMode::CopyVerify);
+  static const bool no_fence = std::getenv("FFX_NO_FENCE") != nullptr;
+  job.proxy_fence = no_fence ? 0u : 1u;
   switch (mode) {
-    case SliceMode::Hash: return launch_mode<SliceMode::Hash, false>(job, max_ctas, stream);
+    case SliceMode::Hash:
+      return commit ? launch_mode<SliceMode::Hash, true>(job, max_ctas, stream)
+                    : launch_mode<SliceMode::Hash, false>(job, max_ctas, stream);
     case SliceMode::Copy:
       return commit ? launch_mode<SliceMode::Copy, true>(job, max_ctas, stream)
                     : launch_mode<SliceMode::Copy, false>(job, max_ctas, stream);

@@ -31,6 +31,7 @@ REGION_MASTER, REGION_ADAM_M, REGION_ADAM_V, REGION_PARAMS, REGION_CURSOR, REGIO
 # faults
 FAULT_POISON_STATE, FAULT_CORRUPT_REPLICA, FAULT_TEAR_SLOT, FAULT_CORRUPT_SUMS = range(4)
 SLOT_EMPTY, SLOT_WRITING, SLOT_COMMITTED = 0, 1, 2
+BATCH_COPY, BATCH_HASH = 0, 1
 U64_MAX = (1 << 64) - 1
 
 
@@ -139,7 +140,9 @@ class SlotInfo(ctypes.Structure):
 class SnapshotOpts(ctypes.Structure):
     _fields_ = [("max_ctas", ctypes.c_uint32), ("batches", ctypes.c_uint32),
                 ("gate_events", ctypes.c_void_p), ("verify_on_store", ctypes.c_uint32),
-                ("weights_kind", ctypes.c_uint32)]
+                ("weights_kind", ctypes.c_uint32), ("split", ctypes.c_uint32),
+                ("hash_batches", ctypes.c_uint32), ("hash_ctas", ctypes.c_uint32),
+                ("copy_engine", ctypes.c_uint32)]
 
 
 class RecoverReport(ctypes.Structure):
@@ -232,6 +235,7 @@ SIGNATURES = {
     "ffx_snapshot": (_I, [_P, _U64, _P, ctypes.POINTER(SnapshotOpts)]),
     "ffx_snapshot_begin": (_I, [_P, _U64, ctypes.POINTER(SnapshotOpts), ctypes.POINTER(_U32)]),
     "ffx_snapshot_next": (_I, [_P, _P, _P, ctypes.POINTER(_U32)]),
+    "ffx_snapshot_next_kind": (_I, [_P, _I, _P, _P, ctypes.POINTER(_U32)]),
     "ffx_snapshot_read_sums": (_I, [_P, _P, _U64, ctypes.POINTER(_U64), _P]),
     "ffx_recover": (_I, [_P, _P, _U64, _P, ctypes.POINTER(RecoverReport)]),
     "ffx_recover_region": (_I, [_P, _U32, _P, _P, _P, ctypes.POINTER(RecoverReport)]),
@@ -581,8 +585,13 @@ class Context:
         check(lib.ffx_snapshot_target(self._c, replica.ptr if replica else None), "snapshot_target")
 
     def snapshot(self, iteration: int, stream=None, max_ctas: int = 0, batches: int = 1,
-                 gate_events=None, verify_on_store: bool = False, weights_kind: bool = False):
+                 gate_events=None, verify_on_store: bool = False, weights_kind: bool = False,
+                 split: bool = False, hash_batches: int = 0, hash_ctas: int = 0, copy_engine: bool = False):
         o = SnapshotOpts()
+        o.split = int(split)
+        o.hash_batches = hash_batches
+        o.hash_ctas = hash_ctas
+        o.copy_engine = int(copy_engine)
         o.max_ctas = max_ctas
         o.batches = batches
         o.verify_on_store = int(verify_on_store)
@@ -595,22 +604,32 @@ class Context:
         check(lib.ffx_snapshot(self._c, iteration, _stream_ptr(stream), ctypes.byref(o)), "snapshot")
 
     def snapshot_begin(self, iteration: int, batches: int = 1, max_ctas: int = 0,
-                       verify_on_store: bool = False) -> int:
+                       verify_on_store: bool = False, split: bool = False, hash_batches: int = 0,
+                       hash_ctas: int = 0, copy_engine: bool = False) -> int:
         o = SnapshotOpts()
         o.max_ctas = max_ctas
         o.batches = batches
         o.verify_on_store = int(verify_on_store)
+        o.split = int(split)
+        o.hash_batches = hash_batches
+        o.hash_ctas = hash_ctas
+        o.copy_engine = int(copy_engine)
         n = ctypes.c_uint32()
         check(lib.ffx_snapshot_begin(self._c, iteration, ctypes.byref(o), ctypes.byref(n)), "snapshot_begin")
         return n.value
 
-    def snapshot_next(self, stream=None, gate_event=None) -> int:
-        """Issue the next batch; returns how many remain."""
+    def snapshot_next(self, stream=None, gate_event=None, kind: Optional[int] = None) -> int:
+        """Issue the next batch (of `kind` under the split policy); returns how
+        many batches of that kind (or in total, kind=None) remain."""
         left = ctypes.c_uint32()
         ev = None
         if gate_event is not None:
             ev = gate_event.cuda_event if hasattr(gate_event, "cuda_event") else gate_event
-        check(lib.ffx_snapshot_next(self._c, _stream_ptr(stream), ev, ctypes.byref(left)), "snapshot_next")
+        if kind is None:
+            check(lib.ffx_snapshot_next(self._c, _stream_ptr(stream), ev, ctypes.byref(left)), "snapshot_next")
+        else:
+            check(lib.ffx_snapshot_next_kind(self._c, kind, _stream_ptr(stream), ev, ctypes.byref(left)),
+                  "snapshot_next_kind")
         return left.value
 
     def read_sums(self, host_tensor, stream=None) -> int:

@@ -7,19 +7,22 @@ layer shards plus cuBLAS bf16 GEMMs sized to a Llama-3-8B layer's compute --
 and stands in for a real training step; the product is the snapshot that
 rides in its gaps.
 
-Scheduling policy (reference semantics: STATE traffic only when no TRAIN
-chunk is queued, inversion bounded by one chunk -- sim_net.cpp:401-454,
+Scheduling (reference semantics: STATE traffic only when no TRAIN chunk is
+queued, inversion bounded by one chunk -- sim_net.cpp:401-454,
 test_transport.cpp:173-197):
-  * the snapshot of iteration n is split into one batch per forward layer;
-  * batch l is gated on an event recorded right after layer l's all-gather
-    completes, i.e. when NVLink goes quiet and the GEMMs start;
-  * it runs on a lower-priority stream with a capped CTA count, so the block
-    scheduler prefers the step's kernels and a batch delays TRAIN by at most
-    its in-flight warp tasks;
-  * the optimizer update of iteration n+1 waits on the snapshot's completion
-    event -- the fp32 master / Adam state is only mutated there (SURVEY 7.2
-    hard part 4), so the snapshot streams from the live buffers with no
-    staging copy.
+  * the step runs on a high-priority stream, snapshot batches on a
+    low-priority one with a capped CTA count, so the block scheduler prefers
+    the step and a batch can delay TRAIN by at most its in-flight tasks;
+  * policy "fused": one fused copy+checksum batch per forward layer, gated on
+    an event recorded right after that layer's all-gather (NVLink goes quiet
+    while the GEMMs run);
+  * policy "split": the copy (TMA copy-only kernel, few SMs -- or the copy
+    engines) goes into those same compute gaps, while the checksum work
+    (SM-heavy, HBM-only) is gated on events recorded right *before* each
+    all-gather, i.e. it runs while the SMs idle behind NCCL;
+  * the optimizer update of iteration n+1 waits on the snapshot's commit --
+    the fp32 master / Adam state is only mutated there (SURVEY 7.2 hard part
+    4), so the snapshot streams from the live buffers with no staging copy.
 """
 from __future__ import annotations
 
@@ -58,54 +61,81 @@ class SyntheticStep:
             torch.matmul(self.x, self.w, out=self.y)
 
     def run(self, hook=None):
-        """One step on self.train.  hook(kind, layer) is called at each gap."""
+        """One step on self.train.  hook(kind, layer) marks the gaps:
+        'pre_ag' before an all-gather, 'fwd'/'bwd' once it completed,
+        'opt' before the optimizer update."""
+        h = hook or (lambda kind, layer: None)
         with torch.cuda.stream(self.train):
             for l in range(self.layers):
+                h("pre_ag", l)
                 dist.all_gather_into_tensor(self.full, self.shard)
-                if hook:
-                    hook("fwd", l)
+                h("fwd", l)
                 self._gemms(self.fwd_gemms)
             for l in reversed(range(self.layers)):
+                h("pre_ag", self.layers + l)
                 dist.all_gather_into_tensor(self.full, self.shard)
-                if hook:
-                    hook("bwd", l)
+                h("bwd", l)
                 self._gemms(2 * self.fwd_gemms)
                 dist.reduce_scatter_tensor(self.grad_shard, self.grad_full)
-            if hook:
-                hook("opt", None)
+            h("opt", None)
             self.shard.add_(self.grad_shard, alpha=-1e-6)  # the optimizer update
 
 
 class SliceScheduler:
-    """Issues one snapshot batch per forward-layer gap of a SyntheticStep."""
+    """Drives one ffx snapshot per step through the gaps of a SyntheticStep."""
 
-    def __init__(self, ctx, step: SyntheticStep, max_ctas: int = 32):
+    def __init__(self, ctx, step: SyntheticStep, policy: str = "split", copy_ctas: int = 8,
+                 hash_ctas: int = 96, copy_engine: bool = False):
+        from paper_2512_03644_b200 import ffx
+        self.ffx = ffx
         self.ctx = ctx
         self.step = step
-        self.max_ctas = max_ctas
+        self.policy = policy
+        self.copy_ctas = copy_ctas
+        self.hash_ctas = hash_ctas
+        self.copy_engine = copy_engine
         self.low = torch.cuda.Stream(priority=0)
+        self.hash_stream = torch.cuda.Stream(priority=0)
         self.done = torch.cuda.Event()
-        self.iteration = 0
-        self.remaining = 0
+        self.copies = self.hashes = 0
 
     def begin(self, iteration: int):
-        self.iteration = iteration
-        self.remaining = self.ctx.snapshot_begin(iteration, batches=self.step.layers, max_ctas=self.max_ctas)
+        L = self.step.layers
+        if self.policy == "fused":
+            self.copies = self.ctx.snapshot_begin(iteration, batches=L, max_ctas=self.copy_ctas)
+            self.hashes = 0
+        else:
+            self.copies = self.ctx.snapshot_begin(iteration, batches=L, max_ctas=self.copy_ctas, split=True,
+                                                  hash_batches=L, hash_ctas=self.hash_ctas,
+                                                  copy_engine=self.copy_engine)
+            self.hashes = L
+
+    def _issue(self, kind, stream, gate=None):
+        left = self.ctx.snapshot_next(stream=stream, gate_event=gate,
+                                      kind=None if self.policy == "fused" else kind)
+        if kind == self.ffx.BATCH_COPY:
+            self.copies = left
+        else:
+            self.hashes = left
+        if self.copies == 0 and self.hashes == 0:
+            self.done.record(stream)  # this stream carried the commit
+
+    def _gap(self):
+        ev = torch.cuda.Event()
+        ev.record(self.step.train)
+        return ev
 
     def hook(self, kind, layer):
-        train = self.step.train
-        if kind == "fwd" and self.remaining:
-            gap = torch.cuda.Event()
-            gap.record(train)
-            self.remaining = self.ctx.snapshot_next(stream=self.low, gate_event=gap)
-            if self.remaining == 0:
-                self.done.record(self.low)
+        if kind == "pre_ag" and self.hashes and layer < self.step.layers:
+            self._issue(self.ffx.BATCH_HASH, self.hash_stream, self._gap())
+        elif kind == "fwd" and self.copies:
+            self._issue(self.ffx.BATCH_COPY, self.low, self._gap())
         elif kind == "opt":
-            while self.remaining:  # more batches than gaps: flush the rest now
-                self.remaining = self.ctx.snapshot_next(stream=self.low)
-                if self.remaining == 0:
-                    self.done.record(self.low)
-            train.wait_event(self.done)  # optimizer mutates the snapshotted state
+            while self.copies:  # more batches than gaps: flush now
+                self._issue(self.ffx.BATCH_COPY, self.low)
+            while self.hashes:
+                self._issue(self.ffx.BATCH_HASH, self.hash_stream)
+            self.step.train.wait_event(self.done)  # optimizer mutates the snapshotted state
 
 
 def time_steps(step: SyntheticStep, n: int, sched: SliceScheduler | None = None, it0: int = 0):
@@ -127,18 +157,20 @@ def time_steps(step: SyntheticStep, n: int, sched: SliceScheduler | None = None,
     return out
 
 
-def measure_overhead(step: SyntheticStep, sched: SliceScheduler, steps: int = 8, warmup: int = 2):
+def measure_overhead(step: SyntheticStep, sched: SliceScheduler, steps: int = 8, warmup: int = 2,
+                     it0: int = 1):
     """Interleaved A/B: steps without and with the concurrent snapshot."""
     time_steps(step, warmup)
-    time_steps(step, warmup, sched, it0=1_000_000)
+    time_steps(step, warmup, sched, it0=it0 + 100_000)
     base, with_snap = [], []
-    it = 1
+    it = it0
     for _ in range(steps):
         base += time_steps(step, 1)
         with_snap += time_steps(step, 1, sched, it0=it)
         it += 1
     b = statistics.median(base)
     w = statistics.median(with_snap)
-    return {"step_ms_without": round(b, 3), "step_ms_with": round(w, 3),
+    return {"policy": sched.policy + ("+ce" if sched.copy_engine else ""), "copy_ctas": sched.copy_ctas,
+            "hash_ctas": sched.hash_ctas, "step_ms_without": round(b, 3), "step_ms_with": round(w, 3),
             "overhead_pct": round(100.0 * (w - b) / b, 3), "steps_each": steps,
             "train_link_bytes_per_step": step.train_link_bytes}

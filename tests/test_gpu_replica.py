@@ -333,3 +333,37 @@ def test_scheduler_begin_next_gated(ffx):
     assert rep.export_frame(30) == orc.pack_blob((1, 0, 0), 30, 1, want)
     with pytest.raises(ffx.StateError):
         origin.snapshot_next(stream=low)
+
+
+@pytest.mark.parametrize("copy_engine", [False, True])
+def test_split_policy_copy_and_hash_batches(ffx, copy_engine):
+    # Split scheduling: copy batches (TMA copy-only / copy engines) and hash
+    # batches (local state -> slot table) on different streams; the slot
+    # commits after both drain and is byte-identical to the fused result.
+    n = (1 << 22) + 12345
+    spec, holder, origin, rep, view = ring_pair(ffx, n)
+    state, want = blob_for(ffx, 1, n)
+    extra = torch.arange(1000, dtype=torch.int32, device="cuda")
+    origin.register(ffx.REGION_BLOB, state)
+    origin.register(ffx.REGION_RNG, extra)
+    a, b = torch.cuda.Stream(), torch.cuda.Stream()
+    origin.snapshot_begin(40, batches=3, max_ctas=4, split=True, hash_batches=5, hash_ctas=16,
+                          copy_engine=copy_engine)
+    left_h = left_c = 1
+    while left_h or left_c:
+        if left_h:
+            left_h = origin.snapshot_next(stream=b, kind=ffx.BATCH_HASH)
+        if left_c:
+            left_c = origin.snapshot_next(stream=a, kind=ffx.BATCH_COPY)
+    torch.cuda.synchronize()
+    concat = want + bytes(extra.cpu().numpy().tobytes())
+    assert rep.newest() == 40
+    assert rep.export_frame(40) == orc.pack_blob((1, 0, 0), 40, 1, concat)
+    origin.inject(ffx.FAULT_POISON_STATE)
+    origin.recover(view, 40)
+    assert host(state) == want
+    # the blocking form interleaves copy then hash batches on one stream
+    origin.snapshot(41, split=True, batches=2, hash_batches=2, max_ctas=2, copy_engine=copy_engine,
+                    verify_on_store=True)
+    torch.cuda.synchronize()
+    assert rep.export_frame(41) == orc.pack_blob((1, 0, 0), 41, 1, concat)
