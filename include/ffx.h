@@ -160,6 +160,9 @@ int ffx_copy_checksums(void* dst, const void* src, uint64_t len, uint64_t slice_
  * (UINT64_MAX if none), dev_result[1] <- number of bad slices. */
 int ffx_copy_verify(void* dst, const void* src, uint64_t len, uint64_t slice_bytes,
                     const uint64_t* dev_expected, uint64_t* dev_result, void* stream);
+/* Copy only (no checksum): the split policy's TMA copy kernel, `ctas` CTAs of
+ * one warp each (0 = 16).  dst may be a peer-mapped pointer. */
+int ffx_copy(void* dst, const void* src, uint64_t len, uint32_t ctas, void* stream);
 /* evo::expand / evo::materialize (evolution.cpp:71-97) into device memory.
  * materialize: FFX_EINVAL when bytes < 32. */
 int ffx_expand(void* dst, const uint8_t digest[32], uint64_t bytes, void* stream);

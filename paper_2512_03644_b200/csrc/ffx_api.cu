@@ -525,6 +525,17 @@ extern "C" int ffx_copy_verify(void* dst, const void* src, uint64_t len, uint64_
   return FFX_OK;
 }
 
+extern "C" int ffx_copy(void* dst, const void* src, uint64_t len, uint32_t ctas, void* stream) {
+  if (len == 0) return FFX_OK;
+  if (!dst || !src) return fail(FFX_EINVAL, "copy: null argument");
+  CopyJob job{};
+  job.nregions = 1;
+  job.reg[0] = CopyRegion{static_cast<const uint8_t*>(src), static_cast<uint8_t*>(dst), len, 0, 0};
+  finalize_copy_job(job);
+  FFX_CUDA(launch_copy(job, ctas, as_stream(stream)));
+  return FFX_OK;
+}
+
 extern "C" int ffx_expand(void* dst, const uint8_t digest[32], uint64_t bytes, void* stream) {
   if (!digest || (bytes && !dst)) return fail(FFX_EINVAL, "expand: null argument");
   uint64_t fold = rd(digest, 8);

@@ -208,6 +208,7 @@ SIGNATURES = {
     "ffx_slice_checksums": (_I, [_P, _U64, _U64, _P, _P]),
     "ffx_copy_checksums": (_I, [_P, _P, _U64, _U64, _P, _P]),
     "ffx_copy_verify": (_I, [_P, _P, _U64, _U64, _P, _P, _P]),
+    "ffx_copy": (_I, [_P, _P, _U64, _U32, _P]),
     "ffx_expand": (_I, [_P, _P, _U64, _P]),
     "ffx_materialize": (_I, [_P, _P, _U64, _P]),
     "ffx_blob_check": (_I, [_P, _U64, ctypes.POINTER(_U64), _P]),

@@ -341,7 +341,7 @@ def test_split_policy_copy_and_hash_batches(ffx, copy_engine):
     # batches (local state -> slot table) on different streams; the slot
     # commits after both drain and is byte-identical to the fused result.
     n = (1 << 22) + 12345
-    spec, holder, origin, rep, view = ring_pair(ffx, n)
+    spec, holder, origin, rep, view = ring_pair(ffx, n + 4000)
     state, want = blob_for(ffx, 1, n)
     extra = torch.arange(1000, dtype=torch.int32, device="cuda")
     origin.register(ffx.REGION_BLOB, state)
