@@ -267,6 +267,10 @@ int ffx_replica_export_frame(ffx_replica* r, uint64_t iteration, void* host_dst,
 /* Where this rank's snapshots land: normally the replica its ring successor
  * created for it and exported (opened with ffx_replica_open). */
 int ffx_snapshot_target(ffx_ctx* ctx, ffx_replica* target);
+/* Double-neighbour replication: a second holder (dp+2) that
+ * receives the same tiles from the same kernel -- one HBM read, two stores,
+ * one checksum pass.  NULL removes it. */
+int ffx_snapshot_target2(ffx_ctx* ctx, ffx_replica* target);
 
 typedef struct ffx_snapshot_opts {
   uint32_t max_ctas;       /* SM budget for the snapshot kernel (0 = whole GPU) */

@@ -119,7 +119,7 @@ struct ffx_replica {
 struct PendingSnapshot {
   bool active = false;
   SliceJob job{};  // fused: copy + hash (+ commit); split: the hash-only job
-  uint32_t batches = 1, next = 0, max_ctas = 0, slot = 0;
+  uint32_t batches = 1, next = 0, max_ctas = 0, slot = 0, slot2 = 0;
   uint64_t iteration = 0, seq = 0, nslices = 0, logical = 0;
   bool verify = false;
   // split policy: copy batches and hash batches drain independently
@@ -136,6 +136,7 @@ struct ffx_ctx {
   uint64_t slice_bytes = 4096;
   std::vector<Region> regions;
   ffx_replica* target = nullptr;
+  ffx_replica* target2 = nullptr;  // second holder (double-neighbour), optional
   unsigned int* done = nullptr;            // commit counter (device)
   unsigned long long* result = nullptr;    // verify result (device, 2 words)
   unsigned long long* result_host = nullptr;  // pinned mirror
@@ -827,6 +828,7 @@ extern "C" int ffx_replica_open(ffx_ctx* c, const uint8_t handle[FFX_HANDLE_BYTE
 extern "C" int ffx_replica_destroy(ffx_replica* r) {
   if (!r) return FFX_OK;
   if (r->ctx && r->ctx->target == r) r->ctx->target = nullptr;
+  if (r->ctx && r->ctx->target2 == r) r->ctx->target2 = nullptr;
   DeviceGuard g(r->ctx ? r->ctx->device : r->device);
   if (r->owned && r->base) cudaFree(r->base);
   if (r->ipc_opened && r->base) cudaIpcCloseMemHandle(r->base);
@@ -992,6 +994,38 @@ extern "C" int ffx_snapshot_target(ffx_ctx* c, ffx_replica* t) {
   return FFX_OK;
 }
 
+extern "C" int ffx_snapshot_target2(ffx_ctx* c, ffx_replica* t) {
+  if (!c) return fail(FFX_EINVAL, "snapshot_target2: null ctx");
+  c->target2 = t;
+  if (t) {
+    int st = refresh_cache(t);
+    if (st) return st;
+    for (const auto& sc : t->cache) c->seq = std::max(c->seq, sc.seq);
+  }
+  return FFX_OK;
+}
+
+namespace {
+
+// Two-version rule (ckpt.cpp:46-52, :86-92): replace the slot holding this
+// iteration, else an empty slot, else the oldest.
+uint32_t pick_slot(const ffx_replica* t, uint64_t iteration) {
+  int v = -1;
+  for (uint32_t i = 0; i < t->versions; ++i)
+    if (t->cache[i].state != kSlotEmpty && t->cache[i].iteration == iteration) v = static_cast<int>(i);
+  if (v < 0)
+    for (uint32_t i = 0; i < t->versions && v < 0; ++i)
+      if (t->cache[i].state == kSlotEmpty) v = static_cast<int>(i);
+  if (v < 0) {
+    v = 0;
+    for (uint32_t i = 1; i < t->versions; ++i)
+      if (t->cache[i].seq < t->cache[static_cast<uint32_t>(v)].seq) v = static_cast<int>(i);
+  }
+  return static_cast<uint32_t>(v);
+}
+
+}  // namespace
+
 extern "C" int ffx_snapshot_begin(ffx_ctx* c, uint64_t iteration, const ffx_snapshot_opts* o,
                                   uint32_t* batches_out) {
   if (!c) return fail(FFX_EINVAL, "snapshot: null ctx");
@@ -1015,20 +1049,14 @@ extern "C" int ffx_snapshot_begin(ffx_ctx* c, uint64_t iteration, const ffx_snap
     return fail(FFX_ECONFIG, "snapshot needs %llu checksum entries, slot has %llu",
                 (unsigned long long)nslices, (unsigned long long)t->layout.table_cap);
 
-  // Two-version rule (ckpt.cpp:46-52, :86-92): replace the slot holding this
-  // iteration, else an empty slot, else the oldest.
-  int v = -1;
-  for (uint32_t i = 0; i < t->versions; ++i)
-    if (t->cache[i].state != kSlotEmpty && t->cache[i].iteration == iteration) v = static_cast<int>(i);
-  if (v < 0)
-    for (uint32_t i = 0; i < t->versions && v < 0; ++i)
-      if (t->cache[i].state == kSlotEmpty) v = static_cast<int>(i);
-  if (v < 0) {
-    v = 0;
-    for (uint32_t i = 1; i < t->versions; ++i)
-      if (t->cache[i].seq < t->cache[static_cast<uint32_t>(v)].seq) v = static_cast<int>(i);
+  ffx_replica* t2 = c->target2;
+  if (t2) {
+    if (pm.logical > t2->capacity || pm.physical > t2->layout.payload_cap || nslices > t2->layout.table_cap)
+      return fail(FFX_ECONFIG, "snapshot payload %llu exceeds the second replica buffer of %llu bytes",
+                  (unsigned long long)pm.logical, (unsigned long long)t2->capacity);
   }
-  const uint32_t slot = static_cast<uint32_t>(v);
+  const uint32_t slot = pick_slot(t, iteration);
+  const uint32_t slot2 = t2 ? pick_slot(t2, iteration) : 0;
   const uint64_t seq = ++c->seq;
 
   PendingSnapshot& P = c->pending;
@@ -1067,6 +1095,17 @@ extern "C" int ffx_snapshot_begin(ffx_ctx* c, uint64_t iteration, const ffx_snap
   cm.seq = seq;
   std::memcpy(cm.meta, &m, sizeof m);
   std::memcpy(cm.snp1, hdr, 32);
+  if (t2) {
+    // Double-neighbour replication: the same tiles stored twice, one table
+    // per replica, each slot committed by its own counter.
+    for (size_t i = 0; i < pm.regs.size(); ++i) job.reg[i].dst2 = t2->payload(slot2) + pm.offs[i];
+    job.sums_out2 = t2->sums(slot2);
+    job.commit2 = cm;
+    job.commit2.slot = t2->slot(slot2);
+    job.commit2.done = c->done + 4;
+    job.commit2.payload_off = t2->layout.payload_off;
+    P.slot2 = slot2;
+  }
 
   P.active = true;
   P.batches = std::max<uint32_t>(1, opts.batches);
@@ -1084,9 +1123,10 @@ extern "C" int ffx_snapshot_begin(ffx_ctx* c, uint64_t iteration, const ffx_snap
     CopyJob& cj = P.copy;
     cj.nregions = job.nregions;
     for (uint32_t i = 0; i < job.nregions; ++i)
-      cj.reg[i] = CopyRegion{job.reg[i].src, job.reg[i].dst, job.reg[i].bytes, 0, 0};
+      cj.reg[i] = CopyRegion{job.reg[i].src, job.reg[i].dst, job.reg[i].bytes, 0, 0, job.reg[i].dst2};
     finalize_copy_job(cj);
     cj.mark = SlotMark{t->slot(slot), iteration, seq};
+    if (t2) cj.mark2 = SlotMark{t2->slot(slot2), iteration, seq};
     // Hash batches: the local state hashed straight into the slot's table.
     for (uint32_t i = 0; i < job.nregions; ++i) job.reg[i].dst = nullptr;
     P.hbatches = std::max<uint32_t>(1, opts.hash_batches ? opts.hash_batches : P.batches);
@@ -1156,6 +1196,8 @@ int issue_copy_batch(ffx_ctx* c, PendingSnapshot& P, uint32_t b, cudaStream_t s)
     const uint64_t off = (c0 - bj.chunk_base[r]) * (32 * 1024);
     const uint64_t end = std::min(bj.reg[r].bytes, (c1 - bj.chunk_base[r]) * (32 * 1024));
     FFX_CUDA(cudaMemcpyAsync(bj.reg[r].dst + off, bj.reg[r].src + off, end - off, cudaMemcpyDefault, s));
+    if (bj.reg[r].dst2)
+      FFX_CUDA(cudaMemcpyAsync(bj.reg[r].dst2 + off, bj.reg[r].src + off, end - off, cudaMemcpyDefault, s));
   }
   return FFX_OK;
 }
@@ -1178,6 +1220,7 @@ int finish_snapshot(ffx_ctx* c, PendingSnapshot& P, cudaStream_t s) {
   P.active = false;
   ffx_replica* t = c->target;
   t->cache[P.slot] = SlotCache{true, kSlotCommitted, P.iteration, P.seq};
+  if (c->target2) c->target2->cache[P.slot2] = SlotCache{true, kSlotCommitted, P.iteration, P.seq};
   c->last_slot = P.slot;
   c->last_nslices = P.nslices;
   c->stats.snapshots++;
@@ -1209,6 +1252,7 @@ extern "C" int ffx_snapshot_next_kind(ffx_ctx* c, int kind, void* stream, void* 
     bj.group_lo = G * b / P.batches;
     bj.group_hi = G * (b + 1) / P.batches;
     bj.commit.finalize = (b + 1 == P.batches);
+    bj.commit2.finalize = bj.commit.finalize;
     if (bj.group_lo != bj.group_hi || bj.commit.finalize) {
       FFX_CUDA(launch_slices(bj, SliceMode::Copy, true, P.max_ctas, s));
       c->stats.kernel_launches++;
@@ -1225,6 +1269,7 @@ extern "C" int ffx_snapshot_next_kind(ffx_ctx* c, int kind, void* stream, void* 
   // Both queues drained: join the other queue's stream, then commit.
   FFX_CUDA(cudaStreamWaitEvent(s, kind == FFX_BATCH_COPY ? c->hash_done : c->copy_done, 0));
   FFX_CUDA(launch_commit(P.job.commit, s));
+  if (P.job.commit2.slot) FFX_CUDA(launch_commit(P.job.commit2, s));
   c->stats.kernel_launches++;
   return finish_snapshot(c, P, s);
 }

@@ -66,12 +66,15 @@ __global__ void __launch_bounds__(32) copy_kernel(const __grid_constant__ CopyJo
   uint8_t* buf = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
   __shared__ __align__(8) uint64_t bars[kCopyStages];
   const int lane = threadIdx.x;
-  if (job.mark.slot != nullptr && lane == 0) {  // WRITING before any payload byte
-    volatile SlotMeta* m = reinterpret_cast<volatile SlotMeta*>(job.mark.slot);
-    m->magic = kSlotMagic;
-    m->iteration = job.mark.iteration;
-    m->seq = job.mark.seq;
-    m->state = kSlotWriting;
+  if (lane == 0) {  // WRITING before any payload byte
+    for (const SlotMark* mk : {&job.mark, &job.mark2}) {
+      if (mk->slot == nullptr) continue;
+      volatile SlotMeta* m = reinterpret_cast<volatile SlotMeta*>(mk->slot);
+      m->magic = kSlotMagic;
+      m->iteration = mk->iteration;
+      m->seq = mk->seq;
+      m->state = kSlotWriting;
+    }
     __threadfence_system();
   }
   if (lane == 0) {
@@ -124,6 +127,8 @@ __global__ void __launch_bounds__(32) copy_kernel(const __grid_constant__ CopyJo
         const uint64_t off = (c - job.chunk_base[r]) * kCopyChunk;
         const uint64_t len = (R.bytes - off < kCopyChunk ? R.bytes - off : kCopyChunk) & ~uint64_t{15};
         bulk_store(R.dst + off, smem_u32(buf + s * kCopyChunk), static_cast<uint32_t>(len));
+        if (R.dst2 != nullptr)  // double neighbour: one load, two stores
+          bulk_store(R.dst2 + off, smem_u32(buf + s * kCopyChunk), static_cast<uint32_t>(len));
         asm volatile("cp.async.bulk.commit_group;" ::: "memory");
       }
       phase ^= pending[s] ? (1u << s) : 0u;
@@ -148,7 +153,10 @@ __global__ void __launch_bounds__(32) copy_kernel(const __grid_constant__ CopyJo
     const uint64_t off = (c - job.chunk_base[r]) * kCopyChunk;
     const uint64_t end = R.bytes - off < kCopyChunk ? R.bytes : off + kCopyChunk;
     const uint64_t from = R.aligned ? off + ((end - off) & ~uint64_t{15}) : off;
-    for (uint64_t o = from + lane; o < end; o += 32) R.dst[o] = R.src[o];
+    for (uint64_t o = from + lane; o < end; o += 32) {
+      R.dst[o] = R.src[o];
+      if (R.dst2 != nullptr) R.dst2[o] = R.src[o];
+    }
   }
 }
 
@@ -183,7 +191,8 @@ void finalize_copy_job(CopyJob& job) {
   for (uint32_t r = 0; r < job.nregions; ++r) {
     job.chunk_base[r] = chunks;
     job.reg[r].aligned = (reinterpret_cast<uintptr_t>(job.reg[r].src) % 16 == 0) &&
-                         (reinterpret_cast<uintptr_t>(job.reg[r].dst) % 16 == 0);
+                         (reinterpret_cast<uintptr_t>(job.reg[r].dst) % 16 == 0) &&
+                         (reinterpret_cast<uintptr_t>(job.reg[r].dst2) % 16 == 0);
     chunks += (job.reg[r].bytes + kCopyChunk - 1) / kCopyChunk;
   }
   for (uint32_t r = job.nregions; r < kMaxRegions; ++r) job.chunk_base[r] = ~0ull;

@@ -22,6 +22,7 @@ struct SliceRegion {
   int32_t tmap;          // index of this region's src/dst tensor-map pair, -1 = none
   uint32_t pad_;
   uint64_t nfull;        // full-length slices (the tensor maps' outer extent)
+  uint8_t* dst2;         // second replica (double-neighbour), null = none
 };
 
 constexpr int kTmaRegions = 4;  // regions that get 2-D TMA tensor maps per launch
@@ -41,10 +42,11 @@ struct SlotCommit {
 };
 
 struct SliceJob {
-  // [2*i] = source, [2*i+1] = destination of tensor-mapped region i: a 2-D
+  // [3*i] = source, [3*i+1] = destination of tensor-mapped region i: a 2-D
   // view {slice_bytes, nfull} with row pitch slice_bytes, 128 x 32 boxes,
   // 128-byte swizzle (conflict-free per-lane row reads).
-  CUtensorMap maps[2 * kTmaRegions];
+  // [3*i+2] = second destination (double-neighbour replication).
+  CUtensorMap maps[3 * kTmaRegions];
   SliceRegion reg[kMaxRegions];
   uint32_t nregions;
   uint32_t pad_;
@@ -52,6 +54,7 @@ struct SliceJob {
   uint64_t group_lo, group_hi;  // warp tasks this launch covers (a scheduler batch)
   uint64_t slice_bytes;
   uint64_t* sums_out;             // may be null
+  uint64_t* sums_out2;            // second replica's table (double-neighbour), may be null
   const uint64_t* sums_expected;  // verify mode
   const uint64_t* init_state;     // per-slice FNV start (null = offset basis)
   unsigned long long* result;     // verify mode: [first bad slice, bad count]
@@ -59,6 +62,7 @@ struct SliceJob {
                                   // (zero between launches; null = static)
   uint32_t proxy_fence;           // tensor path: generic->async proxy fence before each refill
   SlotCommit commit;
+  SlotCommit commit2;             // second replica's slot (slot null = none)
 };
 
 enum class SliceMode { Hash, Copy, CopyVerify, HashVerify };
@@ -69,8 +73,9 @@ struct CopyRegion {
   const uint8_t* src;
   uint8_t* dst;
   uint64_t bytes;
-  uint32_t aligned;  // both pointers 16-byte aligned (set by finalize_copy_job)
+  uint32_t aligned;  // all pointers 16-byte aligned (set by finalize_copy_job)
   uint32_t pad_;
+  uint8_t* dst2;     // second replica (double-neighbour), null = none
 };
 
 struct SlotMark {  // every copy CTA marks the slot WRITING first
@@ -86,6 +91,7 @@ struct CopyJob {
   uint64_t total_chunks;
   uint64_t chunk_lo, chunk_hi;  // this launch's 32 KB chunks
   SlotMark mark;
+  SlotMark mark2;
 };
 
 void finalize_copy_job(CopyJob& job);

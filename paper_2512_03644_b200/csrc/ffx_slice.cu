@@ -196,7 +196,10 @@ __global__ void __launch_bounds__(W * 32) slice_kernel(const __grid_constant__ S
   __syncwarp();
   uint32_t phase = 0;  // bit s: parity of the next completion of stage s
 
-  if constexpr (kCommit) commit_begin(job.commit);
+  if constexpr (kCommit) {
+    if (job.commit2.slot != nullptr) commit_begin(job.commit2);
+    commit_begin(job.commit);
+  }
 
   const uint64_t Sl = job.slice_bytes;
   uint64_t g_next = job.group_lo + static_cast<uint64_t>(blockIdx.x) * W + warp;
@@ -234,8 +237,10 @@ __global__ void __launch_bounds__(W * 32) slice_kernel(const __grid_constant__ S
 
     if (kTensor && R.tmap >= 0 && s0 + 32 <= R.nfull) {
       // ---- 2-D tensor TMA: one 128 x 32 box per step (4 KB), swizzled ---------------
-      const CUtensorMap* msrc = &job.maps[2 * R.tmap];
-      const CUtensorMap* mdst = &job.maps[2 * R.tmap + 1];
+      const CUtensorMap* msrc = &job.maps[3 * R.tmap];
+      const CUtensorMap* mdst = &job.maps[3 * R.tmap + 1];
+      const CUtensorMap* mdst2 = &job.maps[3 * R.tmap + 2];
+      const bool dual = R.dst2 != nullptr;
       const int nsteps = static_cast<int>(Sl / C);
       const int y = static_cast<int>(s0);
       const int pro = nsteps < S ? nsteps : S;
@@ -255,6 +260,7 @@ __global__ void __launch_bounds__(W * 32) slice_kernel(const __grid_constant__ S
         if constexpr (kCopy) {
           if (lane == 0) {
             tensor_store(mdst, k * C, y, tile);
+            if (dual) tensor_store(mdst2, k * C, y, tile);  // double neighbour: read once, write twice
             bulk_commit();
           }
         }
@@ -291,6 +297,7 @@ __global__ void __launch_bounds__(W * 32) slice_kernel(const __grid_constant__ S
         const uint32_t row = stage0 + s * K::STAGE + lane * K::ROWB;
         if constexpr (kCopy) {
           bulk_store(dst + static_cast<uint64_t>(k) * C, row, C);
+          if (R.dst2 != nullptr) bulk_store(R.dst2 + my_off + static_cast<uint64_t>(k) * C, row, C);
           bulk_commit();
         }
         const uint4* rp = reinterpret_cast<const uint4*>(wbase + s * K::STAGE + lane * K::ROWB);
@@ -318,7 +325,10 @@ __global__ void __launch_bounds__(W * 32) slice_kernel(const __grid_constant__ S
           const uint64_t o = base0 + static_cast<uint64_t>(q / K::VPL) * Sl + static_cast<uint64_t>(k) * C +
                              static_cast<uint64_t>(q % K::VPL) * 16;
           buf[i] = load16(R.src, o, R.bytes, al);
-          if constexpr (kCopy) store16(R.dst, o, R.bytes, al, buf[i]);
+          if constexpr (kCopy) {
+            store16(R.dst, o, R.bytes, al, buf[i]);
+            if (R.dst2 != nullptr) store16(R.dst2, o, R.bytes, al && aligned16(R.dst2), buf[i]);
+          }
         }
         __syncwarp();
 #pragma unroll
@@ -343,6 +353,7 @@ __global__ void __launch_bounds__(W * 32) slice_kernel(const __grid_constant__ S
       const uint64_t idx = R.slice_base + s0 + lane;
       const uint64_t v = h.value();
       if (job.sums_out != nullptr) job.sums_out[idx] = v;
+      if (job.sums_out2 != nullptr) job.sums_out2[idx] = v;
       if constexpr (kVerify) {
         if (v != job.sums_expected[idx]) {
           atomicMin(&job.result[0], static_cast<unsigned long long>(idx));
@@ -365,7 +376,10 @@ __global__ void __launch_bounds__(W * 32) slice_kernel(const __grid_constant__ S
         job.sched[1] = 0;
       }
     }
-    if constexpr (kCommit) commit_end(job.commit);
+    if constexpr (kCommit) {
+      if (job.commit2.slot != nullptr) commit_end(job.commit2);
+      commit_end(job.commit);
+    }
   }
 }
 
@@ -436,7 +450,7 @@ void finalize_job(SliceJob& job) {
     groups += (ns + 31) / 32;
   }
   for (uint32_t r = job.nregions; r < kMaxRegions; ++r)
-    job.reg[r] = SliceRegion{nullptr, nullptr, 0, slices, ~0ull, -1, 0, 0};
+    job.reg[r] = SliceRegion{nullptr, nullptr, 0, slices, ~0ull, -1, 0, 0, nullptr};
   for (uint32_t r = 0; r < kMaxRegions; ++r) job.reg[r].tmap = -1;
   job.total_groups = groups;
   job.group_lo = 0;
@@ -482,8 +496,11 @@ void attach_tensor_maps(SliceJob& job, bool copy) {
     const bool al = (reinterpret_cast<uintptr_t>(R.src) % 16 == 0) &&
                     (!copy || reinterpret_cast<uintptr_t>(R.dst) % 16 == 0);
     if (!al || R.nfull < 32 || R.nfull > (1ull << 31)) continue;
-    if (!encode_rows(&job.maps[2 * used], R.src, job.slice_bytes, R.nfull)) continue;
-    if (copy && !encode_rows(&job.maps[2 * used + 1], R.dst, job.slice_bytes, R.nfull)) continue;
+    if (R.dst2 != nullptr && reinterpret_cast<uintptr_t>(R.dst2) % 16 != 0) continue;
+    if (!encode_rows(&job.maps[3 * used], R.src, job.slice_bytes, R.nfull)) continue;
+    if (copy && !encode_rows(&job.maps[3 * used + 1], R.dst, job.slice_bytes, R.nfull)) continue;
+    if (copy && R.dst2 != nullptr && !encode_rows(&job.maps[3 * used + 2], R.dst2, job.slice_bytes, R.nfull))
+      continue;
     R.tmap = used++;
   }
 }

@@ -234,6 +234,7 @@ SIGNATURES = {
     "ffx_replica_export_frame": (_I, [_P, _U64, _P, _U64, ctypes.POINTER(_U64), _P]),
     "ffx_snapshot_target": (_I, [_P, _P]),
     "ffx_snapshot": (_I, [_P, _U64, _P, ctypes.POINTER(SnapshotOpts)]),
+    "ffx_snapshot_target2": (_I, [_P, _P]),
     "ffx_snapshot_begin": (_I, [_P, _U64, ctypes.POINTER(SnapshotOpts), ctypes.POINTER(_U32)]),
     "ffx_snapshot_next": (_I, [_P, _P, _P, ctypes.POINTER(_U32)]),
     "ffx_snapshot_next_kind": (_I, [_P, _I, _P, _P, ctypes.POINTER(_U32)]),
@@ -584,6 +585,9 @@ class Context:
 
     def set_target(self, replica: Optional[Replica]):
         check(lib.ffx_snapshot_target(self._c, replica.ptr if replica else None), "snapshot_target")
+
+    def set_target2(self, replica: Optional[Replica]):
+        check(lib.ffx_snapshot_target2(self._c, replica.ptr if replica else None), "snapshot_target2")
 
     def snapshot(self, iteration: int, stream=None, max_ctas: int = 0, batches: int = 1,
                  gate_events=None, verify_on_store: bool = False, weights_kind: bool = False,

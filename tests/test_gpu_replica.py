@@ -367,3 +367,31 @@ def test_split_policy_copy_and_hash_batches(ffx, copy_engine):
                     verify_on_store=True)
     torch.cuda.synchronize()
     assert rep.export_frame(41) == orc.pack_blob((1, 0, 0), 41, 1, concat)
+
+
+@pytest.mark.parametrize("split", [False, True])
+def test_double_neighbour_dual_store(ffx, split):
+    # Replicas at dp+1 and dp+2: one kernel, two stores per tile.
+    n = (1 << 22) + 999
+    spec = ffx.make_spec(d=4, phi=64, distributed=True)
+    h1 = ffx.Context(0, spec, (2, 0, 0))
+    h2 = ffx.Context(0, spec, (3, 0, 0))
+    origin = ffx.Context(0, spec, (1, 0, 0))
+    r1 = h1.create_replica((1, 0, 0), n, 2)
+    r2 = h2.create_replica((1, 0, 0), n, 2)
+    v1 = origin.open_replica(r1.export())
+    v2 = origin.open_replica(r2.export())
+    origin.set_target(v1)
+    origin.set_target2(v2)
+    state, want = blob_for(ffx, 1, n)
+    origin.register(ffx.REGION_BLOB, state)
+    for it in (5, 6, 7):
+        origin.snapshot(it, split=split, batches=2, hash_batches=3)
+    torch.cuda.synchronize()
+    frame = orc.pack_blob((1, 0, 0), 7, 1, want)
+    assert r1.export_frame(7) == frame and r2.export_frame(7) == frame
+    assert sorted(r1.held()) == [6, 7] and sorted(r2.held()) == [6, 7]
+    # the first holder is lost with its neighbour: recover from dp+2
+    origin.inject(ffx.FAULT_POISON_STATE)
+    origin.recover(v2, 7)
+    assert host(state) == want
