@@ -63,6 +63,9 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-llama", action="store_true", help="skip the Llama-3 8B recovery/overhead legs")
     ap.add_argument("--sched-ctas", type=int, default=32, help="SM budget of scheduled snapshot batches")
+    ap.add_argument("--mode", default="pull", choices=["push", "pull"],
+                    help="N>1 ring stream: origin pushes into its successor's replica, or the holder "
+                         "pulls its predecessor's regions (NeighborBuffer::store side)")
     return ap.parse_args()
 
 
@@ -227,8 +230,22 @@ class Ring:
             self.ctx.register(kind, t)
             self.state.append(t)
         del pyoracle
+        # pull mode: map the ring predecessor's regions (the origin of `held`)
+        self.remote = None
+        if world > 1:
+            exported = [None] * world
+            dist.all_gather_object(exported, self.ctx.export_regions())
+            self.remote = self.ctx.open_remote(exported[ring.predecessor(rank, world)])
+
+    def snapshot(self, it, stream, mode, max_ctas=0):
+        if mode == "pull" and self.remote is not None:
+            self.ctx.snapshot_pull(self.remote, self.held, it, stream=stream, max_ctas=max_ctas)
+        else:
+            self.ctx.snapshot(it, stream=stream, max_ctas=max_ctas)
 
     def close(self):
+        if self.remote is not None:
+            self.remote.close()
         for r in (self.target, self.held):
             try:
                 r.destroy()
@@ -290,7 +307,7 @@ def main():
     it = 0
     for _ in range(args.warmup):
         it += 1
-        R.ctx.snapshot(it, stream=stream, max_ctas=args.max_ctas)
+        R.snapshot(it, stream, args.mode, args.max_ctas)
     stream.synchronize()
     launches0 = R.ctx.stats().kernel_launches
     barrier()
@@ -302,7 +319,7 @@ def main():
     e0.record(stream)
     for _ in range(args.steps):
         it += 1
-        R.ctx.snapshot(it, stream=stream, max_ctas=args.max_ctas)
+        R.snapshot(it, stream, args.mode, args.max_ctas)
     e1.record(stream)
     stream.synchronize()
     ck = clocks.stop()
@@ -312,6 +329,23 @@ def main():
     per_step_ms = ms_max / args.steps
     value = world * n * args.steps / (ms_max * 1e-3) / 1e9
     commit_ok = R.target.newest() == it
+
+    # the other ring-stream mode on the same buffers, for comparison
+    alt = None
+    if world > 1:
+        other = "push" if args.mode == "pull" else "pull"
+        barrier()
+        torch.cuda.synchronize()
+        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a0.record(stream)
+        for _ in range(args.steps):
+            it += 1
+            R.snapshot(it, stream, other, args.max_ctas)
+        a1.record(stream)
+        stream.synchronize()
+        barrier()
+        ams = max_over_ranks(a0.elapsed_time(a1))
+        alt = {"mode": other, "per_gpu_gbs": round(n * args.steps / (ams * 1e-3) / 1e9, 2)}
 
     # ---- recovery: rank (1 % world) loses its state and pulls it back --------
     fail_rank = 1 % world
@@ -346,7 +380,7 @@ def main():
                     f0.record(stream)
                 it += 1
                 R.state[0].copy_(host, non_blocking=True)        # take(it, host_ptr, len): H2D
-                R.ctx.snapshot(it, stream=stream, max_ctas=args.max_ctas)
+                R.snapshot(it, stream, args.mode, args.max_ctas)
                 R.ctx.read_sums(table_host, stream=stream)       # D2H of the step's result
             f1.record(stream)
         stream.synchronize()
@@ -403,10 +437,12 @@ def main():
                                    % (n, "1-GPU local replica" if world == 1 else "ring-neighbour replica over NVLink"),
                        "bytes_per_rank": n, "slice_bytes": args.slice_bytes, "replica_versions": 2,
                        "l2": "inputs 2.3 GB/rank > 126 MB L2; no flush needed",
-                       "parallelism": "dp%d ring" % world if world > 1 else "single GPU"},
+                       "parallelism": "dp%d ring" % world if world > 1 else "single GPU",
+                       "ring_stream": args.mode if world > 1 else "local"},
             "per_gpu_gbs": round(value / world, 3),
             "nvlink_frac_per_gpu": round(value / world / NVLINK_MEASURED_GBS, 4) if world > 1 else None,
-            "roofline": roof, "recovery": rec, "llama3_8b": llama, "cpu_baseline": cpu, "e2e": e2e,
+            "roofline": roof, "recovery": rec, "alt_ring_stream": alt, "llama3_8b": llama,
+            "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": int(launches), "clocks": ck, "commit_ok": bool(commit_ok),
         }), flush=True)
 

@@ -317,6 +317,29 @@ int ffx_snapshot_next_kind(ffx_ctx* ctx, int kind, void* stream, void* gate_even
 int ffx_snapshot_read_sums(ffx_ctx* ctx, uint64_t* host_dst, uint64_t max_entries, uint64_t* n_out,
                            void* stream);
 
+/* ---- pull mode: the holder drives the ring stream -------------------------
+ * NeighborBuffer::store is the holder's action in the reference
+ * (ckpt.cpp:77-93).  In pull mode the holder's kernel reads the origin's
+ * registered regions over NVLink (peer loads run at the link's full read
+ * rate), hashes them and commits its own slot; the commit also sets the
+ * origin's ack word, which the origin's stream waits on before its next
+ * optimizer update (ffx_snapshot_wait_pulled). */
+#define FFX_REGIONS_HANDLE_BYTES 2048
+typedef struct ffx_remote ffx_remote;
+/* Origin: describe this ctx's unique regions (CUDA IPC) for its holder. */
+int ffx_regions_export(ffx_ctx* ctx, uint8_t handle[FFX_REGIONS_HANDLE_BYTES]);
+/* Holder: map an origin's regions. */
+int ffx_remote_open(ffx_ctx* ctx, const uint8_t handle[FFX_REGIONS_HANDLE_BYTES], ffx_remote** out);
+int ffx_remote_close(ffx_remote* r);
+/* Holder: snapshot `origin` at `iteration` into the replica it holds for it. */
+int ffx_snapshot_pull(ffx_ctx* ctx, ffx_remote* origin, ffx_replica* held, uint64_t iteration, void* stream,
+                      const ffx_snapshot_opts* opts);
+int ffx_snapshot_begin_pull(ffx_ctx* ctx, ffx_remote* origin, ffx_replica* held, uint64_t iteration,
+                            const ffx_snapshot_opts* opts, uint32_t* batches);
+/* Origin: make `stream` wait until the holder has committed `iteration`
+ * (cuStreamWaitValue64 on the ack word; no kernel, no host round trip). */
+int ffx_snapshot_wait_pulled(ffx_ctx* ctx, uint64_t iteration, void* stream);
+
 /* ---- recovery (assemble_restore, ckpt.cpp:111-167) ------------------------ */
 
 typedef struct ffx_recover_report {

@@ -73,6 +73,11 @@ uint64_t rd(const uint8_t* p, int n) {
   return v;
 }
 
+// ctx scratch words (ctx->done, 64 x u32): 0 commit counter, 4 second-replica
+// commit counter, 8-9 snapshot task counter, 12-13 verify task counter,
+// 16-17 split hash-batch task counter, 24-25 pull-mode ack (u64).
+constexpr uint32_t kAckWord = 24;
+
 bool valid_spec(const ffx_cluster_spec* s) {
   return s && s->data_parallel && s->pipeline_parallel && s->tensor_parallel && s->gpus_per_node;
 }
@@ -125,6 +130,8 @@ struct PendingSnapshot {
   // split policy: copy batches and hash batches drain independently
   bool split = false, copy_engine = false;
   CopyJob copy{};
+  ffx_replica* tgt = nullptr;   // destination replica(s) of this snapshot
+  ffx_replica* tgt2 = nullptr;
   uint32_t hbatches = 0, hnext = 0, hash_ctas = 0;
 };
 
@@ -144,6 +151,7 @@ struct ffx_ctx {
   cudaEvent_t copy_done = nullptr, hash_done = nullptr;  // split-policy joins
   uint64_t seq = 0;
   uint32_t last_slot = 0;
+  ffx_replica* last_target = nullptr;
   uint64_t last_nslices = 0;
   ffx_stats stats{};
 };
@@ -829,6 +837,7 @@ extern "C" int ffx_replica_destroy(ffx_replica* r) {
   if (!r) return FFX_OK;
   if (r->ctx && r->ctx->target == r) r->ctx->target = nullptr;
   if (r->ctx && r->ctx->target2 == r) r->ctx->target2 = nullptr;
+  if (r->ctx && r->ctx->last_target == r) r->ctx->last_target = nullptr;
   DeviceGuard g(r->ctx ? r->ctx->device : r->device);
   if (r->owned && r->base) cudaFree(r->base);
   if (r->ipc_opened && r->base) cudaIpcCloseMemHandle(r->base);
@@ -1026,45 +1035,60 @@ uint32_t pick_slot(const ffx_replica* t, uint64_t iteration) {
 
 }  // namespace
 
-extern "C" int ffx_snapshot_begin(ffx_ctx* c, uint64_t iteration, const ffx_snapshot_opts* o,
-                                  uint32_t* batches_out) {
-  if (!c) return fail(FFX_EINVAL, "snapshot: null ctx");
-  ffx_replica* t = c->target;
-  if (!t) return fail(FFX_ESTATE, "snapshot: no target replica (ffx_snapshot_target)");
+namespace {
+
+struct SrcRegion {
+  const uint8_t* dev;  // local or peer-mapped
+  uint64_t bytes;
+};
+
+// Shared by push (sources = this rank's registered regions, destination = the
+// successor's replica) and pull (sources = the predecessor's regions mapped
+// over NVLink, destination = the replica this rank holds).
+int begin_impl(ffx_ctx* c, ffx_replica* t, ffx_replica* t2, const std::vector<SrcRegion>& srcs, ffx_role role,
+               uint64_t* ack, uint64_t iteration, const ffx_snapshot_opts* o, uint32_t* batches_out) {
   if (c->pending.active)
     return fail(FFX_ESTATE, "snapshot of iteration %llu still has %u batches to issue",
                 (unsigned long long)c->pending.iteration, c->pending.batches - c->pending.next);
+  if (srcs.size() > kMaxRegions) return fail(FFX_ECONFIG, "at most %u regions", kMaxRegions);
   ffx_snapshot_opts opts{};
   if (o) opts = *o;
-  const PayloadMap pm = payload_map(c);
-  if (pm.logical > t->capacity)
-    return fail(FFX_ECONFIG, "snapshot payload %llu exceeds the replica buffer of %llu bytes",
-                (unsigned long long)pm.logical, (unsigned long long)t->capacity);
-  if (pm.physical > t->layout.payload_cap)
-    return fail(FFX_ECONFIG, "snapshot regions need %llu payload bytes, slot has %llu",
-                (unsigned long long)pm.physical, (unsigned long long)t->layout.payload_cap);
-  uint64_t nslices = 0;
-  for (const Region* r : pm.regs) nslices += slices_of(r->bytes, c->slice_bytes);
-  if (nslices > t->layout.table_cap)
-    return fail(FFX_ECONFIG, "snapshot needs %llu checksum entries, slot has %llu",
-                (unsigned long long)nslices, (unsigned long long)t->layout.table_cap);
-
-  ffx_replica* t2 = c->target2;
-  if (t2) {
-    if (pm.logical > t2->capacity || pm.physical > t2->layout.payload_cap || nslices > t2->layout.table_cap)
-      return fail(FFX_ECONFIG, "snapshot payload %llu exceeds the second replica buffer of %llu bytes",
-                  (unsigned long long)pm.logical, (unsigned long long)t2->capacity);
+  uint64_t logical = 0, physical = 0, nslices = 0;
+  std::vector<uint64_t> offs;
+  for (const SrcRegion& r : srcs) {
+    offs.push_back(physical);
+    logical += r.bytes;
+    physical = align_up(physical + r.bytes, kRegionAlign);
+    nslices += slices_of(r.bytes, c->slice_bytes);
+  }
+  for (ffx_replica* rr : {t, t2}) {
+    if (!rr) continue;
+    if (logical > rr->capacity)
+      return fail(FFX_ECONFIG, "snapshot payload %llu exceeds the replica buffer of %llu bytes",
+                  (unsigned long long)logical, (unsigned long long)rr->capacity);
+    if (physical > rr->layout.payload_cap)
+      return fail(FFX_ECONFIG, "snapshot regions need %llu payload bytes, slot has %llu",
+                  (unsigned long long)physical, (unsigned long long)rr->layout.payload_cap);
+    if (nslices > rr->layout.table_cap)
+      return fail(FFX_ECONFIG, "snapshot needs %llu checksum entries, slot has %llu",
+                  (unsigned long long)nslices, (unsigned long long)rr->layout.table_cap);
   }
   const uint32_t slot = pick_slot(t, iteration);
   const uint32_t slot2 = t2 ? pick_slot(t2, iteration) : 0;
-  const uint64_t seq = ++c->seq;
+  uint64_t seq = ++c->seq;
+  for (ffx_replica* rr : {t, t2})
+    if (rr)
+      for (const auto& sc : rr->cache) seq = std::max(seq, sc.seq + 1);
+  c->seq = seq;
 
   PendingSnapshot& P = c->pending;
   P = PendingSnapshot{};
+  P.tgt = t;
+  P.tgt2 = t2;
   SliceJob& job = P.job;
-  job.nregions = static_cast<uint32_t>(pm.regs.size());
-  for (size_t i = 0; i < pm.regs.size(); ++i)
-    job.reg[i] = SliceRegion{pm.regs[i]->dev, t->payload(slot) + pm.offs[i], pm.regs[i]->bytes, 0, 0};
+  job.nregions = static_cast<uint32_t>(srcs.size());
+  for (size_t i = 0; i < srcs.size(); ++i)
+    job.reg[i] = SliceRegion{srcs[i].dev, t->payload(slot) + offs[i], srcs[i].bytes, 0, 0};
   job.slice_bytes = c->slice_bytes;
   job.sums_out = t->sums(slot);
   job.sched = c->done + 8;  // dynamic task counter (words 8-9 of the ctx scratch)
@@ -1075,17 +1099,17 @@ extern "C" int ffx_snapshot_begin(ffx_ctx* c, uint64_t iteration, const ffx_snap
   m.state = kSlotCommitted;
   m.iteration = iteration;
   m.seq = seq;
-  m.payload_len = pm.logical;
+  m.payload_len = logical;
   m.slice_bytes = c->slice_bytes;
   m.num_slices = nslices;
-  m.dp = c->self.dp;
-  m.pp = c->self.pp;
-  m.tp = c->self.tp;
+  m.dp = role.dp;
+  m.pp = role.pp;
+  m.tp = role.tp;
   m.kind = opts.weights_kind ? 0 : 1;
   m.num_regions = job.nregions;
-  for (size_t i = 0; i < pm.regs.size(); ++i) m.region_bytes[i] = pm.regs[i]->bytes;
+  for (size_t i = 0; i < srcs.size(); ++i) m.region_bytes[i] = srcs[i].bytes;
   uint8_t hdr[32];
-  ffx_pack_header(c->self, iteration, m.kind, pm.logical > 0xffffffffull ? 0 : pm.logical, 0, hdr);
+  ffx_pack_header(role, iteration, m.kind, logical > 0xffffffffull ? 0 : logical, 0, hdr);
 
   SlotCommit& cm = job.commit;
   cm.slot = t->slot(slot);
@@ -1095,10 +1119,12 @@ extern "C" int ffx_snapshot_begin(ffx_ctx* c, uint64_t iteration, const ffx_snap
   cm.seq = seq;
   std::memcpy(cm.meta, &m, sizeof m);
   std::memcpy(cm.snp1, hdr, 32);
+  cm.ack = ack;
+  cm.ack_value = iteration;
   if (t2) {
     // Double-neighbour replication: the same tiles stored twice, one table
     // per replica, each slot committed by its own counter.
-    for (size_t i = 0; i < pm.regs.size(); ++i) job.reg[i].dst2 = t2->payload(slot2) + pm.offs[i];
+    for (size_t i = 0; i < srcs.size(); ++i) job.reg[i].dst2 = t2->payload(slot2) + offs[i];
     job.sums_out2 = t2->sums(slot2);
     job.commit2 = cm;
     job.commit2.slot = t2->slot(slot2);
@@ -1114,9 +1140,13 @@ extern "C" int ffx_snapshot_begin(ffx_ctx* c, uint64_t iteration, const ffx_snap
   P.iteration = iteration;
   P.seq = seq;
   P.nslices = nslices;
-  P.logical = pm.logical;
+  P.logical = logical;
   P.verify = opts.verify_on_store != 0;
   P.split = opts.split != 0;
+  if (P.split && ack) {
+    P.active = false;
+    return fail(FFX_EINVAL, "pull snapshots are fused (the split policy is push-only)");
+  }
   if (P.split) {
     // Copy batches: TMA copy-only (or copy engines) into the slot payload.
     P.copy_engine = opts.copy_engine != 0;
@@ -1134,6 +1164,210 @@ extern "C" int ffx_snapshot_begin(ffx_ctx* c, uint64_t iteration, const ffx_snap
   }
   if (batches_out) *batches_out = P.batches;
   return FFX_OK;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// pull mode: the holder reads the origin's registered regions over NVLink
+
+struct ffx_remote {
+  ffx_ctx* ctx = nullptr;  // holder context that opened it
+  ffx_role role{};
+  std::vector<SrcRegion> regs;
+  uint64_t* ack = nullptr;      // origin's ack word (peer-mapped)
+  std::vector<void*> opened;    // IPC mappings to close
+};
+
+namespace {
+
+constexpr uint32_t kRegionsMagic = 0x47524646u;  // "FFRG"
+
+struct RegionsBlob {
+  uint32_t magic, abi;
+  int32_t pid, device;
+  uint16_t dp, pp, tp, pad_;
+  uint32_t nregions;
+  cudaIpcMemHandle_t ack_ipc;
+  uint64_t ack_off, ack_raw;
+  struct Entry {
+    cudaIpcMemHandle_t ipc;
+    uint64_t off, raw, bytes;
+  } r[kMaxRegions];
+};
+static_assert(sizeof(RegionsBlob) <= FFX_REGIONS_HANDLE_BYTES, "regions handle too large");
+
+template <typename Fn>
+Fn driver_fn(const char* name) {
+  void* p = nullptr;
+  cudaDriverEntryPointQueryResult q{};
+  if (cudaGetDriverEntryPoint(name, &p, cudaEnableDefault, &q) != cudaSuccess || q != cudaDriverEntryPointSuccess)
+    return nullptr;
+  return reinterpret_cast<Fn>(p);
+}
+
+// Allocation base of a device pointer (IPC handles name whole allocations).
+int alloc_base(const void* p, uint8_t** base) {
+  using Fn = CUresult (*)(CUdeviceptr*, size_t*, CUdeviceptr);
+  static Fn fn = driver_fn<Fn>("cuMemGetAddressRange");
+  if (!fn) return fail(FFX_ECUDA, "cuMemGetAddressRange unavailable");
+  CUdeviceptr b = 0;
+  size_t sz = 0;
+  if (fn(&b, &sz, reinterpret_cast<CUdeviceptr>(p)) != CUDA_SUCCESS)
+    return fail(FFX_EINVAL, "pointer %p is not device memory", p);
+  *base = reinterpret_cast<uint8_t*>(b);
+  return FFX_OK;
+}
+
+}  // namespace
+
+extern "C" int ffx_regions_export(ffx_ctx* c, uint8_t handle[FFX_REGIONS_HANDLE_BYTES]) {
+  if (!c || !handle) return fail(FFX_EINVAL, "regions_export: null argument");
+  DeviceGuard g(c->device);
+  RegionsBlob b{};
+  b.magic = kRegionsMagic;
+  b.abi = FFX_ABI_VERSION;
+  b.pid = getpid();
+  b.device = c->device;
+  b.dp = c->self.dp;
+  b.pp = c->self.pp;
+  b.tp = c->self.tp;
+  uint8_t* base = nullptr;
+  uint8_t* ack = reinterpret_cast<uint8_t*>(c->done + kAckWord);
+  int st = alloc_base(ack, &base);
+  if (st) return st;
+  FFX_CUDA(cudaIpcGetMemHandle(&b.ack_ipc, base));
+  b.ack_off = static_cast<uint64_t>(ack - base);
+  b.ack_raw = reinterpret_cast<uint64_t>(ack);
+  for (const auto& r : c->regions) {
+    if (!r.unique) continue;
+    auto& e = b.r[b.nregions++];
+    e.bytes = r.bytes;
+    e.raw = reinterpret_cast<uint64_t>(r.dev);
+    if (r.bytes == 0) continue;
+    st = alloc_base(r.dev, &base);
+    if (st) return st;
+    FFX_CUDA(cudaIpcGetMemHandle(&e.ipc, base));
+    e.off = static_cast<uint64_t>(r.dev - base);
+  }
+  std::memset(handle, 0, FFX_REGIONS_HANDLE_BYTES);
+  std::memcpy(handle, &b, sizeof b);
+  return FFX_OK;
+}
+
+extern "C" int ffx_remote_open(ffx_ctx* c, const uint8_t handle[FFX_REGIONS_HANDLE_BYTES], ffx_remote** out) {
+  if (!c || !handle || !out) return fail(FFX_EINVAL, "remote_open: null argument");
+  RegionsBlob b;
+  std::memcpy(&b, handle, sizeof b);
+  if (b.magic != kRegionsMagic || b.abi != FFX_ABI_VERSION)
+    return fail(FFX_EINVAL, "remote_open: not an ffx regions handle");
+  DeviceGuard g(c->device);
+  auto* r = new ffx_remote;
+  r->ctx = c;
+  r->role = ffx_role{b.dp, b.pp, b.tp};
+  const bool local = b.pid == getpid();
+  std::vector<std::pair<std::string, uint8_t*>> seen;  // one mapping per exported allocation
+  auto map = [&](const cudaIpcMemHandle_t& h, uint8_t** base) -> int {
+    const std::string key(reinterpret_cast<const char*>(&h), sizeof h);
+    for (const auto& kv : seen)
+      if (kv.first == key) {
+        *base = kv.second;
+        return FFX_OK;
+      }
+    void* p = nullptr;
+    cudaError_t e = cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaIpcOpenMemHandle");
+    r->opened.push_back(p);
+    seen.emplace_back(key, static_cast<uint8_t*>(p));
+    *base = static_cast<uint8_t*>(p);
+    return FFX_OK;
+  };
+  if (local && b.device != c->device) {
+    cudaError_t e = cudaDeviceEnablePeerAccess(b.device, 0);
+    if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+    else if (e != cudaSuccess) {
+      delete r;
+      return cuda_fail(e, "cudaDeviceEnablePeerAccess");
+    }
+  }
+  int st = FFX_OK;
+  uint8_t* base = nullptr;
+  if (local) {
+    r->ack = reinterpret_cast<uint64_t*>(b.ack_raw);
+  } else if (!(st = map(b.ack_ipc, &base))) {
+    r->ack = reinterpret_cast<uint64_t*>(base + b.ack_off);
+  }
+  for (uint32_t i = 0; i < b.nregions && !st; ++i) {
+    const auto& e = b.r[i];
+    if (local || e.bytes == 0) {
+      r->regs.push_back(SrcRegion{reinterpret_cast<const uint8_t*>(e.raw), e.bytes});
+    } else if (!(st = map(e.ipc, &base))) {
+      r->regs.push_back(SrcRegion{base + e.off, e.bytes});
+    }
+  }
+  if (st) {
+    ffx_remote_close(r);
+    return st;
+  }
+  *out = r;
+  return FFX_OK;
+}
+
+extern "C" int ffx_remote_close(ffx_remote* r) {
+  if (!r) return FFX_OK;
+  DeviceGuard g(r->ctx ? r->ctx->device : 0);
+  for (void* p : r->opened) cudaIpcCloseMemHandle(p);
+  delete r;
+  return FFX_OK;
+}
+
+extern "C" int ffx_snapshot_begin_pull(ffx_ctx* c, ffx_remote* origin, ffx_replica* held, uint64_t iteration,
+                                       const ffx_snapshot_opts* o, uint32_t* batches_out) {
+  if (!c || !origin || !held) return fail(FFX_EINVAL, "snapshot_pull: null argument");
+  if (held->origin.dp != origin->role.dp || held->origin.pp != origin->role.pp ||
+      held->origin.tp != origin->role.tp)
+    return fail(FFX_ECONFIG, "replica is for d%up%ut%u, origin is d%up%ut%u", held->origin.dp, held->origin.pp,
+                held->origin.tp, origin->role.dp, origin->role.pp, origin->role.tp);
+  return begin_impl(c, held, nullptr, origin->regs, origin->role, origin->ack, iteration, o, batches_out);
+}
+
+extern "C" int ffx_snapshot_pull(ffx_ctx* c, ffx_remote* origin, ffx_replica* held, uint64_t iteration,
+                                 void* stream, const ffx_snapshot_opts* o) {
+  uint32_t batches = 1;
+  int st = ffx_snapshot_begin_pull(c, origin, held, iteration, o, &batches);
+  if (st) return st;
+  auto* gates = o ? static_cast<void**>(o->gate_events) : nullptr;
+  for (uint32_t b = 0; b < batches; ++b) {
+    uint32_t left = 0;
+    st = ffx_snapshot_next_kind(c, FFX_BATCH_COPY, stream, gates ? gates[b] : nullptr, &left);
+    if (st) {
+      c->pending.active = false;
+      return st;
+    }
+  }
+  return FFX_OK;
+}
+
+extern "C" int ffx_snapshot_wait_pulled(ffx_ctx* c, uint64_t iteration, void* stream) {
+  if (!c) return fail(FFX_EINVAL, "wait_pulled: null ctx");
+  using Fn = CUresult (*)(CUstream, CUdeviceptr, cuuint64_t, unsigned int);
+  static Fn fn = driver_fn<Fn>("cuStreamWaitValue64");
+  if (!fn) return fail(FFX_ECUDA, "cuStreamWaitValue64 unavailable");
+  DeviceGuard g(c->device);
+  if (fn(static_cast<CUstream>(stream), reinterpret_cast<CUdeviceptr>(c->done + kAckWord), iteration,
+         CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS)
+    return fail(FFX_ECUDA, "cuStreamWaitValue64 failed");
+  return FFX_OK;
+}
+
+extern "C" int ffx_snapshot_begin(ffx_ctx* c, uint64_t iteration, const ffx_snapshot_opts* o,
+                                  uint32_t* batches_out) {
+  if (!c) return fail(FFX_EINVAL, "snapshot: null ctx");
+  if (!c->target) return fail(FFX_ESTATE, "snapshot: no target replica (ffx_snapshot_target)");
+  std::vector<SrcRegion> srcs;
+  for (const auto& r : c->regions)
+    if (r.unique) srcs.push_back(SrcRegion{r.dev, r.bytes});
+  return begin_impl(c, c->target, c->target2, srcs, c->self, nullptr, iteration, o, batches_out);
 }
 
 namespace {
@@ -1218,9 +1452,10 @@ int issue_hash_batch(ffx_ctx* c, PendingSnapshot& P, uint32_t b, cudaStream_t s)
 
 int finish_snapshot(ffx_ctx* c, PendingSnapshot& P, cudaStream_t s) {
   P.active = false;
-  ffx_replica* t = c->target;
+  ffx_replica* t = P.tgt;
   t->cache[P.slot] = SlotCache{true, kSlotCommitted, P.iteration, P.seq};
-  if (c->target2) c->target2->cache[P.slot2] = SlotCache{true, kSlotCommitted, P.iteration, P.seq};
+  if (P.tgt2) P.tgt2->cache[P.slot2] = SlotCache{true, kSlotCommitted, P.iteration, P.seq};
+  c->last_target = t;
   c->last_slot = P.slot;
   c->last_nslices = P.nslices;
   c->stats.snapshots++;
@@ -1309,12 +1544,12 @@ extern "C" int ffx_snapshot(ffx_ctx* c, uint64_t iteration, void* stream, const 
 extern "C" int ffx_snapshot_read_sums(ffx_ctx* c, uint64_t* host_dst, uint64_t max_entries,
                                       uint64_t* n_out, void* stream) {
   if (!c || !n_out) return fail(FFX_EINVAL, "snapshot_read_sums: null argument");
-  if (!c->target || !c->stats.snapshots) return fail(FFX_ESTATE, "snapshot_read_sums: no snapshot taken");
+  if (!c->last_target || !c->stats.snapshots) return fail(FFX_ESTATE, "snapshot_read_sums: no snapshot taken");
   const uint64_t n = std::min(max_entries, c->last_nslices);
   *n_out = n;
   if (n && host_dst) {
     DeviceGuard g(c->device);
-    FFX_CUDA(cudaMemcpyAsync(host_dst, c->target->sums(c->last_slot), n * 8, cudaMemcpyDefault,
+    FFX_CUDA(cudaMemcpyAsync(host_dst, c->last_target->sums(c->last_slot), n * 8, cudaMemcpyDefault,
                              as_stream(stream)));
   }
   return FFX_OK;

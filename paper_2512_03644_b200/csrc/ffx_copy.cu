@@ -182,6 +182,10 @@ __global__ void commit_kernel(const __grid_constant__ SlotCommit c) {
   __threadfence_system();
   reinterpret_cast<volatile SlotMeta*>(c.slot)->state = kSlotCommitted;
   __threadfence_system();
+  if (c.ack != nullptr) {
+    *reinterpret_cast<volatile uint64_t*>(c.ack) = c.ack_value;
+    __threadfence_system();
+  }
 }
 
 }  // namespace

@@ -39,6 +39,8 @@ struct SlotCommit {
   uint64_t iteration, seq;
   uint4 meta[kMetaBytes / 16];  // final SlotMeta image (state field = COMMITTED)
   uint4 snp1[2];                // SNP1 header image
+  uint64_t* ack;                // pull mode: origin's word set to ack_value after commit
+  uint64_t ack_value;
 };
 
 struct SliceJob {

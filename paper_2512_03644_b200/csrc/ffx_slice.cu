@@ -159,6 +159,10 @@ __device__ __forceinline__ void commit_end(const SlotCommit& c) {
   __threadfence_system();
   reinterpret_cast<volatile SlotMeta*>(c.slot)->state = kSlotCommitted;
   __threadfence_system();
+  if (c.ack != nullptr) {  // pull mode: release the origin's optimizer update
+    *reinterpret_cast<volatile uint64_t*>(c.ack) = c.ack_value;
+    __threadfence_system();
+  }
   *c.done = 0;
 }
 

@@ -21,6 +21,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libffx.so")
 ABI_VERSION = 1
 HANDLE_BYTES = 256
+REGIONS_HANDLE_BYTES = 2048
 MAX_REGIONS = 16
 
 # status codes (ffx.h)
@@ -235,6 +236,12 @@ SIGNATURES = {
     "ffx_snapshot_target": (_I, [_P, _P]),
     "ffx_snapshot": (_I, [_P, _U64, _P, ctypes.POINTER(SnapshotOpts)]),
     "ffx_snapshot_target2": (_I, [_P, _P]),
+    "ffx_regions_export": (_I, [_P, _P]),
+    "ffx_remote_open": (_I, [_P, _P, ctypes.POINTER(_P)]),
+    "ffx_remote_close": (_I, [_P]),
+    "ffx_snapshot_pull": (_I, [_P, _P, _P, _U64, _P, ctypes.POINTER(SnapshotOpts)]),
+    "ffx_snapshot_begin_pull": (_I, [_P, _P, _P, _U64, ctypes.POINTER(SnapshotOpts), ctypes.POINTER(_U32)]),
+    "ffx_snapshot_wait_pulled": (_I, [_P, _U64, _P]),
     "ffx_snapshot_begin": (_I, [_P, _U64, ctypes.POINTER(SnapshotOpts), ctypes.POINTER(_U32)]),
     "ffx_snapshot_next": (_I, [_P, _P, _P, ctypes.POINTER(_U32)]),
     "ffx_snapshot_next_kind": (_I, [_P, _I, _P, _P, ctypes.POINTER(_U32)]),
@@ -531,6 +538,22 @@ class Replica:
             self._h = ctypes.c_void_p(0)
 
 
+class Remote:
+    """An origin rank's regions mapped into a holder (pull mode)."""
+
+    def __init__(self, handle_ptr: int):
+        self._h = ctypes.c_void_p(handle_ptr)
+
+    @property
+    def ptr(self):
+        return self._h
+
+    def close(self):
+        if self._h:
+            check(lib.ffx_remote_close(self._h), "remote_close")
+            self._h = ctypes.c_void_p(0)
+
+
 class Context:
     """One rank's ffx context: state registry, snapshot issue, recovery."""
 
@@ -585,6 +608,29 @@ class Context:
 
     def set_target(self, replica: Optional[Replica]):
         check(lib.ffx_snapshot_target(self._c, replica.ptr if replica else None), "snapshot_target")
+
+    # ---- pull mode -------------------------------------------------------------
+    def export_regions(self) -> bytes:
+        buf = ctypes.create_string_buffer(REGIONS_HANDLE_BYTES)
+        check(lib.ffx_regions_export(self._c, buf), "regions_export")
+        return buf.raw
+
+    def open_remote(self, handle: bytes) -> "Remote":
+        h = ctypes.c_void_p()
+        check(lib.ffx_remote_open(self._c, ctypes.create_string_buffer(bytes(handle), REGIONS_HANDLE_BYTES),
+                                  ctypes.byref(h)), "remote_open")
+        return Remote(h.value)
+
+    def snapshot_pull(self, origin: "Remote", held: Replica, iteration: int, stream=None, max_ctas: int = 0,
+                      batches: int = 1):
+        o = SnapshotOpts()
+        o.max_ctas = max_ctas
+        o.batches = batches
+        check(lib.ffx_snapshot_pull(self._c, origin.ptr, held.ptr, iteration, _stream_ptr(stream),
+                                    ctypes.byref(o)), "snapshot_pull")
+
+    def wait_pulled(self, iteration: int, stream=None):
+        check(lib.ffx_snapshot_wait_pulled(self._c, iteration, _stream_ptr(stream)), "snapshot_wait_pulled")
 
     def set_target2(self, replica: Optional[Replica]):
         check(lib.ffx_snapshot_target2(self._c, replica.ptr if replica else None), "snapshot_target2")
