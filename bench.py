@@ -486,7 +486,8 @@ def llama_leg(args, ffx, torch, dist, world, rank, local, barrier):
         runs = []
         for policy, kw in (("fused", {"copy_ctas": args.sched_ctas}),
                            ("split", {"copy_ctas": 8, "hash_ctas": 96}),
-                           ("split", {"copy_ctas": 8, "hash_ctas": 96, "copy_engine": True})):
+                           ("split", {"copy_ctas": 8, "hash_ctas": 96, "copy_engine": True}),
+                           ("split", {"copy_ctas": 8, "hash_ctas": 32, "copy_engine": True})):
             sched = SliceScheduler(R.ctx, step, policy=policy, **kw)
             runs.append(measure_overhead(step, sched, steps=6, warmup=2, it0=10 + 1000 * len(runs)))
         best = min(runs, key=lambda r: r["overhead_pct"])
