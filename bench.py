@@ -63,7 +63,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-llama", action="store_true", help="skip the Llama-3 8B recovery/overhead legs")
     ap.add_argument("--sched-ctas", type=int, default=32, help="SM budget of scheduled snapshot batches")
-    ap.add_argument("--mode", default="pull", choices=["push", "pull"],
+    ap.add_argument("--mode", default="push", choices=["push", "pull"],
                     help="N>1 ring stream: origin pushes into its successor's replica, or the holder "
                          "pulls its predecessor's regions (NeighborBuffer::store side)")
     return ap.parse_args()
@@ -487,9 +487,9 @@ def llama_leg(args, ffx, torch, dist, world, rank, local, barrier):
         for policy, kw in (("fused", {"copy_ctas": args.sched_ctas}),
                            ("split", {"copy_ctas": 8, "hash_ctas": 96}),
                            ("split", {"copy_ctas": 8, "hash_ctas": 96, "copy_engine": True}),
-                           ("split", {"copy_ctas": 8, "hash_ctas": 32, "copy_engine": True})):
+                           ("split", {"copy_ctas": 8, "hash_ctas": 0, "copy_engine": True})):
             sched = SliceScheduler(R.ctx, step, policy=policy, **kw)
-            runs.append(measure_overhead(step, sched, steps=6, warmup=2, it0=10 + 1000 * len(runs)))
+            runs.append(measure_overhead(step, sched, steps=8, warmup=2, it0=10 + 1000 * len(runs)))
         best = min(runs, key=lambda r: r["overhead_pct"])
         out["step_overhead"] = dict(best, all_policies=runs)
         # the snapshots taken inside the step must recover bit-exactly too

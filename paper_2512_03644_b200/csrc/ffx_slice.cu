@@ -41,6 +41,16 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
+// Volatile so a row's loads issue back to back ahead of its hashing rather
+// than being sunk next to their first use.
+__device__ __forceinline__ uint4 lds128(const void* p) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "r"(smem_u32(p)));
+  return v;
+}
+
 // 16 bytes at base+o, zero past `bytes`; byte loads when unaligned / ragged.
 __device__ __forceinline__ uint4 load16(const uint8_t* base, uint64_t o, uint64_t bytes, bool al) {
   if (al && o + 16 <= bytes) return ld_stream(base + o);
@@ -256,6 +266,7 @@ __global__ void __launch_bounds__(W * 32) slice_kernel(const __grid_constant__ S
         }
       }
       const int sw = lane & 7;
+      uint4 v[K::VPL];
       for (int k = 0; k < nsteps; ++k) {
         const int s = k % S;
         mbar_wait(bar0 + 8 * s, (phase >> s) & 1u);
@@ -270,7 +281,9 @@ __global__ void __launch_bounds__(W * 32) slice_kernel(const __grid_constant__ S
         }
         const uint8_t* row = wbase + s * K::STAGE + lane * C;
 #pragma unroll
-        for (int w = 0; w < K::VPL; ++w) h.vec(*reinterpret_cast<const uint4*>(row + ((w ^ sw) << 4)));
+        for (int w = 0; w < K::VPL; ++w) v[w] = lds128(row + ((w ^ sw) << 4));  // all 8 loads in flight
+#pragma unroll
+        for (int w = 0; w < K::VPL; ++w) h.vec(v[w]);
         if (k + S < nsteps) {
           __syncwarp();
           if (lane == 0) {
@@ -514,8 +527,11 @@ cudaError_t launch_slices(const SliceJob& job_in, SliceMode mode, bool commit, u
   SliceJob job = job_in;
   const int v = variant();
   if (v == 0 || v >= 3) attach_tensor_maps(job, mode == SliceMode::Copy || mode == SliceMode::CopyVerify);
-  static const bool no_fence = std::getenv("FFX_NO_FENCE") != nullptr;
-  job.proxy_fence = no_fence ? 0u : 1u;
+  // The refill of a stage is a generic-read -> async-write (WAR) sequence,
+  // ordered by the warp barrier; the proxy fence is only required for
+  // generic writes read by the async proxy (kept per task, optional per step).
+  static const bool fence = std::getenv("FFX_STEP_FENCE") != nullptr;
+  job.proxy_fence = fence ? 1u : 0u;
   switch (mode) {
     case SliceMode::Hash:
       return commit ? launch_mode<SliceMode::Hash, true>(job, max_ctas, stream)

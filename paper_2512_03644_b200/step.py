@@ -100,15 +100,16 @@ class SliceScheduler:
         self.copies = self.hashes = 0
 
     def begin(self, iteration: int):
-        L = self.step.layers
+        # one batch per all-gather gap, forward and backward (2L gaps)
+        G = 2 * self.step.layers
         if self.policy == "fused":
-            self.copies = self.ctx.snapshot_begin(iteration, batches=L, max_ctas=self.copy_ctas)
+            self.copies = self.ctx.snapshot_begin(iteration, batches=G, max_ctas=self.copy_ctas)
             self.hashes = 0
         else:
-            self.copies = self.ctx.snapshot_begin(iteration, batches=L, max_ctas=self.copy_ctas, split=True,
-                                                  hash_batches=L, hash_ctas=self.hash_ctas,
+            self.copies = self.ctx.snapshot_begin(iteration, batches=G, max_ctas=self.copy_ctas, split=True,
+                                                  hash_batches=G, hash_ctas=self.hash_ctas,
                                                   copy_engine=self.copy_engine)
-            self.hashes = L
+            self.hashes = G
 
     def _issue(self, kind, stream, gate=None):
         left = self.ctx.snapshot_next(stream=stream, gate_event=gate,
@@ -126,9 +127,9 @@ class SliceScheduler:
         return ev
 
     def hook(self, kind, layer):
-        if kind == "pre_ag" and self.hashes and layer < self.step.layers:
+        if kind == "pre_ag" and self.hashes:
             self._issue(self.ffx.BATCH_HASH, self.hash_stream, self._gap())
-        elif kind == "fwd" and self.copies:
+        elif kind in ("fwd", "bwd") and self.copies:
             self._issue(self.ffx.BATCH_COPY, self.low, self._gap())
         elif kind == "opt":
             while self.copies:  # more batches than gaps: flush now
