@@ -1,22 +1,25 @@
 // ffx_slice.cu -- the snapshot / recovery kernel: fused copy + per-slice
 // FNV-1a-64 (+ verify against a checksum table, + slot commit).
 //
-// Work unit: one warp task = 32 consecutive slices of one region, one lane
-// per slice (FNV-1a is byte-serial, hash.cpp:102-110, so parallelism comes
-// from independent slice chains).  Each step moves C bytes of every slice:
+// Work unit: one warp task = 32*RPL consecutive slices of one region; lane l
+// owns slices l, l+32, ... (FNV-1a is byte-serial, hash.cpp:102-110, so the
+// parallelism is independent slice chains).  Each step moves 128 bytes of
+// every slice of the task:
 //
-//   full, aligned task (the bulk of any payload) -- TMA bulk-copy pipeline:
-//     cp.async.bulk global->smem (one C-byte row per lane, S stages, mbarrier
-//     complete_tx) -> cp.async.bulk smem->global to the destination (local
-//     HBM or an NVLink peer's replica) -> each lane hashes its row from
-//     shared memory.  No payload byte passes through registers on the copy
-//     path; loads run S steps ahead of the hash.
+//   full, aligned task (the bulk of any payload) -- 2-D tensor TMA: the
+//     region is viewed as {slice_bytes, nslices} with row pitch slice_bytes;
+//     one cp.async.bulk.tensor load brings a 128 x (32*RPL) box (row j =
+//     slice j) into shared memory with 128-byte swizzle (S stages, mbarrier
+//     complete_tx), one tensor store writes it to the destination (local HBM
+//     or the NVLink peer's replica; twice for double-neighbour replication),
+//     and each lane hashes its rows from shared memory, reading chunk w of
+//     row j at (w ^ (j & 7)) so every LDS.128 phase is conflict-free.  No
+//     payload byte passes through registers on the copy path.
 //   ragged task (region tail, unaligned pointers) -- register path: 16-byte
-//     loads, stores and a padded shared-memory transpose.
+//     loads / stores and a padded shared-memory transpose.
 //
-// Rows are padded by 16 bytes so the eight lanes of each LDS.128 phase hit
-// distinct banks.  Tasks are handed out dynamically (one atomic per task) so
-// the last wave does not idle SMs.
+// Tasks are handed out dynamically (one atomic per task) so the last wave
+// does not idle SMs.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -176,27 +179,29 @@ __device__ __forceinline__ void commit_end(const SlotCommit& c) {
   *c.done = 0;
 }
 
-template <int C, int S, int W, bool kTensor>
+template <int S, int W, int RPL>
 struct Cfg {
-  static constexpr int VPL = C / 16;  // 16-byte vectors per row
-  // Row-copy stages pad each row by 16 bytes; tensor-TMA stages are dense
-  // 4 KB tiles whose 128-byte swizzle does the bank spreading instead.
-  static constexpr int ROWB = kTensor ? C : C + 16;
-  static constexpr int STAGE = 32 * ROWB;
-  static constexpr int WARPB = S * STAGE > 32 * (C + 16) ? S * STAGE : 32 * (C + 16);
-  static constexpr int ALIGN = kTensor ? 1024 : 128;
-  static constexpr int BARB = ((W * S * 8 + ALIGN - 1) / ALIGN) * ALIGN;
-  static constexpr int SMEM = BARB + W * WARPB + ALIGN;  // + slack to align the base
+  static constexpr int C = 128;                      // bytes of each slice per step (one TMA row)
+  static constexpr int VPL = C / 16;                 // 16-byte vectors per row
+  static constexpr int ROWS = 32 * RPL;              // slices per warp task (RPL per lane)
+  static constexpr int STAGE = ROWS * C;             // one 128 x ROWS TMA box, dense + swizzled
+  static constexpr int PADROW = C + 16;              // register-path row, padded for banks
+  static constexpr int WARPB = S * STAGE > 32 * PADROW ? S * STAGE : 32 * PADROW;
+  static constexpr int BARB = ((W * S * 8 + 1023) / 1024) * 1024;
+  static constexpr int SMEM = BARB + W * WARPB + 1024;  // + slack to 1 KB-align the base
 };
 
-template <int C, int S, int W, bool kTensor, SliceMode M, bool kCommit>
+// One warp task = ROWS consecutive slices of one region; lane l owns slices
+// l, l+32, ... (RPL independent FNV chains per lane -- the ILP that hides the
+// chains' multiply latency).
+template <int S, int W, int RPL, SliceMode M, bool kCommit>
 __global__ void __launch_bounds__(W * 32) slice_kernel(const __grid_constant__ SliceJob job) {
-  using K = Cfg<C, S, W, kTensor>;
-  static_assert(!kTensor || C == 128, "tensor tiles are 128-byte rows");
+  using K = Cfg<S, W, RPL>;
+  constexpr int C = K::C;
   constexpr bool kCopy = (M == SliceMode::Copy || M == SliceMode::CopyVerify);
   constexpr bool kVerify = (M == SliceMode::CopyVerify || M == SliceMode::HashVerify);
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = smem_raw + ((K::ALIGN - (smem_u32(smem_raw) & (K::ALIGN - 1))) & (K::ALIGN - 1));
+  uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   uint8_t* wbase = smem + K::BARB + warp * K::WARPB;
@@ -235,22 +240,25 @@ __global__ void __launch_bounds__(W * 32) slice_kernel(const __grid_constant__ S
     for (int i = 1; i < static_cast<int>(kMaxRegions); ++i)
       if (i < static_cast<int>(job.nregions) && g >= job.reg[i].group_base) R = job.reg[i];
     const bool al = aligned16(R.src) && (!kCopy || aligned16(R.dst));
-    const uint64_t s0 = (g - R.group_base) * 32;
-    const uint64_t base0 = s0 * Sl;
-    const uint64_t my_off = base0 + static_cast<uint64_t>(lane) * Sl;
-    const uint64_t my_len = my_off < R.bytes ? umin64(Sl, R.bytes - my_off) : 0;
+    const uint64_t s0 = (g - R.group_base) * K::ROWS;
 
-    Fnv h;
-    h.init();
-    if (job.init_state != nullptr && my_len) h.set(job.init_state[R.slice_base + s0 + lane]);
+    Fnv h[RPL];
+    uint64_t len[RPL];
+#pragma unroll
+    for (int r = 0; r < RPL; ++r) {
+      const uint64_t off = (s0 + lane + 32 * r) * Sl;
+      len[r] = off < R.bytes ? umin64(Sl, R.bytes - off) : 0;
+      h[r].init();
+      if (job.init_state != nullptr && len[r]) h[r].set(job.init_state[R.slice_base + s0 + lane + 32 * r]);
+    }
 
     // Stages are free once this lane's earlier bulk stores finished reading
     // them and every lane is past its previous hash.
     if constexpr (kCopy) bulk_wait_read_all();
     __syncwarp();
 
-    if (kTensor && R.tmap >= 0 && s0 + 32 <= R.nfull) {
-      // ---- 2-D tensor TMA: one 128 x 32 box per step (4 KB), swizzled ---------------
+    if (R.tmap >= 0 && s0 + K::ROWS <= R.nfull) {
+      // ---- 2-D tensor TMA: one 128 x ROWS box per step, 128 B swizzle ---------------
       const CUtensorMap* msrc = &job.maps[3 * R.tmap];
       const CUtensorMap* mdst = &job.maps[3 * R.tmap + 1];
       const CUtensorMap* mdst2 = &job.maps[3 * R.tmap + 2];
@@ -259,14 +267,13 @@ __global__ void __launch_bounds__(W * 32) slice_kernel(const __grid_constant__ S
       const int y = static_cast<int>(s0);
       const int pro = nsteps < S ? nsteps : S;
       if (lane == 0) {
-        fence_async_smem();
+        fence_async_smem();  // rows written by the register path -> async proxy
         for (int k = 0; k < pro; ++k) {
-          mbar_expect_tx(bar0 + 8 * k, 32 * C);
+          mbar_expect_tx(bar0 + 8 * k, K::STAGE);
           tensor_load(stage0 + k * K::STAGE, msrc, k * C, y, bar0 + 8 * k);
         }
       }
-      const int sw = lane & 7;
-      uint4 v[K::VPL];
+      const int sw = lane & 7;  // (lane + 32 r) & 7 == lane & 7
       for (int k = 0; k < nsteps; ++k) {
         const int s = k % S;
         mbar_wait(bar0 + 8 * s, (phase >> s) & 1u);
@@ -279,96 +286,75 @@ __global__ void __launch_bounds__(W * 32) slice_kernel(const __grid_constant__ S
             bulk_commit();
           }
         }
-        const uint8_t* row = wbase + s * K::STAGE + lane * C;
+        uint4 v[RPL][K::VPL];
 #pragma unroll
-        for (int w = 0; w < K::VPL; ++w) v[w] = lds128(row + ((w ^ sw) << 4));  // all 8 loads in flight
+        for (int r = 0; r < RPL; ++r) {
+          const uint8_t* row = wbase + s * K::STAGE + (lane + 32 * r) * C;
 #pragma unroll
-        for (int w = 0; w < K::VPL; ++w) h.vec(v[w]);
+          for (int w = 0; w < K::VPL; ++w) v[r][w] = lds128(row + ((w ^ sw) << 4));
+        }
+#pragma unroll
+        for (int w = 0; w < K::VPL; ++w)
+#pragma unroll
+          for (int r = 0; r < RPL; ++r) h[r].vec(v[r][w]);  // RPL chains interleaved
         if (k + S < nsteps) {
           __syncwarp();
           if (lane == 0) {
             if constexpr (kCopy) bulk_wait_read_all();
             if (job.proxy_fence) fence_async_smem();
-            mbar_expect_tx(bar0 + 8 * s, 32 * C);
+            mbar_expect_tx(bar0 + 8 * s, K::STAGE);
             tensor_load(tile, msrc, (k + S) * C, y, bar0 + 8 * s);
           }
         }
       }
-    } else if (!kTensor && al && base0 + 32 * Sl <= R.bytes) {
-      // ---- TMA pipeline: 32 full slices --------------------------------------------
-      const int nsteps = static_cast<int>(Sl / C);
-      const uint8_t* src = R.src + my_off;
-      uint8_t* dst = kCopy ? R.dst + my_off : nullptr;
-      fence_async_smem();
-      const int pro = nsteps < S ? nsteps : S;
-      for (int k = 0; k < pro; ++k) {
-        if (lane == 0) mbar_expect_tx(bar0 + 8 * k, 32 * C);
-        __syncwarp();
-        bulk_load(stage0 + k * K::STAGE + lane * K::ROWB, src + static_cast<uint64_t>(k) * C, C,
-                  bar0 + 8 * k);
-      }
-      for (int k = 0; k < nsteps; ++k) {
-        const int s = k % S;
-        mbar_wait(bar0 + 8 * s, (phase >> s) & 1u);
-        phase ^= 1u << s;
-        const uint32_t row = stage0 + s * K::STAGE + lane * K::ROWB;
-        if constexpr (kCopy) {
-          bulk_store(dst + static_cast<uint64_t>(k) * C, row, C);
-          if (R.dst2 != nullptr) bulk_store(R.dst2 + my_off + static_cast<uint64_t>(k) * C, row, C);
-          bulk_commit();
-        }
-        const uint4* rp = reinterpret_cast<const uint4*>(wbase + s * K::STAGE + lane * K::ROWB);
-#pragma unroll
-        for (int w = 0; w < K::VPL; ++w) h.vec(rp[w]);
-        if (k + S < nsteps) {
-          if constexpr (kCopy) bulk_wait_read_all();
-          __syncwarp();
-          fence_async_smem();
-          if (lane == 0) mbar_expect_tx(bar0 + 8 * s, 32 * C);
-          __syncwarp();
-          bulk_load(row, src + static_cast<uint64_t>(k + S) * C, C, bar0 + 8 * s);
-        }
-      }
     } else {
-      // ---- register path: ragged tail or unaligned pointers ------------------------
-      const uint64_t max_len = umin64(Sl, R.bytes - base0);
-      const int nsteps = static_cast<int>((max_len + C - 1) / C);
+      // ---- register path: ragged tail or unaligned pointers, 32 slices at a time ----
       uint4* rows = reinterpret_cast<uint4*>(wbase);
-      for (int k = 0; k < nsteps; ++k) {
-        uint4 buf[K::VPL];
 #pragma unroll
-        for (int i = 0; i < K::VPL; ++i) {
-          const int q = i * 32 + lane;
-          const uint64_t o = base0 + static_cast<uint64_t>(q / K::VPL) * Sl + static_cast<uint64_t>(k) * C +
-                             static_cast<uint64_t>(q % K::VPL) * 16;
-          buf[i] = load16(R.src, o, R.bytes, al);
-          if constexpr (kCopy) {
-            store16(R.dst, o, R.bytes, al, buf[i]);
-            if (R.dst2 != nullptr) store16(R.dst2, o, R.bytes, al && aligned16(R.dst2), buf[i]);
+      for (int r = 0; r < RPL; ++r) {
+        const uint64_t sub0 = s0 + 32 * r;
+        if (sub0 * Sl >= R.bytes) break;
+        const uint64_t base0 = sub0 * Sl;
+        const uint64_t max_len = umin64(Sl, R.bytes - base0);
+        const int nsteps = static_cast<int>((max_len + C - 1) / C);
+        for (int k = 0; k < nsteps; ++k) {
+          uint4 buf[K::VPL];
+#pragma unroll
+          for (int i = 0; i < K::VPL; ++i) {
+            const int q = i * 32 + lane;
+            const uint64_t o = base0 + static_cast<uint64_t>(q / K::VPL) * Sl + static_cast<uint64_t>(k) * C +
+                               static_cast<uint64_t>(q % K::VPL) * 16;
+            buf[i] = load16(R.src, o, R.bytes, al);
+            if constexpr (kCopy) {
+              store16(R.dst, o, R.bytes, al, buf[i]);
+              if (R.dst2 != nullptr) store16(R.dst2, o, R.bytes, al && aligned16(R.dst2), buf[i]);
+            }
           }
-        }
-        __syncwarp();
+          __syncwarp();
 #pragma unroll
-        for (int i = 0; i < K::VPL; ++i) {
-          const int q = i * 32 + lane;
-          rows[(q / K::VPL) * (K::VPL + 1) + (q % K::VPL)] = buf[i];
-        }
-        __syncwarp();
-        const int64_t rem = static_cast<int64_t>(my_len) - static_cast<int64_t>(k) * C;
-        const uint4* rp = rows + lane * (K::VPL + 1);
-        if (rem >= C) {
+          for (int i = 0; i < K::VPL; ++i) {
+            const int q = i * 32 + lane;
+            rows[(q / K::VPL) * (K::VPL + 1) + (q % K::VPL)] = buf[i];
+          }
+          __syncwarp();
+          const int64_t rem = static_cast<int64_t>(len[r]) - static_cast<int64_t>(k) * C;
+          const uint4* rp = rows + lane * (K::VPL + 1);
+          if (rem >= C) {
 #pragma unroll
-          for (int w = 0; w < K::VPL; ++w) h.vec(rp[w]);
-        } else if (rem > 0) {
-          const uint8_t* rb = reinterpret_cast<const uint8_t*>(rp);
-          for (int b = 0; b < rem; ++b) h.byte(rb[b]);
+            for (int w = 0; w < K::VPL; ++w) h[r].vec(rp[w]);
+          } else if (rem > 0) {
+            const uint8_t* rb = reinterpret_cast<const uint8_t*>(rp);
+            for (int b = 0; b < rem; ++b) h[r].byte(rb[b]);
+          }
         }
       }
     }
 
-    if (my_len) {
-      const uint64_t idx = R.slice_base + s0 + lane;
-      const uint64_t v = h.value();
+#pragma unroll
+    for (int r = 0; r < RPL; ++r) {
+      if (!len[r]) continue;
+      const uint64_t idx = R.slice_base + s0 + lane + 32 * r;
+      const uint64_t v = h[r].value();
       if (job.sums_out != nullptr) job.sums_out[idx] = v;
       if (job.sums_out2 != nullptr) job.sums_out2[idx] = v;
       if constexpr (kVerify) {
@@ -402,10 +388,10 @@ __global__ void __launch_bounds__(W * 32) slice_kernel(const __grid_constant__ S
 
 int g_sms = 0;
 
-template <int C, int S, int W, bool kTensor, SliceMode M, bool kCommit>
+template <int S, int W, int RPL, SliceMode M, bool kCommit>
 cudaError_t launch_t(const SliceJob& job, uint32_t max_ctas, cudaStream_t stream) {
-  auto kern = slice_kernel<C, S, W, kTensor, M, kCommit>;
-  constexpr int smem = Cfg<C, S, W, kTensor>::SMEM;
+  auto kern = slice_kernel<S, W, RPL, M, kCommit>;
+  constexpr int smem = Cfg<S, W, RPL>::SMEM;
   static int occ = 0;
   if (occ == 0) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -431,17 +417,22 @@ int variant() {
   return v;
 }
 
+// Kernel variants for tuning (FFX_SLICE_VARIANT): stages / warps per CTA /
+// slices per lane.  The warp-task size (32 * RPL slices) follows the variant.
+struct Variant {
+  int S, W, RPL;
+};
+constexpr Variant kVariants[] = {{4, 4, 1}, {2, 4, 2}, {3, 4, 2}, {6, 4, 1}, {3, 4, 1}, {2, 8, 2}};
+
 template <SliceMode M, bool kCommit>
 cudaError_t launch_mode(const SliceJob& job, uint32_t max_ctas, cudaStream_t stream) {
   switch (variant()) {
-    case 1: return launch_t<128, 3, 4, false, M, kCommit>(job, max_ctas, stream);
-    case 2: return launch_t<128, 4, 4, false, M, kCommit>(job, max_ctas, stream);
-    case 3: return launch_t<128, 6, 4, true, M, kCommit>(job, max_ctas, stream);
-    case 4: return launch_t<128, 8, 4, true, M, kCommit>(job, max_ctas, stream);
-    case 5: return launch_t<128, 3, 4, true, M, kCommit>(job, max_ctas, stream);
-    case 6: return launch_t<128, 2, 4, true, M, kCommit>(job, max_ctas, stream);
-    case 7: return launch_t<128, 2, 8, true, M, kCommit>(job, max_ctas, stream);
-    default: return launch_t<128, 4, 4, true, M, kCommit>(job, max_ctas, stream);
+    case 1: return launch_t<2, 4, 2, M, kCommit>(job, max_ctas, stream);
+    case 2: return launch_t<3, 4, 2, M, kCommit>(job, max_ctas, stream);
+    case 3: return launch_t<6, 4, 1, M, kCommit>(job, max_ctas, stream);
+    case 4: return launch_t<3, 4, 1, M, kCommit>(job, max_ctas, stream);
+    case 5: return launch_t<2, 8, 2, M, kCommit>(job, max_ctas, stream);
+    default: return launch_t<4, 4, 1, M, kCommit>(job, max_ctas, stream);
   }
 }
 
@@ -457,14 +448,20 @@ int sm_count() {
   return g_sms;
 }
 
+int task_rows() {
+  const int v = variant();
+  return 32 * kVariants[(v >= 0 && v < static_cast<int>(sizeof kVariants / sizeof kVariants[0])) ? v : 0].RPL;
+}
+
 void finalize_job(SliceJob& job) {
+  const uint64_t rows = static_cast<uint64_t>(task_rows());
   uint64_t groups = 0, slices = 0;
   for (uint32_t r = 0; r < job.nregions; ++r) {
     const uint64_t ns = (job.reg[r].bytes + job.slice_bytes - 1) / job.slice_bytes;
     job.reg[r].slice_base = slices;
     job.reg[r].group_base = groups;
     slices += ns;
-    groups += (ns + 31) / 32;
+    groups += (ns + rows - 1) / rows;
   }
   for (uint32_t r = job.nregions; r < kMaxRegions; ++r)
     job.reg[r] = SliceRegion{nullptr, nullptr, 0, slices, ~0ull, -1, 0, 0, nullptr};
@@ -488,12 +485,12 @@ PFN_cuTensorMapEncodeTiled_v12000 encoder() {
   return fn;
 }
 
-bool encode_rows(CUtensorMap* map, const void* base, uint64_t slice_bytes, uint64_t nfull) {
+bool encode_rows(CUtensorMap* map, const void* base, uint64_t slice_bytes, uint64_t nfull, uint32_t rows) {
   auto enc = encoder();
   if (!enc) return false;
   const cuuint64_t dims[2] = {slice_bytes, nfull};
   const cuuint64_t strides[1] = {slice_bytes};
-  const cuuint32_t box[2] = {128, 32};
+  const cuuint32_t box[2] = {128, rows};
   const cuuint32_t estr[2] = {1, 1};
   return enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), dims, strides, box, estr,
              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -512,11 +509,13 @@ void attach_tensor_maps(SliceJob& job, bool copy) {
     R.nfull = R.bytes / job.slice_bytes;
     const bool al = (reinterpret_cast<uintptr_t>(R.src) % 16 == 0) &&
                     (!copy || reinterpret_cast<uintptr_t>(R.dst) % 16 == 0);
-    if (!al || R.nfull < 32 || R.nfull > (1ull << 31)) continue;
+    const uint32_t rows = static_cast<uint32_t>(task_rows());
+    if (!al || R.nfull < rows || R.nfull > (1ull << 31)) continue;
     if (R.dst2 != nullptr && reinterpret_cast<uintptr_t>(R.dst2) % 16 != 0) continue;
-    if (!encode_rows(&job.maps[3 * used], R.src, job.slice_bytes, R.nfull)) continue;
-    if (copy && !encode_rows(&job.maps[3 * used + 1], R.dst, job.slice_bytes, R.nfull)) continue;
-    if (copy && R.dst2 != nullptr && !encode_rows(&job.maps[3 * used + 2], R.dst2, job.slice_bytes, R.nfull))
+    if (!encode_rows(&job.maps[3 * used], R.src, job.slice_bytes, R.nfull, rows)) continue;
+    if (copy && !encode_rows(&job.maps[3 * used + 1], R.dst, job.slice_bytes, R.nfull, rows)) continue;
+    if (copy && R.dst2 != nullptr &&
+        !encode_rows(&job.maps[3 * used + 2], R.dst2, job.slice_bytes, R.nfull, rows))
       continue;
     R.tmap = used++;
   }
@@ -525,8 +524,7 @@ void attach_tensor_maps(SliceJob& job, bool copy) {
 cudaError_t launch_slices(const SliceJob& job_in, SliceMode mode, bool commit, uint32_t max_ctas,
                           cudaStream_t stream) {
   SliceJob job = job_in;
-  const int v = variant();
-  if (v == 0 || v >= 3) attach_tensor_maps(job, mode == SliceMode::Copy || mode == SliceMode::CopyVerify);
+  attach_tensor_maps(job, mode == SliceMode::Copy || mode == SliceMode::CopyVerify);
   // The refill of a stage is a generic-read -> async-write (WAR) sequence,
   // ordered by the warp barrier; the proxy fence is only required for
   // generic writes read by the async proxy (kept per task, optional per step).
