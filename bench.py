@@ -63,6 +63,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-llama", action="store_true", help="skip the Llama-3 8B recovery/overhead legs")
     ap.add_argument("--sched-ctas", type=int, default=32, help="SM budget of scheduled snapshot batches")
+    ap.add_argument("--no-70b", action="store_true", help="skip the 70B double-neighbour leg (N >= 3)")
+    ap.add_argument("--prefix-70b", type=int, default=16 << 30, help="70B state prefix per rank (bytes)")
     ap.add_argument("--mode", default="push", choices=["push", "pull"],
                     help="N>1 ring stream: origin pushes into its successor's replica, or the holder "
                          "pulls its predecessor's regions (NeighborBuffer::store side)")
@@ -418,6 +420,12 @@ def main():
     llama = None
     if world > 1 and not args.no_llama:
         llama = llama_leg(args, ffx, torch, dist, world, rank, local, barrier)
+    seventy = None
+    if world >= 3 and not args.no_70b:
+        try:
+            seventy = seventy_leg(args, ffx, torch, dist, world, rank, local, barrier)
+        except Exception as ex:
+            seventy = {"error": repr(ex)}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -442,6 +450,7 @@ def main():
             "per_gpu_gbs": round(value / world, 3),
             "nvlink_frac_per_gpu": round(value / world / NVLINK_MEASURED_GBS, 4) if world > 1 else None,
             "roofline": roof, "recovery": rec, "alt_ring_stream": alt, "llama3_8b": llama,
+            "llama3_70b_double_neighbour": seventy,
             "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": int(launches), "clocks": ck, "commit_ok": bool(commit_ok),
         }), flush=True)
@@ -449,6 +458,87 @@ def main():
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+PHI_LLAMA3_70B = 70_553_706_496
+
+
+def seventy_leg(args, ffx, torch, dist, world, rank, local, barrier):
+    """configs[4]: Llama-3 70B ZeRO-3 over 8 ranks with double-neighbour
+    replication.  The full layout does not fit in HBM (sizing below), so the
+    dual-store snapshot (replicas at dp+1 and dp+2) and an
+    adjacent-pair recovery are measured on a capacity-scaled prefix."""
+    import pyoracle
+    from paper_2512_03644_b200 import ring
+    free, total = torch.cuda.mem_get_info()
+    own = (12 * PHI_LLAMA3_70B + 7) // 8 + (2 * PHI_LLAMA3_70B + 7) // 8
+    sizing = {"own_state_bytes": own, "hbm_bytes": total,
+              "double_neighbour_2_versions_bytes": own + 4 * own,
+              "double_neighbour_1_version_bytes": own + 2 * own,
+              "single_neighbour_1_version_bytes": own + own,
+              "fits": {"double_2v": own * 5 <= total, "double_1v": own * 3 <= total,
+                       "single_1v": own * 2 <= total}}
+    prefix = args.prefix_70b
+    spec = ffx.make_spec(d=world, phi=PHI_LLAMA3_70B, distributed=True)
+    ctx = ffx.Context(local, spec, ffx.Role(rank, 0, 0), args.slice_bytes)
+
+    def all_gather(b):
+        out = [None] * world
+        dist.all_gather_object(out, b)
+        return out
+
+    held, targets, handles = ring.wire_ring(
+        rank, world, lambda origin: ctx.create_replica(ffx.Role(origin, 0, 0), prefix, 2),
+        lambda r: r.export(), ctx.open_replica, all_gather, replicas=2)
+    ctx.set_target(targets[0])
+    ctx.set_target2(targets[1])
+    state = torch.empty(prefix, dtype=torch.uint8, device="cuda")
+    ffx.materialize(state, pyoracle.optimizer_init(70, rank, 0, 0, True))
+    ctx.register(ffx.REGION_BLOB, state)
+    s = torch.cuda.Stream()
+    for it in (1, 2):
+        ctx.snapshot(it, stream=s)
+    s.synchronize()
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    k = 3
+    e0.record(s)
+    for it in range(3, 3 + k):
+        ctx.snapshot(it, stream=s)
+    e1.record(s)
+    s.synchronize()
+    t = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    egress = 2 * prefix * k / (float(t.item()) * 1e-3) / 1e9
+    last = 2 + k
+    # adjacent pair (ranks 1 and 2) lost: the reference falls back
+    # (controller.cpp:162-167); with replicas at dp+1 and dp+2 both recover.
+    plan = ffx.plan_recovery(spec, [], [ffx.Role(1, 0, 0), ffx.Role(2, 0, 0)], last, 0, replicas=2)
+    sources = {o: (h, kk) for o, h, kk in ring.recovery_sources(plan.forwards, world)}
+    rec = None
+    barrier()
+    if rank in sources:
+        h, kk = sources[rank]
+        view = ctx.open_replica(handles[h][kk])
+        ctx.inject(ffx.FAULT_POISON_STATE)
+        rpt = ctx.recover(view, last, stream=s)
+        rec = {"holder": h, "recovery_s": round(rpt.seconds, 5),
+               "recovery_gbs": round(prefix / rpt.seconds / 1e9, 1),
+               "bit_exact": bool(rpt.bad_slices == 0 and ffx.blob_is_sound(state))}
+        view.destroy()
+    recs = all_gather(rec)
+    barrier()
+    for r in targets + held:
+        r.destroy()
+    ctx.close()
+    del state
+    torch.cuda.empty_cache()
+    return {"sizing": sizing, "prefix_bytes_per_rank": prefix,
+            "dual_store_egress_gbs_per_gpu": round(egress, 1),
+            "plan_reference_rule": ffx.plan_recovery(spec, [], [ffx.Role(1, 0, 0), ffx.Role(2, 0, 0)],
+                                                     last, 0, replicas=1).kind,
+            "plan_double_neighbour": plan.kind,
+            "adjacent_pair_recovery": [x for x in recs if x]}
 
 
 def llama_leg(args, ffx, torch, dist, world, rank, local, barrier):
