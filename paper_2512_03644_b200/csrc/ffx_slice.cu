@@ -194,7 +194,7 @@ struct Cfg {
 // One warp task = ROWS consecutive slices of one region; lane l owns slices
 // l, l+32, ... (RPL independent FNV chains per lane -- the ILP that hides the
 // chains' multiply latency).
-template <int S, int W, int RPL, SliceMode M, bool kCommit>
+template <int S, int W, int RPL, bool kStg, SliceMode M, bool kCommit>
 __global__ void __launch_bounds__(W * 32) slice_kernel(const __grid_constant__ SliceJob job) {
   using K = Cfg<S, W, RPL>;
   constexpr int C = K::C;
@@ -279,11 +279,25 @@ __global__ void __launch_bounds__(W * 32) slice_kernel(const __grid_constant__ S
         mbar_wait(bar0 + 8 * s, (phase >> s) & 1u);
         phase ^= 1u << s;
         const uint32_t tile = stage0 + s * K::STAGE;
-        if constexpr (kCopy) {
+        if constexpr (kCopy && !kStg) {
           if (lane == 0) {
             tensor_store(mdst, k * C, y, tile);
             if (dual) tensor_store(mdst2, k * C, y, tile);  // double neighbour: read once, write twice
             bulk_commit();
+          }
+        }
+        if constexpr (kCopy && kStg) {
+          // SM stores instead of a TMA store: 8 lanes x 16 B cover one 128 B
+          // row segment, so each STG.128 writes 4 full lines.
+          const uint8_t* tp = wbase + s * K::STAGE;
+#pragma unroll
+          for (int i = 0; i < K::ROWS / 4; ++i) {
+            const int j = i * 4 + (lane >> 3);
+            const int w = lane & 7;
+            const uint4 val = lds128(tp + j * C + ((w ^ (j & 7)) << 4));
+            const uint64_t o = (s0 + j) * Sl + static_cast<uint64_t>(k) * C + w * 16;
+            st_stream(R.dst + o, val);
+            if (dual) st_stream(R.dst2 + o, val);
           }
         }
         uint4 v[RPL][K::VPL];
@@ -388,9 +402,9 @@ __global__ void __launch_bounds__(W * 32) slice_kernel(const __grid_constant__ S
 
 int g_sms = 0;
 
-template <int S, int W, int RPL, SliceMode M, bool kCommit>
+template <int S, int W, int RPL, bool kStg, SliceMode M, bool kCommit>
 cudaError_t launch_t(const SliceJob& job, uint32_t max_ctas, cudaStream_t stream) {
-  auto kern = slice_kernel<S, W, RPL, M, kCommit>;
+  auto kern = slice_kernel<S, W, RPL, kStg, M, kCommit>;
   constexpr int smem = Cfg<S, W, RPL>::SMEM;
   static int occ = 0;
   if (occ == 0) {
@@ -420,19 +434,23 @@ int variant() {
 // Kernel variants for tuning (FFX_SLICE_VARIANT): stages / warps per CTA /
 // slices per lane.  The warp-task size (32 * RPL slices) follows the variant.
 struct Variant {
-  int S, W, RPL;
+  int S, W, RPL, stg;
 };
-constexpr Variant kVariants[] = {{4, 4, 1}, {2, 4, 2}, {3, 4, 2}, {6, 4, 1}, {3, 4, 1}, {2, 8, 2}};
+constexpr Variant kVariants[] = {{4, 4, 1, 0}, {2, 4, 2, 0}, {3, 4, 2, 0}, {6, 4, 1, 0}, {3, 4, 1, 0},
+                                 {2, 8, 2, 0}, {4, 4, 1, 1}, {3, 4, 2, 1}, {6, 4, 1, 1}};
 
 template <SliceMode M, bool kCommit>
 cudaError_t launch_mode(const SliceJob& job, uint32_t max_ctas, cudaStream_t stream) {
   switch (variant()) {
-    case 1: return launch_t<2, 4, 2, M, kCommit>(job, max_ctas, stream);
-    case 2: return launch_t<3, 4, 2, M, kCommit>(job, max_ctas, stream);
-    case 3: return launch_t<6, 4, 1, M, kCommit>(job, max_ctas, stream);
-    case 4: return launch_t<3, 4, 1, M, kCommit>(job, max_ctas, stream);
-    case 5: return launch_t<2, 8, 2, M, kCommit>(job, max_ctas, stream);
-    default: return launch_t<4, 4, 1, M, kCommit>(job, max_ctas, stream);
+    case 1: return launch_t<2, 4, 2, false, M, kCommit>(job, max_ctas, stream);
+    case 2: return launch_t<3, 4, 2, false, M, kCommit>(job, max_ctas, stream);
+    case 3: return launch_t<6, 4, 1, false, M, kCommit>(job, max_ctas, stream);
+    case 4: return launch_t<3, 4, 1, false, M, kCommit>(job, max_ctas, stream);
+    case 5: return launch_t<2, 8, 2, false, M, kCommit>(job, max_ctas, stream);
+    case 6: return launch_t<4, 4, 1, true, M, kCommit>(job, max_ctas, stream);
+    case 7: return launch_t<3, 4, 2, true, M, kCommit>(job, max_ctas, stream);
+    case 8: return launch_t<6, 4, 1, true, M, kCommit>(job, max_ctas, stream);
+    default: return launch_t<4, 4, 1, false, M, kCommit>(job, max_ctas, stream);
   }
 }
 
