@@ -287,6 +287,12 @@ typedef struct ffx_snapshot_opts {
   uint32_t hash_batches;   /* split: hash batches (0 = batches) */
   uint32_t hash_ctas;      /* split: SM budget of hash batches (0 = whole GPU) */
   uint32_t copy_engine;    /* split: copy batches by cudaMemcpyAsync (no SMs) */
+  uint32_t pad_;
+  /* Measured gaps: relative sizes of the copy batches (`batches` entries,
+   * e.g. the durations of the step's idle-link windows measured with events
+   * in a calibration step).  NULL = equal batches.  Hash batches of the
+   * split policy stay equal. */
+  const double* batch_weights;
 } ffx_snapshot_opts;
 
 enum ffx_batch_kind { FFX_BATCH_COPY = 0, FFX_BATCH_HASH = 1 };
@@ -358,6 +364,15 @@ typedef struct ffx_recover_report {
  * Blocks until verified. */
 int ffx_recover(ffx_ctx* ctx, ffx_replica* src, uint64_t target, void* stream,
                 ffx_recover_report* report);
+
+/* Parallel peer gathers: the same snapshot held by several replicas (e.g. the
+ * dp+1 and dp+2 holders of double-neighbour replication); each region's
+ * slices are split into nsrc parts pulled concurrently from the nsrc sources
+ * by one kernel, all verified against the first source's checksum table.
+ * Every source must hold a committed, matching slot (same checks as
+ * ffx_recover).  nsrc in 1..4. */
+int ffx_recover_from(ffx_ctx* ctx, ffx_replica* const* srcs, uint32_t nsrc, uint64_t target, void* stream,
+                     ffx_recover_report* report);
 
 /* Pull one redundant region (weights from a live DP peer, ckpt.cpp:150-152)
  * from a peer device pointer, verifying against the peer's slice table

@@ -133,6 +133,10 @@ struct PendingSnapshot {
   ffx_replica* tgt = nullptr;   // destination replica(s) of this snapshot
   ffx_replica* tgt2 = nullptr;
   uint32_t hbatches = 0, hnext = 0, hash_ctas = 0;
+  std::vector<double> frac;  // cumulative batch boundaries in [0, 1] (measured-gap weights)
+  uint64_t cut(uint64_t total, uint32_t b) const {
+    return b >= batches ? total : static_cast<uint64_t>(static_cast<double>(total) * frac[b]);
+  }
 };
 
 struct ffx_ctx {
@@ -1135,6 +1139,17 @@ int begin_impl(ffx_ctx* c, ffx_replica* t, ffx_replica* t2, const std::vector<Sr
 
   P.active = true;
   P.batches = std::max<uint32_t>(1, opts.batches);
+  P.frac.assign(P.batches + 1, 0.0);
+  {
+    double sum = 0;
+    for (uint32_t b = 0; b < P.batches; ++b) {
+      const double w = opts.batch_weights ? opts.batch_weights[b] : 1.0;
+      sum += (w > 0 ? w : 0);
+      P.frac[b + 1] = sum;
+    }
+    for (uint32_t b = 0; b <= P.batches; ++b) P.frac[b] = sum > 0 ? P.frac[b] / sum : double(b) / P.batches;
+    P.frac[P.batches] = 1.0;
+  }
   P.max_ctas = opts.max_ctas;
   P.slot = slot;
   P.iteration = iteration;
@@ -1409,8 +1424,8 @@ namespace {
 int issue_copy_batch(ffx_ctx* c, PendingSnapshot& P, uint32_t b, cudaStream_t s) {
   CopyJob bj = P.copy;
   const uint64_t n = P.copy.total_chunks;
-  bj.chunk_lo = n * b / P.batches;
-  bj.chunk_hi = n * (b + 1) / P.batches;
+  bj.chunk_lo = P.cut(n, b);
+  bj.chunk_hi = P.cut(n, b + 1);
   if (bj.chunk_lo == bj.chunk_hi) return FFX_OK;
   if (!P.copy_engine) {
     FFX_CUDA(launch_copy(bj, P.max_ctas, s));
@@ -1484,8 +1499,8 @@ extern "C" int ffx_snapshot_next_kind(ffx_ctx* c, int kind, void* stream, void* 
     // Fused: batch b covers warp tasks [G*b/B, G*(b+1)/B); the last commits.
     const uint64_t G = P.job.total_groups;
     SliceJob bj = P.job;
-    bj.group_lo = G * b / P.batches;
-    bj.group_hi = G * (b + 1) / P.batches;
+    bj.group_lo = P.cut(G, b);
+    bj.group_hi = P.cut(G, b + 1);
     bj.commit.finalize = (b + 1 == P.batches);
     bj.commit2.finalize = bj.commit.finalize;
     if (bj.group_lo != bj.group_hi || bj.commit.finalize) {
@@ -1558,45 +1573,77 @@ extern "C" int ffx_snapshot_read_sums(ffx_ctx* c, uint64_t* host_dst, uint64_t m
 // ---------------------------------------------------------------------------
 // recovery
 
-extern "C" int ffx_recover(ffx_ctx* c, ffx_replica* src, uint64_t target, void* stream,
-                           ffx_recover_report* rep) {
-  if (!c || !src) return fail(FFX_EINVAL, "recover: null argument");
+namespace {
+
+// ckpt.cpp:111-136 (checked): missing, invalid, wrong kind, stale, wrong role,
+// plus the B200 layout checks (region count / sizes match the registry).
+int check_source(ffx_ctx* c, ffx_replica* src, uint64_t target, SlotMeta* m, uint32_t* slot) {
+  const int v = find_slot(src, target, m);
+  if (v == -2) return fail(FFX_ECUDA, "recover: cannot read replica metadata: %s", g_err.c_str());
+  if (v < 0) return fail(FFX_ERESTORE, "unique-state source missing: no snapshot at iteration %llu",
+                         (unsigned long long)target);
+  *slot = static_cast<uint32_t>(v);
+  if (m->state != kSlotCommitted)
+    return fail(FFX_ERESTORE, "unique-state source invalid: slot %d torn (write never committed)", v);
+  if (m->kind != 1) return fail(FFX_ERESTORE, "unique-state source has the wrong kind");
+  if (m->iteration != target)
+    return fail(FFX_ERESTORE, "unique-state source is at iteration %llu, want %llu",
+                (unsigned long long)m->iteration, (unsigned long long)target);
+  if (m->dp != c->self.dp || m->pp != c->self.pp || m->tp != c->self.tp)
+    return fail(FFX_ERESTORE, "unique-state source is for d%up%ut%u, want d%up%ut%u", m->dp, m->pp,
+                m->tp, c->self.dp, c->self.pp, c->self.tp);
+  const PayloadMap pm = payload_map(c);
+  if (m->num_regions != pm.regs.size())
+    return fail(FFX_ERESTORE, "snapshot has %u regions, %zu registered", m->num_regions, pm.regs.size());
+  for (size_t i = 0; i < pm.regs.size(); ++i)
+    if (m->region_bytes[i] != pm.regs[i]->bytes)
+      return fail(FFX_ERESTORE, "region %zu: snapshot %llu bytes, registered %llu", i,
+                  (unsigned long long)m->region_bytes[i], (unsigned long long)pm.regs[i]->bytes);
+  return FFX_OK;
+}
+
+}  // namespace
+
+extern "C" int ffx_recover_from(ffx_ctx* c, ffx_replica* const* srcs, uint32_t nsrc, uint64_t target,
+                                void* stream, ffx_recover_report* rep) {
+  if (!c || !srcs || nsrc == 0 || nsrc > 4) return fail(FFX_EINVAL, "recover: 1..4 sources");
   DeviceGuard g(c->device);
   ffx_recover_report local{};
   ffx_recover_report& R = rep ? *rep : local;
   std::memset(&R, 0, sizeof R);
   R.first_bad_slice = ~0ull;
-  SlotMeta m;
-  const int v = find_slot(src, target, &m);
-  if (v == -2) return fail(FFX_ECUDA, "recover: cannot read replica metadata: %s", g_err.c_str());
-  // ckpt.cpp:111-136 (checked): missing, invalid, wrong kind, stale, wrong role.
-  if (v < 0) return fail(FFX_ERESTORE, "unique-state source missing: no snapshot at iteration %llu",
-                         (unsigned long long)target);
-  R.slot = static_cast<uint32_t>(v);
-  if (m.state != kSlotCommitted)
-    return fail(FFX_ERESTORE, "unique-state source invalid: slot %d torn (write never committed)", v);
-  if (m.kind != 1) return fail(FFX_ERESTORE, "unique-state source has the wrong kind");
-  if (m.iteration != target)
-    return fail(FFX_ERESTORE, "unique-state source is at iteration %llu, want %llu",
-                (unsigned long long)m.iteration, (unsigned long long)target);
-  if (m.dp != c->self.dp || m.pp != c->self.pp || m.tp != c->self.tp)
-    return fail(FFX_ERESTORE, "unique-state source is for d%up%ut%u, want d%up%ut%u", m.dp, m.pp,
-                m.tp, c->self.dp, c->self.pp, c->self.tp);
+  SlotMeta m[4];
+  uint32_t slot[4];
+  for (uint32_t i = 0; i < nsrc; ++i) {
+    if (!srcs[i]) return fail(FFX_EINVAL, "recover: null source %u", i);
+    int st = check_source(c, srcs[i], target, &m[i], &slot[i]);
+    if (st) return st;
+    if (m[i].slice_bytes != m[0].slice_bytes)
+      return fail(FFX_ERESTORE, "sources disagree on the slice size");
+  }
+  R.slot = slot[0];
   const PayloadMap pm = payload_map(c);
-  if (m.num_regions != pm.regs.size())
-    return fail(FFX_ERESTORE, "snapshot has %u regions, %zu registered", m.num_regions, pm.regs.size());
-  for (size_t i = 0; i < pm.regs.size(); ++i)
-    if (m.region_bytes[i] != pm.regs[i]->bytes)
-      return fail(FFX_ERESTORE, "region %zu: snapshot %llu bytes, registered %llu", i,
-                  (unsigned long long)m.region_bytes[i], (unsigned long long)pm.regs[i]->bytes);
+  if (pm.regs.size() * nsrc > kMaxRegions) nsrc = 1;  // not enough region entries to split
+  const uint64_t S = m[0].slice_bytes;
 
+  // Parallel peer gathers: region r's slices are cut into nsrc consecutive
+  // parts, part i pulled from source i.  Sub-regions keep registration
+  // order, so the global slice numbering (and the checksum table) is that
+  // of the whole snapshot; every part verifies against source 0's table.
   cudaStream_t s = as_stream(stream);
   SliceJob job{};
-  job.nregions = static_cast<uint32_t>(pm.regs.size());
-  for (size_t i = 0; i < pm.regs.size(); ++i)
-    job.reg[i] = SliceRegion{src->payload(R.slot) + pm.offs[i], pm.regs[i]->dev, pm.regs[i]->bytes, 0, 0};
-  job.slice_bytes = m.slice_bytes;
-  job.sums_expected = src->sums(R.slot);
+  for (size_t r = 0; r < pm.regs.size(); ++r) {
+    const uint64_t ns = slices_of(pm.regs[r]->bytes, S);
+    for (uint32_t i = 0; i < nsrc; ++i) {
+      const uint64_t a = ns * i / nsrc, b = ns * (i + 1) / nsrc;
+      const uint64_t lo = a * S, hi = std::min(b * S, pm.regs[r]->bytes);
+      if (hi <= lo && !(nsrc == 1)) continue;
+      job.reg[job.nregions++] =
+          SliceRegion{srcs[i]->payload(slot[i]) + pm.offs[r] + lo, pm.regs[r]->dev + lo, hi - lo, 0, 0};
+    }
+  }
+  job.slice_bytes = S;
+  job.sums_expected = srcs[0]->sums(slot[0]);
   job.result = c->result;
   job.sched = c->done + 12;
   finalize_job(job);
@@ -1623,6 +1670,12 @@ extern "C" int ffx_recover(ffx_ctx* c, ffx_replica* src, uint64_t target, void* 
                 (unsigned long long)R.first_bad_slice);
   }
   return FFX_OK;
+}
+
+extern "C" int ffx_recover(ffx_ctx* c, ffx_replica* src, uint64_t target, void* stream,
+                           ffx_recover_report* rep) {
+  if (!c || !src) return fail(FFX_EINVAL, "recover: null argument");
+  return ffx_recover_from(c, &src, 1, target, stream, rep);
 }
 
 extern "C" int ffx_recover_region(ffx_ctx* c, uint32_t idx, const void* peer_src,

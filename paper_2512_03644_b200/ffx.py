@@ -143,7 +143,8 @@ class SnapshotOpts(ctypes.Structure):
                 ("gate_events", ctypes.c_void_p), ("verify_on_store", ctypes.c_uint32),
                 ("weights_kind", ctypes.c_uint32), ("split", ctypes.c_uint32),
                 ("hash_batches", ctypes.c_uint32), ("hash_ctas", ctypes.c_uint32),
-                ("copy_engine", ctypes.c_uint32)]
+                ("copy_engine", ctypes.c_uint32), ("pad_", ctypes.c_uint32),
+                ("batch_weights", ctypes.POINTER(ctypes.c_double))]
 
 
 class RecoverReport(ctypes.Structure):
@@ -247,6 +248,7 @@ SIGNATURES = {
     "ffx_snapshot_next_kind": (_I, [_P, _I, _P, _P, ctypes.POINTER(_U32)]),
     "ffx_snapshot_read_sums": (_I, [_P, _P, _U64, ctypes.POINTER(_U64), _P]),
     "ffx_recover": (_I, [_P, _P, _U64, _P, ctypes.POINTER(RecoverReport)]),
+    "ffx_recover_from": (_I, [_P, ctypes.POINTER(_P), _U32, _U64, _P, ctypes.POINTER(RecoverReport)]),
     "ffx_recover_region": (_I, [_P, _U32, _P, _P, _P, ctypes.POINTER(RecoverReport)]),
     "ffx_ipc_export": (_I, [_P, _P]),
     "ffx_ipc_open": (_I, [_P, ctypes.POINTER(_P)]),
@@ -656,8 +658,11 @@ class Context:
 
     def snapshot_begin(self, iteration: int, batches: int = 1, max_ctas: int = 0,
                        verify_on_store: bool = False, split: bool = False, hash_batches: int = 0,
-                       hash_ctas: int = 0, copy_engine: bool = False) -> int:
+                       hash_ctas: int = 0, copy_engine: bool = False, batch_weights=None) -> int:
         o = SnapshotOpts()
+        if batch_weights is not None:
+            self._weights = (ctypes.c_double * len(batch_weights))(*batch_weights)  # kept alive
+            o.batch_weights = self._weights
         o.max_ctas = max_ctas
         o.batches = batches
         o.verify_on_store = int(verify_on_store)
@@ -693,6 +698,14 @@ class Context:
     def recover(self, replica: Replica, target: int, stream=None) -> RecoverReport:
         rep = RecoverReport()
         check(lib.ffx_recover(self._c, replica.ptr, target, _stream_ptr(stream), ctypes.byref(rep)), "recover")
+        return rep
+
+    def recover_from(self, replicas, target: int, stream=None) -> RecoverReport:
+        """Parallel gather of one snapshot from several holders."""
+        rep = RecoverReport()
+        arr = (ctypes.c_void_p * len(replicas))(*[r.ptr.value for r in replicas])
+        check(lib.ffx_recover_from(self._c, arr, len(replicas), target, _stream_ptr(stream), ctypes.byref(rep)),
+              "recover_from")
         return rep
 
     def recover_region(self, index: int, peer_src: int, peer_sums: int, stream=None) -> RecoverReport:

@@ -99,16 +99,40 @@ class SliceScheduler:
         self.done = torch.cuda.Event()
         self.copies = self.hashes = 0
 
+    weights = None  # measured idle-link window per copy gap (calibrate())
+
+    def calibrate(self):
+        """Measure the step's idle-link windows: from each all-gather's
+        completion to the next collective (or the optimizer).  The copy
+        batches are then sized in proportion (ffx_snapshot_opts.batch_weights)."""
+        marks = []
+
+        def rec(kind, layer):
+            ev = torch.cuda.Event(enable_timing=True)
+            ev.record(self.step.train)
+            marks.append((kind, ev))
+
+        self.step.run(rec)
+        torch.cuda.synchronize()
+        w = []
+        for i, (kind, ev) in enumerate(marks):
+            if kind in ("fwd", "bwd") and i + 1 < len(marks):
+                w.append(max(ev.elapsed_time(marks[i + 1][1]), 1e-3))
+        self.weights = w
+        return w
+
     def begin(self, iteration: int):
         # one batch per all-gather gap, forward and backward (2L gaps)
         G = 2 * self.step.layers
+        weights = self.weights if self.weights and len(self.weights) == G else None
         if self.policy == "fused":
-            self.copies = self.ctx.snapshot_begin(iteration, batches=G, max_ctas=self.copy_ctas)
+            self.copies = self.ctx.snapshot_begin(iteration, batches=G, max_ctas=self.copy_ctas,
+                                                  batch_weights=weights)
             self.hashes = 0
         else:
             self.copies = self.ctx.snapshot_begin(iteration, batches=G, max_ctas=self.copy_ctas, split=True,
                                                   hash_batches=G, hash_ctas=self.hash_ctas,
-                                                  copy_engine=self.copy_engine)
+                                                  copy_engine=self.copy_engine, batch_weights=weights)
             self.hashes = G
 
     def _issue(self, kind, stream, gate=None):
@@ -162,6 +186,7 @@ def measure_overhead(step: SyntheticStep, sched: SliceScheduler, steps: int = 8,
                      it0: int = 1):
     """Interleaved A/B: steps without and with the concurrent snapshot."""
     time_steps(step, warmup)
+    sched.calibrate()
     time_steps(step, warmup, sched, it0=it0 + 100_000)
     base, with_snap = [], []
     it = it0
@@ -172,6 +197,7 @@ def measure_overhead(step: SyntheticStep, sched: SliceScheduler, steps: int = 8,
     b = statistics.median(base)
     w = statistics.median(with_snap)
     return {"policy": sched.policy + ("+ce" if sched.copy_engine else ""), "copy_ctas": sched.copy_ctas,
+            "measured_gaps_ms": [round(sum(sched.weights), 3), len(sched.weights)] if sched.weights else None,
             "hash_ctas": sched.hash_ctas, "step_ms_without": round(b, 3), "step_ms_with": round(w, 3),
             "overhead_pct": round(100.0 * (w - b) / b, 3), "steps_each": steps,
             "train_link_bytes_per_step": step.train_link_bytes}
