@@ -17,6 +17,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "ffx_device.cuh"
 #include "ffx_kernels.h"
@@ -160,6 +161,29 @@ __global__ void __launch_bounds__(32) copy_kernel(const __grid_constant__ CopyJo
   }
 }
 
+// SM copy (measurement reference for the probe, FFX_COPY_SM=1): grid-stride
+// 16-byte loads / stores, 4 in flight per thread.
+__global__ void __launch_bounds__(256) sm_copy_kernel(const __grid_constant__ CopyJob job) {
+  for (uint32_t r = 0; r < job.nregions; ++r) {
+    const CopyRegion& R = job.reg[r];
+    const uint64_t nv = R.bytes / 16;
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    const uint4* s = reinterpret_cast<const uint4*>(R.src);
+    uint4* d = reinterpret_cast<uint4*>(R.dst);
+    uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+    for (; i + 3 * stride < nv; i += 4 * stride) {
+      const uint4 a = ld_stream(s + i), b = ld_stream(s + i + stride), c = ld_stream(s + i + 2 * stride),
+                  e = ld_stream(s + i + 3 * stride);
+      st_stream(d + i, a);
+      st_stream(d + i + stride, b);
+      st_stream(d + i + 2 * stride, c);
+      st_stream(d + i + 3 * stride, e);
+    }
+    for (; i < nv; i += stride) st_stream(d + i, ld_stream(s + i));
+    if (blockIdx.x == 0 && threadIdx.x < R.bytes % 16) R.dst[nv * 16 + threadIdx.x] = R.src[nv * 16 + threadIdx.x];
+  }
+}
+
 // Single thread: the final slot commit (meta, SNP1 header, then COMMITTED).
 __global__ void commit_kernel(const __grid_constant__ SlotCommit c) {
   __threadfence_system();
@@ -211,6 +235,11 @@ cudaError_t launch_copy(const CopyJob& job, uint32_t ctas, cudaStream_t stream) 
     cudaError_t e = cudaFuncSetAttribute(copy_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kCopySmem);
     if (e != cudaSuccess) return e;
     attr = true;
+  }
+  static const bool sm = std::getenv("FFX_COPY_SM") != nullptr;
+  if (sm && job.chunk_lo == 0 && job.chunk_hi == job.total_chunks && job.mark.slot == nullptr) {
+    sm_copy_kernel<<<ctas ? ctas : 148 * 8, 256, 0, stream>>>(job);
+    return cudaGetLastError();
   }
   const uint64_t n = job.chunk_hi - job.chunk_lo;
   const uint64_t grid = std::max<uint64_t>(1, std::min<uint64_t>(n, ctas ? ctas : 16));
