@@ -120,6 +120,19 @@ __device__ __forceinline__ void tensor_store(const CUtensorMap* map, int x, int 
                ::"l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(src)
                : "memory");
 }
+// 3-D variant: box {128, ROWS, KC} -- KC consecutive 128 B chunks of each
+// slice per op, laid out in shared memory as KC planes of ROWS x 128 B.
+__device__ __forceinline__ void tensor_load3(uint32_t dst, const CUtensorMap* map, int y, int z, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];"
+      ::"r"(dst), "l"(reinterpret_cast<uint64_t>(map)), "r"(0), "r"(y), "r"(z), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void tensor_store3(const CUtensorMap* map, int y, int z, uint32_t src) {
+  asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.tile.bulk_group [%0, {%1, %2, %3}], [%4];"
+               ::"l"(reinterpret_cast<uint64_t>(map)), "r"(0), "r"(y), "r"(z), "r"(src)
+               : "memory");
+}
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_read_all() {
   asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
@@ -179,12 +192,13 @@ __device__ __forceinline__ void commit_end(const SlotCommit& c) {
   *c.done = 0;
 }
 
-template <int S, int W, int RPL>
+template <int S, int W, int RPL, int KC>
 struct Cfg {
-  static constexpr int C = 128;                      // bytes of each slice per step (one TMA row)
+  static constexpr int C = 128;                      // bytes of each slice per plane (one TMA row)
   static constexpr int VPL = C / 16;                 // 16-byte vectors per row
   static constexpr int ROWS = 32 * RPL;              // slices per warp task (RPL per lane)
-  static constexpr int STAGE = ROWS * C;             // one 128 x ROWS TMA box, dense + swizzled
+  static constexpr int PLANE = ROWS * C;             // 128 x ROWS, dense + swizzled
+  static constexpr int STAGE = PLANE * KC;           // one TMA box: KC planes
   static constexpr int PADROW = C + 16;              // register-path row, padded for banks
   static constexpr int WARPB = S * STAGE > 32 * PADROW ? S * STAGE : 32 * PADROW;
   static constexpr int BARB = ((W * S * 8 + 1023) / 1024) * 1024;
@@ -194,9 +208,10 @@ struct Cfg {
 // One warp task = ROWS consecutive slices of one region; lane l owns slices
 // l, l+32, ... (RPL independent FNV chains per lane -- the ILP that hides the
 // chains' multiply latency).
-template <int S, int W, int RPL, bool kStg, SliceMode M, bool kCommit>
+template <int S, int W, int RPL, int KC, bool kStg, SliceMode M, bool kCommit>
 __global__ void __launch_bounds__(W * 32) slice_kernel(const __grid_constant__ SliceJob job) {
-  using K = Cfg<S, W, RPL>;
+  using K = Cfg<S, W, RPL, KC>;
+  static_assert(!kStg || KC == 1, "SM stores are implemented for single-plane boxes");
   constexpr int C = K::C;
   constexpr bool kCopy = (M == SliceMode::Copy || M == SliceMode::CopyVerify);
   constexpr bool kVerify = (M == SliceMode::CopyVerify || M == SliceMode::HashVerify);
@@ -263,14 +278,15 @@ __global__ void __launch_bounds__(W * 32) slice_kernel(const __grid_constant__ S
       const CUtensorMap* mdst = &job.maps[3 * R.tmap + 1];
       const CUtensorMap* mdst2 = &job.maps[3 * R.tmap + 2];
       const bool dual = R.dst2 != nullptr;
-      const int nsteps = static_cast<int>(Sl / C);
+      const int nsteps = static_cast<int>(Sl / (C * KC));
       const int y = static_cast<int>(s0);
       const int pro = nsteps < S ? nsteps : S;
       if (lane == 0) {
         fence_async_smem();  // rows written by the register path -> async proxy
         for (int k = 0; k < pro; ++k) {
           mbar_expect_tx(bar0 + 8 * k, K::STAGE);
-          tensor_load(stage0 + k * K::STAGE, msrc, k * C, y, bar0 + 8 * k);
+          if constexpr (KC == 1) tensor_load(stage0 + k * K::STAGE, msrc, k * C, y, bar0 + 8 * k);
+          else tensor_load3(stage0 + k * K::STAGE, msrc, y, k * KC, bar0 + 8 * k);
         }
       }
       const int sw = lane & 7;  // (lane + 32 r) & 7 == lane & 7
@@ -281,8 +297,13 @@ __global__ void __launch_bounds__(W * 32) slice_kernel(const __grid_constant__ S
         const uint32_t tile = stage0 + s * K::STAGE;
         if constexpr (kCopy && !kStg) {
           if (lane == 0) {
-            tensor_store(mdst, k * C, y, tile);
-            if (dual) tensor_store(mdst2, k * C, y, tile);  // double neighbour: read once, write twice
+            if constexpr (KC == 1) {
+              tensor_store(mdst, k * C, y, tile);
+              if (dual) tensor_store(mdst2, k * C, y, tile);  // double neighbour: read once, write twice
+            } else {
+              tensor_store3(mdst, y, k * KC, tile);
+              if (dual) tensor_store3(mdst2, y, k * KC, tile);
+            }
             bulk_commit();
           }
         }
@@ -300,24 +321,28 @@ __global__ void __launch_bounds__(W * 32) slice_kernel(const __grid_constant__ S
             if (dual) st_stream(R.dst2 + o, val);
           }
         }
-        uint4 v[RPL][K::VPL];
 #pragma unroll
-        for (int r = 0; r < RPL; ++r) {
-          const uint8_t* row = wbase + s * K::STAGE + (lane + 32 * r) * C;
+        for (int kc = 0; kc < KC; ++kc) {  // planes in byte order
+          uint4 v[RPL][K::VPL];
 #pragma unroll
-          for (int w = 0; w < K::VPL; ++w) v[r][w] = lds128(row + ((w ^ sw) << 4));
+          for (int r = 0; r < RPL; ++r) {
+            const uint8_t* row = wbase + s * K::STAGE + kc * K::PLANE + (lane + 32 * r) * C;
+#pragma unroll
+            for (int w = 0; w < K::VPL; ++w) v[r][w] = lds128(row + ((w ^ sw) << 4));
+          }
+#pragma unroll
+          for (int w = 0; w < K::VPL; ++w)
+#pragma unroll
+            for (int r = 0; r < RPL; ++r) h[r].vec(v[r][w]);  // RPL chains interleaved
         }
-#pragma unroll
-        for (int w = 0; w < K::VPL; ++w)
-#pragma unroll
-          for (int r = 0; r < RPL; ++r) h[r].vec(v[r][w]);  // RPL chains interleaved
         if (k + S < nsteps) {
           __syncwarp();
           if (lane == 0) {
             if constexpr (kCopy) bulk_wait_read_all();
             if (job.proxy_fence) fence_async_smem();
             mbar_expect_tx(bar0 + 8 * s, K::STAGE);
-            tensor_load(tile, msrc, (k + S) * C, y, bar0 + 8 * s);
+            if constexpr (KC == 1) tensor_load(tile, msrc, (k + S) * C, y, bar0 + 8 * s);
+            else tensor_load3(tile, msrc, y, (k + S) * KC, bar0 + 8 * s);
           }
         }
       }
@@ -402,10 +427,10 @@ __global__ void __launch_bounds__(W * 32) slice_kernel(const __grid_constant__ S
 
 int g_sms = 0;
 
-template <int S, int W, int RPL, bool kStg, SliceMode M, bool kCommit>
+template <int S, int W, int RPL, bool kStg, SliceMode M, bool kCommit, int KC = 1>
 cudaError_t launch_t(const SliceJob& job, uint32_t max_ctas, cudaStream_t stream) {
-  auto kern = slice_kernel<S, W, RPL, kStg, M, kCommit>;
-  constexpr int smem = Cfg<S, W, RPL>::SMEM;
+  auto kern = slice_kernel<S, W, RPL, KC, kStg, M, kCommit>;
+  constexpr int smem = Cfg<S, W, RPL, KC>::SMEM;
   static int occ = 0;
   if (occ == 0) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -434,10 +459,12 @@ int variant() {
 // Kernel variants for tuning (FFX_SLICE_VARIANT): stages / warps per CTA /
 // slices per lane.  The warp-task size (32 * RPL slices) follows the variant.
 struct Variant {
-  int S, W, RPL, stg;
+  int S, W, RPL, stg, KC;
 };
-constexpr Variant kVariants[] = {{4, 4, 1, 0}, {2, 4, 2, 0}, {3, 4, 2, 0}, {6, 4, 1, 0}, {3, 4, 1, 0},
-                                 {2, 8, 2, 0}, {4, 4, 1, 1}, {3, 4, 2, 1}, {6, 4, 1, 1}};
+constexpr Variant kVariants[] = {{4, 4, 1, 0, 1}, {2, 4, 2, 0, 1}, {3, 4, 2, 0, 1}, {6, 4, 1, 0, 1},
+                                 {3, 4, 1, 0, 1}, {2, 8, 2, 0, 1}, {4, 4, 1, 1, 1}, {3, 4, 2, 1, 1},
+                                 {6, 4, 1, 1, 1}, {2, 4, 1, 0, 2}, {3, 4, 1, 0, 2}, {2, 4, 1, 0, 4},
+                                 {2, 8, 1, 0, 2}};
 
 template <SliceMode M, bool kCommit>
 cudaError_t launch_mode(const SliceJob& job, uint32_t max_ctas, cudaStream_t stream) {
@@ -450,6 +477,10 @@ cudaError_t launch_mode(const SliceJob& job, uint32_t max_ctas, cudaStream_t str
     case 6: return launch_t<4, 4, 1, true, M, kCommit>(job, max_ctas, stream);
     case 7: return launch_t<3, 4, 2, true, M, kCommit>(job, max_ctas, stream);
     case 8: return launch_t<6, 4, 1, true, M, kCommit>(job, max_ctas, stream);
+    case 9: return launch_t<2, 4, 1, false, M, kCommit, 2>(job, max_ctas, stream);
+    case 10: return launch_t<3, 4, 1, false, M, kCommit, 2>(job, max_ctas, stream);
+    case 11: return launch_t<2, 4, 1, false, M, kCommit, 4>(job, max_ctas, stream);
+    case 12: return launch_t<2, 8, 1, false, M, kCommit, 2>(job, max_ctas, stream);
     default: return launch_t<4, 4, 1, false, M, kCommit>(job, max_ctas, stream);
   }
 }
@@ -466,10 +497,14 @@ int sm_count() {
   return g_sms;
 }
 
-int task_rows() {
+namespace {
+const Variant& active_variant() {
   const int v = variant();
-  return 32 * kVariants[(v >= 0 && v < static_cast<int>(sizeof kVariants / sizeof kVariants[0])) ? v : 0].RPL;
+  return kVariants[(v >= 0 && v < static_cast<int>(sizeof kVariants / sizeof kVariants[0])) ? v : 0];
 }
+}  // namespace
+
+int task_rows() { return 32 * active_variant().RPL; }
 
 void finalize_job(SliceJob& job) {
   const uint64_t rows = static_cast<uint64_t>(task_rows());
@@ -503,9 +538,20 @@ PFN_cuTensorMapEncodeTiled_v12000 encoder() {
   return fn;
 }
 
-bool encode_rows(CUtensorMap* map, const void* base, uint64_t slice_bytes, uint64_t nfull, uint32_t rows) {
+bool encode_rows(CUtensorMap* map, const void* base, uint64_t slice_bytes, uint64_t nfull, uint32_t rows,
+                 uint32_t kc) {
   auto enc = encoder();
   if (!enc) return false;
+  if (kc > 1) {
+    // {byte in chunk, slice, chunk}: strides {slice_bytes, 128}; box {128, rows, kc}
+    const cuuint64_t dims3[3] = {128, nfull, slice_bytes / 128};
+    const cuuint64_t strides3[2] = {slice_bytes, 128};
+    const cuuint32_t box3[3] = {128, rows, kc};
+    const cuuint32_t estr3[3] = {1, 1, 1};
+    return enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<void*>(base), dims3, strides3, box3, estr3,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+  }
   const cuuint64_t dims[2] = {slice_bytes, nfull};
   const cuuint64_t strides[1] = {slice_bytes};
   const cuuint32_t box[2] = {128, rows};
@@ -530,10 +576,12 @@ void attach_tensor_maps(SliceJob& job, bool copy) {
     const uint32_t rows = static_cast<uint32_t>(task_rows());
     if (!al || R.nfull < rows || R.nfull > (1ull << 31)) continue;
     if (R.dst2 != nullptr && reinterpret_cast<uintptr_t>(R.dst2) % 16 != 0) continue;
-    if (!encode_rows(&job.maps[3 * used], R.src, job.slice_bytes, R.nfull, rows)) continue;
-    if (copy && !encode_rows(&job.maps[3 * used + 1], R.dst, job.slice_bytes, R.nfull, rows)) continue;
+    const uint32_t kc = static_cast<uint32_t>(active_variant().KC);
+    if (job.slice_bytes % (128ull * kc) != 0) continue;
+    if (!encode_rows(&job.maps[3 * used], R.src, job.slice_bytes, R.nfull, rows, kc)) continue;
+    if (copy && !encode_rows(&job.maps[3 * used + 1], R.dst, job.slice_bytes, R.nfull, rows, kc)) continue;
     if (copy && R.dst2 != nullptr &&
-        !encode_rows(&job.maps[3 * used + 2], R.dst2, job.slice_bytes, R.nfull, rows))
+        !encode_rows(&job.maps[3 * used + 2], R.dst2, job.slice_bytes, R.nfull, rows, kc))
       continue;
     R.tmap = used++;
   }
