@@ -461,9 +461,12 @@ int variant() {
 struct Variant {
   int S, W, RPL, stg, KC;
 };
-constexpr Variant kVariants[] = {{4, 4, 1, 0, 1}, {2, 4, 2, 0, 1}, {3, 4, 2, 0, 1}, {6, 4, 1, 0, 1},
+// 0 (default): 3 stages, 4 warps, 1 slice per lane, 2 chunks (256 B of
+// each slice) per TMA op -- the best of the round-1 sweep
+// (profiles/r1_variant_sweep_1gpu.jsonl); 10 was the previous default.
+constexpr Variant kVariants[] = {{3, 4, 1, 0, 2}, {2, 4, 2, 0, 1}, {3, 4, 2, 0, 1}, {6, 4, 1, 0, 1},
                                  {3, 4, 1, 0, 1}, {2, 8, 2, 0, 1}, {4, 4, 1, 1, 1}, {3, 4, 2, 1, 1},
-                                 {6, 4, 1, 1, 1}, {2, 4, 1, 0, 2}, {3, 4, 1, 0, 2}, {2, 4, 1, 0, 4},
+                                 {6, 4, 1, 1, 1}, {2, 4, 1, 0, 2}, {4, 4, 1, 0, 1}, {2, 4, 1, 0, 4},
                                  {2, 8, 1, 0, 2}};
 
 template <SliceMode M, bool kCommit>
@@ -478,10 +481,10 @@ cudaError_t launch_mode(const SliceJob& job, uint32_t max_ctas, cudaStream_t str
     case 7: return launch_t<3, 4, 2, true, M, kCommit>(job, max_ctas, stream);
     case 8: return launch_t<6, 4, 1, true, M, kCommit>(job, max_ctas, stream);
     case 9: return launch_t<2, 4, 1, false, M, kCommit, 2>(job, max_ctas, stream);
-    case 10: return launch_t<3, 4, 1, false, M, kCommit, 2>(job, max_ctas, stream);
+    case 10: return launch_t<4, 4, 1, false, M, kCommit>(job, max_ctas, stream);
     case 11: return launch_t<2, 4, 1, false, M, kCommit, 4>(job, max_ctas, stream);
     case 12: return launch_t<2, 8, 1, false, M, kCommit, 2>(job, max_ctas, stream);
-    default: return launch_t<4, 4, 1, false, M, kCommit>(job, max_ctas, stream);
+    default: return launch_t<3, 4, 1, false, M, kCommit, 2>(job, max_ctas, stream);
   }
 }
 
