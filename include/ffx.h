@@ -374,6 +374,23 @@ int ffx_recover(ffx_ctx* ctx, ffx_replica* src, uint64_t target, void* stream,
 int ffx_recover_from(ffx_ctx* ctx, ffx_replica* const* srcs, uint32_t nsrc, uint64_t target, void* stream,
                      ffx_recover_report* report);
 
+/* A redundant region's live copy on a DP peer (weights, ckpt.cpp:150-152):
+ * peer-mapped pointer + the peer's slice table (ffx_slice_checksums with this
+ * ctx's slice size). */
+typedef struct ffx_peer_region {
+  uint32_t region_index; /* index in this ctx's registration order */
+  uint32_t pad_;
+  const void* src;
+  const uint64_t* sums;
+} ffx_peer_region;
+
+/* Full-state restore in one kernel (assemble_restore, ckpt.cpp:140-167): the
+ * unique regions from the replica holders (split across nsrc sources) and
+ * every redundant region from its live peer, all gathered concurrently and
+ * each part verified against its own source's checksum table. */
+int ffx_recover_full(ffx_ctx* ctx, ffx_replica* const* srcs, uint32_t nsrc, uint64_t target,
+                     const ffx_peer_region* redundant, uint32_t nred, void* stream, ffx_recover_report* report);
+
 /* Pull one redundant region (weights from a live DP peer, ckpt.cpp:150-152)
  * from a peer device pointer, verifying against the peer's slice table
  * (computed by the peer with ffx_slice_checksums). */

@@ -9,6 +9,7 @@
 #include <unistd.h>
 
 #include <algorithm>
+#include <numeric>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -1668,6 +1669,93 @@ extern "C" int ffx_recover_from(ffx_ctx* c, ffx_replica* const* srcs, uint32_t n
     return fail(FFX_ERESTORE, "unique-state source invalid: snapshot checksum mismatch in %llu "
                 "slices (first slice %llu)", (unsigned long long)R.bad_slices,
                 (unsigned long long)R.first_bad_slice);
+  }
+  return FFX_OK;
+}
+
+extern "C" int ffx_recover_full(ffx_ctx* c, ffx_replica* const* srcs, uint32_t nsrc, uint64_t target,
+                                const ffx_peer_region* redundant, uint32_t nred, void* stream,
+                                ffx_recover_report* rep) {
+  if (!c || (nsrc && !srcs) || (nred && !redundant) || nsrc > 4) return fail(FFX_EINVAL, "recover_full: bad arguments");
+  DeviceGuard g(c->device);
+  ffx_recover_report local{};
+  ffx_recover_report& R = rep ? *rep : local;
+  std::memset(&R, 0, sizeof R);
+  R.first_bad_slice = ~0ull;
+  SlotMeta m[4];
+  uint32_t slot[4];
+  for (uint32_t i = 0; i < nsrc; ++i) {
+    int st = check_source(c, srcs[i], target, &m[i], &slot[i]);
+    if (st) return st;
+    if (m[i].slice_bytes != c->slice_bytes)
+      return fail(FFX_ERESTORE, "snapshot slice size %llu, context %llu", (unsigned long long)m[i].slice_bytes,
+                  (unsigned long long)c->slice_bytes);
+  }
+  const PayloadMap pm = payload_map(c);
+  if (nsrc == 0 && !pm.regs.empty()) return fail(FFX_ERESTORE, "unique-state source missing");
+  const uint64_t S = c->slice_bytes;
+  // One kernel, every source at once: the unique regions split across the
+  // replica holders, each redundant region from its live DP peer (weights,
+  // ckpt.cpp:150-152), each part verified against its own source's table.
+  SliceJob job{};
+  auto add = [&](const uint8_t* src, uint8_t* dst, uint64_t bytes, const uint64_t* expected) -> int {
+    if (job.nregions >= kMaxRegions) return fail(FFX_ECONFIG, "recover_full: more than %u parts", kMaxRegions);
+    SliceRegion sr{src, dst, bytes, 0, 0};
+    sr.expected = expected;
+    job.reg[job.nregions++] = sr;
+    return FFX_OK;
+  };
+  uint64_t total = 0;
+  for (size_t r = 0; r < pm.regs.size(); ++r) {
+    const uint64_t ns = slices_of(pm.regs[r]->bytes, S);
+    const uint64_t base = std::accumulate(pm.regs.begin(), pm.regs.begin() + r, uint64_t{0},
+                                          [&](uint64_t a, const Region* q) { return a + slices_of(q->bytes, S); });
+    for (uint32_t i = 0; i < nsrc; ++i) {
+      const uint64_t a = ns * i / nsrc, b = ns * (i + 1) / nsrc;
+      const uint64_t lo = a * S, hi = std::min(b * S, pm.regs[r]->bytes);
+      if (hi <= lo) continue;
+      int st = add(srcs[i]->payload(slot[i]) + pm.offs[r] + lo, pm.regs[r]->dev + lo, hi - lo,
+                   srcs[i]->sums(slot[i]) + base + a);
+      if (st) return st;
+    }
+    total += pm.regs[r]->bytes;
+  }
+  for (uint32_t j = 0; j < nred; ++j) {
+    const ffx_peer_region& pr = redundant[j];
+    if (pr.region_index >= c->regions.size() || c->regions[pr.region_index].unique)
+      return fail(FFX_ERANGE, "recover_full: region %u is not a registered redundant region", pr.region_index);
+    if (!pr.src || !pr.sums) return fail(FFX_EINVAL, "recover_full: null peer pointer");
+    const Region& reg = c->regions[pr.region_index];
+    int st = add(static_cast<const uint8_t*>(pr.src), reg.dev, reg.bytes, pr.sums);
+    if (st) return st;
+    total += reg.bytes;
+  }
+  cudaStream_t s = as_stream(stream);
+  job.slice_bytes = S;
+  job.result = c->result;
+  job.sched = c->done + 12;
+  finalize_job(job);
+  const unsigned long long init[2] = {~0ull, 0ull};
+  FFX_CUDA(cudaMemcpyAsync(c->result, init, sizeof init, cudaMemcpyHostToDevice, s));
+  FFX_CUDA(cudaEventRecord(c->ev0, s));
+  FFX_CUDA(launch_slices(job, SliceMode::CopyVerify, false, 0, s));
+  FFX_CUDA(cudaEventRecord(c->ev1, s));
+  c->stats.kernel_launches++;
+  FFX_CUDA(cudaMemcpyAsync(c->result_host, c->result, 16, cudaMemcpyDeviceToHost, s));
+  FFX_CUDA(cudaStreamSynchronize(s));
+  float ms = 0;
+  cudaEventElapsedTime(&ms, c->ev0, c->ev1);
+  R.seconds = ms * 1e-3;
+  R.bytes = total;
+  R.slot = nsrc ? slot[0] : 0;
+  R.first_bad_slice = c->result_host[0];
+  R.bad_slices = c->result_host[1];
+  c->stats.recoveries++;
+  c->stats.recovered_bytes += total;
+  if (R.bad_slices) {
+    c->stats.verify_failures++;
+    return fail(FFX_ERESTORE, "restore source invalid: checksum mismatch in %llu slices (first %llu)",
+                (unsigned long long)R.bad_slices, (unsigned long long)R.first_bad_slice);
   }
   return FFX_OK;
 }

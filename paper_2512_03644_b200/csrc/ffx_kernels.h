@@ -23,6 +23,7 @@ struct SliceRegion {
   uint32_t pad_;
   uint64_t nfull;        // full-length slices (the tensor maps' outer extent)
   uint8_t* dst2;         // second replica (double-neighbour), null = none
+  const uint64_t* expected;  // verify: this region's own table (region-local index), else the job's
 };
 
 constexpr int kTmaRegions = 4;  // regions that get 2-D TMA tensor maps per launch

@@ -397,7 +397,8 @@ __global__ void __launch_bounds__(W * 32) slice_kernel(const __grid_constant__ S
       if (job.sums_out != nullptr) job.sums_out[idx] = v;
       if (job.sums_out2 != nullptr) job.sums_out2[idx] = v;
       if constexpr (kVerify) {
-        if (v != job.sums_expected[idx]) {
+        const uint64_t want = R.expected != nullptr ? R.expected[s0 + lane + 32 * r] : job.sums_expected[idx];
+        if (v != want) {
           atomicMin(&job.result[0], static_cast<unsigned long long>(idx));
           atomicAdd(&job.result[1], 1ull);
         }

@@ -153,6 +153,11 @@ class RecoverReport(ctypes.Structure):
                 ("seconds", ctypes.c_double)]
 
 
+class PeerRegion(ctypes.Structure):
+    _fields_ = [("region_index", ctypes.c_uint32), ("pad_", ctypes.c_uint32),
+                ("src", ctypes.c_void_p), ("sums", ctypes.c_void_p)]
+
+
 class Stats(ctypes.Structure):
     _fields_ = [("snapshots", ctypes.c_uint64), ("snapshot_bytes", ctypes.c_uint64),
                 ("recoveries", ctypes.c_uint64), ("recovered_bytes", ctypes.c_uint64),
@@ -248,6 +253,8 @@ SIGNATURES = {
     "ffx_snapshot_next_kind": (_I, [_P, _I, _P, _P, ctypes.POINTER(_U32)]),
     "ffx_snapshot_read_sums": (_I, [_P, _P, _U64, ctypes.POINTER(_U64), _P]),
     "ffx_recover": (_I, [_P, _P, _U64, _P, ctypes.POINTER(RecoverReport)]),
+    "ffx_recover_full": (_I, [_P, ctypes.POINTER(_P), _U32, _U64, ctypes.POINTER(PeerRegion), _U32, _P,
+                              ctypes.POINTER(RecoverReport)]),
     "ffx_recover_from": (_I, [_P, ctypes.POINTER(_P), _U32, _U64, _P, ctypes.POINTER(RecoverReport)]),
     "ffx_recover_region": (_I, [_P, _U32, _P, _P, _P, ctypes.POINTER(RecoverReport)]),
     "ffx_ipc_export": (_I, [_P, _P]),
@@ -698,6 +705,16 @@ class Context:
     def recover(self, replica: Replica, target: int, stream=None) -> RecoverReport:
         rep = RecoverReport()
         check(lib.ffx_recover(self._c, replica.ptr, target, _stream_ptr(stream), ctypes.byref(rep)), "recover")
+        return rep
+
+    def recover_full(self, replicas, target: int, redundant=(), stream=None) -> RecoverReport:
+        """Full-state restore: unique regions from the replica holders, redundant
+        regions [(region_index, peer_ptr, peer_sums_ptr)] from live peers, one kernel."""
+        rep = RecoverReport()
+        arr = (ctypes.c_void_p * max(1, len(replicas)))(*[r.ptr.value for r in replicas])
+        red = (PeerRegion * max(1, len(redundant)))(*[PeerRegion(i, 0, p, s) for i, p, s in redundant])
+        check(lib.ffx_recover_full(self._c, arr, len(replicas), target, red, len(redundant),
+                                   _stream_ptr(stream), ctypes.byref(rep)), "recover_full")
         return rep
 
     def recover_from(self, replicas, target: int, stream=None) -> RecoverReport:

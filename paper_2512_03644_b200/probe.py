@@ -66,6 +66,14 @@ def main():
         out["%s_fused_gbs" % name] = round(scale * n / t / 1e9, 1)
     t = timed(lambda: ffx.slice_checksums(src, args.slice, sums))
     out["hash_read_gbs"] = round(n / t / 1e9, 1)
+    # whole-payload checksum64 (SNP1 export path): speculative low byte + affine combine
+    t = timed(lambda: ffx.checksum64(src), reps=3, warm=1)
+    out["whole_checksum64_gbs"] = round(n / t / 1e9, 1)
+    # synthetic state generation (evo::materialize) and soundness check
+    t = timed(lambda: ffx.materialize(src, bytes(range(32))))
+    out["materialize_gbs"] = round(n / t / 1e9, 1)
+    t = timed(lambda: ffx.blob_first_bad(src), reps=3, warm=1)
+    out["blob_check_gbs"] = round(n / t / 1e9, 1)
     print(json.dumps(out))
 
 
