@@ -73,32 +73,55 @@ __global__ void expand_kernel(uint8_t* dst, uint64_t fold, uint64_t bytes, uint6
   }
 }
 
+// blob_is_sound, one 16-byte vector (bytes past `bytes` ignored).
+__device__ __forceinline__ void check_vec(uint64_t fold, uint64_t o, uint64_t bytes, const uint4& got,
+                                          unsigned long long* result) {
+  const uint64_t w = (o - 32) / 8;
+  const uint64_t a = mix64(fold + (w + 1) * kGolden);
+  const uint64_t b = mix64(fold + (w + 2) * kGolden);
+  const uint32_t want[4] = {static_cast<uint32_t>(a), static_cast<uint32_t>(a >> 32),
+                            static_cast<uint32_t>(b), static_cast<uint32_t>(b >> 32)};
+  const uint32_t have[4] = {got.x, got.y, got.z, got.w};
+  const uint64_t n = bytes - o < 16 ? bytes - o : 16;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    uint32_t diff = want[i] ^ have[i];
+    const int64_t valid = static_cast<int64_t>(n) - 4 * i;
+    if (valid <= 0) diff = 0;
+    else if (valid < 4) diff &= (1u << (8 * valid)) - 1u;
+    if (diff) {
+      atomicMin(result, static_cast<unsigned long long>(o + 4 * i + (__ffs(diff) - 1) / 8));
+      break;
+    }
+  }
+}
+
+constexpr int kCheckUnroll = 4;  // 16-byte loads in flight per thread (read-only stream)
+
 __global__ void check_kernel(const uint8_t* blob, uint64_t bytes, unsigned long long* result) {
-  uint64_t fold = 0;
-  for (int i = 7; i >= 0; --i) fold = (fold << 8) | blob[i];
+  __shared__ uint64_t s_fold;
+  if (threadIdx.x == 0) {
+    uint64_t f = 0;
+    for (int i = 7; i >= 0; --i) f = (f << 8) | blob[i];
+    s_fold = f;
+  }
+  __syncthreads();
+  const uint64_t fold = s_fold;
   const uint64_t nvec = (bytes + 15) / 16;
   const bool al = aligned16(blob);
-  for (uint64_t t = 2 + blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; t < nvec;
-       t += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-    const uint64_t o = 16 * t;
-    const uint64_t w = (o - 32) / 8;
-    const uint64_t a = mix64(fold + (w + 1) * kGolden);
-    const uint64_t b = mix64(fold + (w + 2) * kGolden);
-    const uint4 got = load16(blob, o, bytes, al);
-    const uint32_t want[4] = {static_cast<uint32_t>(a), static_cast<uint32_t>(a >> 32),
-                              static_cast<uint32_t>(b), static_cast<uint32_t>(b >> 32)};
-    const uint32_t have[4] = {got.x, got.y, got.z, got.w};
-    const uint64_t n = bytes - o < 16 ? bytes - o : 16;
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  for (uint64_t t0 = 2 + blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; t0 < nvec;
+       t0 += kCheckUnroll * stride) {
+    uint4 got[kCheckUnroll];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      uint32_t diff = want[i] ^ have[i];
-      const int64_t valid = static_cast<int64_t>(n) - 4 * i;
-      if (valid <= 0) diff = 0;
-      else if (valid < 4) diff &= (1u << (8 * valid)) - 1u;
-      if (diff) {
-        atomicMin(result, static_cast<unsigned long long>(o + 4 * i + (__ffs(diff) - 1) / 8));
-        break;
-      }
+    for (int u = 0; u < kCheckUnroll; ++u) {  // issue every load before any compare
+      const uint64_t t = t0 + u * stride;
+      got[u] = t < nvec ? load16(blob, 16 * t, bytes, al) : make_uint4(0, 0, 0, 0);
+    }
+#pragma unroll
+    for (int u = 0; u < kCheckUnroll; ++u) {
+      const uint64_t t = t0 + u * stride;
+      if (t < nvec) check_vec(fold, 16 * t, bytes, got[u], result);
     }
   }
 }

@@ -241,9 +241,16 @@ __global__ void __launch_bounds__(W * 32) slice_kernel(const __grid_constant__ S
   for (;;) {
     uint64_t g;
     if (job.sched != nullptr) {
+      // Claims run from the LAST task down: each region's ragged tail (and
+      // tiny register-path regions) starts first and overlaps the bulk
+      // instead of running alone after it -- one latency-bound register-path
+      // task claimed last held an SM for ~130 us after the rest drained
+      // (ncu PM sampling, profiles/r1_ncu_snapshot_kc2_details.csv).
       unsigned t = 0;
       if (lane == 0) t = atomicAdd(&job.sched[0], 1u);
-      g = job.group_lo + __shfl_sync(0xffffffffu, t, 0);
+      t = __shfl_sync(0xffffffffu, t, 0);
+      if (t >= job.group_hi - job.group_lo) break;
+      g = job.group_hi - 1 - t;
     } else {
       g = g_next;
       g_next += g_stride;
