@@ -65,6 +65,7 @@ def parse():
     ap.add_argument("--sched-ctas", type=int, default=32, help="SM budget of scheduled snapshot batches")
     ap.add_argument("--no-70b", action="store_true", help="skip the 70B double-neighbour leg (N >= 3)")
     ap.add_argument("--prefix-70b", type=int, default=16 << 30, help="70B state prefix per rank (bytes)")
+    ap.add_argument("--no-mcast", action="store_true", help="skip the NVSwitch-multicast double neighbour")
     ap.add_argument("--mode", default="push", choices=["push", "pull"],
                     help="N>1 ring stream: origin pushes into its successor's replica, or the holder "
                          "pulls its predecessor's regions (NeighborBuffer::store side)")
@@ -203,7 +204,7 @@ class Ring:
     """This rank's ffx context, its state, the replica it holds for its ring
     predecessor and the view of the replica its successor holds for it."""
 
-    def __init__(self, ffx, torch, dist, world, rank, local, n, spec, slice_bytes, regions):
+    def __init__(self, ffx, torch, dist, world, rank, local, n, spec, slice_bytes, regions, versions=2):
         from paper_2512_03644_b200 import ring
         import pyoracle
         self.ffx, self.n = ffx, n
@@ -212,7 +213,7 @@ class Ring:
         if world == 1:
             # the ring collapses onto one GPU: a second context plays the holder
             self.holder = ffx.Context(local, spec, ffx.Role(1, 0, 0), slice_bytes)
-            self.held = self.holder.create_replica(ffx.Role(rank, 0, 0), n, 2)
+            self.held = self.holder.create_replica(ffx.Role(rank, 0, 0), n, versions)
             self.target = self.ctx.open_replica(self.held.export())
             self.handles = None
         else:
@@ -221,7 +222,7 @@ class Ring:
                 dist.all_gather_object(out, b)
                 return out
             held, targets, handles = ring.wire_ring(
-                rank, world, lambda origin: self.ctx.create_replica(ffx.Role(origin, 0, 0), n, 2),
+                rank, world, lambda origin: self.ctx.create_replica(ffx.Role(origin, 0, 0), n, versions),
                 lambda r: r.export(), self.ctx.open_replica, all_gather)
             self.held, self.target, self.handles = held[0], targets[0], handles
         self.ctx.set_target(self.target)
@@ -420,6 +421,12 @@ def main():
     llama = None
     if world > 1 and not args.no_llama:
         llama = llama_leg(args, ffx, torch, dist, world, rank, local, barrier)
+    dfail = None
+    if world in (2, 4) and not args.no_llama:
+        try:
+            dfail = llama_dfail_leg(args, ffx, torch, dist, world, rank, local, barrier)
+        except Exception as ex:
+            dfail = {"error": repr(ex)}
     seventy = None
     if world >= 3 and not args.no_70b:
         try:
@@ -450,6 +457,7 @@ def main():
             "per_gpu_gbs": round(value / world, 3),
             "nvlink_frac_per_gpu": round(value / world / NVLINK_MEASURED_GBS, 4) if world > 1 else None,
             "roofline": roof, "recovery": rec, "alt_ring_stream": alt, "llama3_8b": llama,
+            "llama3_8b_failure_at_d": dfail,
             "llama3_70b_double_neighbour": seventy,
             "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": int(launches), "clocks": ck, "commit_ok": bool(commit_ok),
@@ -531,14 +539,135 @@ def seventy_leg(args, ffx, torch, dist, world, rank, local, barrier):
     for r in targets + held:
         r.destroy()
     ctx.close()
+    torch.cuda.empty_cache()
+    mc = None
+    if not args.no_mcast:
+        ok = all(all_gather(bool(ffx.mcast_supported(local))))
+        if ok:
+            try:
+                mc = seventy_mcast(args, ffx, torch, dist, world, rank, local, barrier, all_gather, spec,
+                                   prefix, state, k)
+            except Exception as ex:  # reported, never fatal
+                mc = {"error": repr(ex)}
+        else:
+            mc = {"skipped": "no multicast support"}
     del state
     torch.cuda.empty_cache()
     return {"sizing": sizing, "prefix_bytes_per_rank": prefix,
+            "multicast": mc,
             "dual_store_egress_gbs_per_gpu": round(egress, 1),
             "plan_reference_rule": ffx.plan_recovery(spec, [], [ffx.Role(1, 0, 0), ffx.Role(2, 0, 0)],
                                                      last, 0, replicas=1).kind,
             "plan_double_neighbour": plan.kind,
             "adjacent_pair_recovery": [x for x in recs if x]}
+
+
+def seventy_mcast(args, ffx, torch, dist, world, rank, local, barrier, all_gather, spec, prefix, state, k):
+    """The same double neighbour with one egress per tile: each origin's
+    snapshot kernel stores into an NVSwitch multicast range bound to the
+    replica slots of dp+1 and dp+2 (ring.wire_mcast_ring), then the same
+    adjacent-pair loss is recovered from the dp+2 holders."""
+    from paper_2512_03644_b200 import ring
+    ctx = ffx.Context(local, spec, ffx.Role(rank, 0, 0), args.slice_bytes)
+    ctx.register(ffx.REGION_BLOB, state)
+    held, own, preds, view, handles = ring.wire_mcast_ring(
+        rank, world, lambda origin: ctx.create_shared_replica(ffx.Role(origin, 0, 0), prefix, 2),
+        lambda r: r.export(), ctx.open_replica, lambda: ctx.create_mcast(prefix, 2, members=3),
+        lambda m: m.export(), ctx.open_mcast, all_gather, barrier)
+    ctx.set_target_mcast(own, view)
+    s = torch.cuda.Stream()
+    for it in (1, 2):
+        ctx.snapshot(it, stream=s)
+    s.synchronize()
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(s)
+    for it in range(3, 3 + k):
+        ctx.snapshot(it, stream=s)
+    e1.record(s)
+    s.synchronize()
+    t = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    unique = prefix * k / (float(t.item()) * 1e-3) / 1e9
+    last = 2 + k
+    plan = ffx.plan_recovery(spec, [], [ffx.Role(1, 0, 0), ffx.Role(2, 0, 0)], last, 0, replicas=2)
+    sources = {o: (h, kk) for o, h, kk in ring.recovery_sources(plan.forwards, world)}
+    rec = None
+    barrier()
+    if rank in sources:
+        h, kk = sources[rank]
+        src = ctx.open_replica(handles[h][kk])
+        ctx.inject(ffx.FAULT_POISON_STATE)
+        rpt = ctx.recover(src, last, stream=s)
+        rec = {"holder": h, "recovery_s": round(rpt.seconds, 5),
+               "recovery_gbs": round(prefix / rpt.seconds / 1e9, 1),
+               "bit_exact": bool(rpt.bad_slices == 0 and ffx.blob_is_sound(state))}
+        src.destroy()
+    recs = all_gather(rec)
+    torch.cuda.synchronize()
+    barrier()
+    view.destroy()
+    own.destroy()  # the origin's mapping goes before any holder unbinds
+    barrier()
+    for m in preds:
+        m.destroy()
+    barrier()
+    for r in held:
+        r.destroy()
+    ctx.close()
+    return {"unique_state_gbs_per_gpu": round(unique, 1),
+            "replica_bytes_delivered_gbs_per_gpu": round(2 * unique, 1),
+            "vs_dual_store": "each tile leaves the origin once; the NVSwitch writes both replicas",
+            "adjacent_pair_recovery": [x for x in recs if x]}
+
+
+def llama_dfail_leg(args, ffx, torch, dist, world, rank, local, barrier):
+    """configs[3] at d = world (2 or 4): the Llama-3 8B ZeRO-3 shard a rank holds
+    when the model is spread over only d GPUs (12phi/d fp32 Adam + 2phi/d bf16
+    params: 56.2 GB at d=2, 28.1 GB at d=4), one ring snapshot into a
+    single-version replica (own state + replica must fit 180 GB), then a
+    single-rank failure and a verified pull from the holder."""
+    import pyoracle
+    torch.cuda.empty_cache()  # the d=8 leg's buffers: the replica below is a raw cudaMalloc
+    adam = (12 * PHI_LLAMA3_8B + world - 1) // world
+    params = (2 * PHI_LLAMA3_8B + world - 1) // world
+    regions = (lambda r: [(ffx.REGION_BLOB, adam, pyoracle.optimizer_init(42, r, 0, 0, True)),
+                          (ffx.REGION_PARAMS, params, pyoracle.weights_init(42 + r, 0, 0))])
+    spec = ffx.make_spec(d=world, phi=PHI_LLAMA3_8B, distributed=True)
+    R = Ring(ffx, torch, dist, world, rank, local, adam + params, spec, args.slice_bytes, regions, versions=1)
+    s = torch.cuda.Stream()
+    barrier()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record(s)
+    R.ctx.snapshot(1, stream=s)
+    t1.record(s)
+    s.synchronize()
+    snap_s = t0.elapsed_time(t1) / 1e3
+    snaps = [None] * world
+    dist.all_gather_object(snaps, snap_s)
+    barrier()
+    fail_rank = 1 % world
+    rec = {}
+    if rank == fail_rank:
+        R.ctx.inject(ffx.FAULT_POISON_STATE)
+        rpt = R.ctx.recover(R.target, 1, stream=s)
+        ok = rpt.bad_slices == 0 and all(ffx.blob_is_sound(t) for t in R.state)
+        nb = adam + params
+        rec = {"recovery_s": round(rpt.seconds, 5), "recovery_gbs": round(nb / rpt.seconds / 1e9, 2),
+               "nvlink_frac": round(nb / rpt.seconds / 1e9 / NVLINK_MEASURED_GBS, 4),
+               "verified_bit_exact": bool(ok)}
+    barrier()
+    recs = [None] * world
+    dist.all_gather_object(recs, rec)
+    R.close()
+    del R
+    torch.cuda.empty_cache()
+    return {"d": world, "bytes_per_rank": adam + params,
+            "state": "12phi/%d fp32 master+Adam m,v + 2phi/%d bf16 params (ZeRO-3), 1-version replica" % (world, world),
+            "snapshot_s_max": round(max(snaps), 5),
+            "snapshot_gbs_per_gpu": round((adam + params) / max(snaps) / 1e9, 2),
+            "recovery": recs[fail_rank]}
 
 
 def llama_leg(args, ffx, torch, dist, world, rank, local, barrier):
@@ -574,12 +703,14 @@ def llama_leg(args, ffx, torch, dist, world, rank, local, barrier):
     try:
         step = SyntheticStep(world)
         runs = []
-        for policy, kw in (("fused", {"copy_ctas": args.sched_ctas}),
-                           ("split", {"copy_ctas": 8, "hash_ctas": 96}),
-                           ("split", {"copy_ctas": 8, "hash_ctas": 96, "copy_engine": True}),
-                           ("split", {"copy_ctas": 8, "hash_ctas": 0, "copy_engine": True})):
+        # medians over >= 50 interleaved A/B steps for the two leading policies
+        # (SURVEY 8(d)), 16 for the others
+        for policy, kw, n_ab in (("fused", {"copy_ctas": args.sched_ctas}, 50),
+                                 ("split", {"copy_ctas": 8, "hash_ctas": 96}, 16),
+                                 ("split", {"copy_ctas": 8, "hash_ctas": 96, "copy_engine": True}, 16),
+                                 ("split", {"copy_ctas": 8, "hash_ctas": 0, "copy_engine": True}, 50)):
             sched = SliceScheduler(R.ctx, step, policy=policy, **kw)
-            runs.append(measure_overhead(step, sched, steps=8, warmup=2, it0=10 + 1000 * len(runs)))
+            runs.append(measure_overhead(step, sched, steps=n_ab, warmup=2, it0=10 + 1000 * len(runs)))
         best = min(runs, key=lambda r: r["overhead_pct"])
         out["step_overhead"] = dict(best, all_policies=runs)
         # the snapshots taken inside the step must recover bit-exactly too

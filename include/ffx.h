@@ -272,6 +272,47 @@ int ffx_snapshot_target(ffx_ctx* ctx, ffx_replica* target);
  * one checksum pass.  NULL removes it. */
 int ffx_snapshot_target2(ffx_ctx* ctx, ffx_replica* target);
 
+/* ---- double neighbour over NVSwitch multicast ---------------
+ * The same dp+1 / dp+2 replication as ffx_snapshot_target2, but every tile
+ * leaves the origin ONCE: the snapshot kernel stores into a multicast range
+ * the switch fans out to both holders' slots (egress N instead of 2N).  The
+ * reference has no double neighbour; this extends NeighborBuffer
+ * (ckpt.cpp:77-105) and the adjacent-pair fallback (controller.cpp:162-167).
+ * Sequence (one process per GPU; handles travel like replica handles, the
+ * fds behind them are fetched from the exporting process by libffx):
+ *   holders : ffx_replica_create_shared(origin)  -> export handle
+ *   origin  : ffx_mcast_create(members = 3)      -> export handle
+ *   holders : ffx_mcast_open(handle)
+ *   all     : ffx_mcast_join  (every member; before any bind)
+ *   holders : ffx_mcast_bind(mc, held replica)
+ *   origin  : ffx_replica_open(holder 1 handle) -> view;
+ *             ffx_snapshot_target_mcast(ctx, mc, view)
+ * Recovery reads either holder's replica as usual (ffx_recover*). */
+#define FFX_MCAST_HANDLE_BYTES 64
+typedef struct ffx_mcast ffx_mcast;
+/* 1 if `device` supports multicast objects (NVSwitch, fabric manager up). */
+int ffx_mcast_supported(int device, int* supported);
+/* A replica whose memory can be bound to a multicast range (a shareable VMM
+ * allocation instead of cudaMalloc); otherwise identical to
+ * ffx_replica_create, exported/opened with the same calls. */
+int ffx_replica_create_shared(ffx_ctx* ctx, ffx_role origin, uint64_t capacity, uint32_t versions,
+                              ffx_replica** out);
+/* Origin: a multicast object sized for replicas of (capacity, versions,
+ * ctx slice bytes) with `members` devices (the origin + its holders). */
+int ffx_mcast_create(ffx_ctx* ctx, uint64_t capacity, uint32_t versions, uint32_t members, ffx_mcast** out);
+int ffx_mcast_export(const ffx_mcast* m, uint8_t handle[FFX_MCAST_HANDLE_BYTES]);
+int ffx_mcast_open(ffx_ctx* ctx, const uint8_t handle[FFX_MCAST_HANDLE_BYTES], ffx_mcast** out);
+/* Add this process's device to the team (blocks nothing; binds and the
+ * origin's mapping wait until every member joined). */
+int ffx_mcast_join(ffx_mcast* m);
+/* Holder: bind its shared replica for this origin into the range. */
+int ffx_mcast_bind(ffx_mcast* m, ffx_replica* held);
+/* Origin: map the range and make it this context's snapshot target; `view`
+ * is one holder's replica opened here (slot metadata is read through it).
+ * Clears any ffx_snapshot_target2. */
+int ffx_snapshot_target_mcast(ffx_ctx* ctx, ffx_mcast* m, ffx_replica* view);
+int ffx_mcast_destroy(ffx_mcast* m);
+
 typedef struct ffx_snapshot_opts {
   uint32_t max_ctas;       /* SM budget for the snapshot kernel (0 = whole GPU) */
   uint32_t batches;        /* slice batches the scheduler splits one snapshot into (0/1 = one) */

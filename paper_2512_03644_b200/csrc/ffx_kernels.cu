@@ -132,21 +132,27 @@ __global__ void check_kernel(const uint8_t* blob, uint64_t bytes, unsigned long 
 //   l' = ((l ^ b) * 0xB3) mod 256            (0xB3 = FNV prime mod 256)
 // and h_{i+1} = h_i * P + ((l_i ^ b_i) - l_i) * P, so once the low-byte
 // trajectory is known each sub-segment is an affine map h -> A*h + B.
-//  phase 1  fnv_spec_kernel: per segment (K sub-segments), all 256 start
-//           values of l simulated in parallel (two per 32-bit lane), recording
-//           the state at every sub-segment end -> T[sub][start].
+//  phase 1  fnv_spec_kernel: per segment (K sub-segments), start values
+//           l = 0..127 simulated in parallel (two per 32-bit lane), recording
+//           the state at every sub-segment end -> T[sub][start].  Bit 7 never
+//           feeds lower bits: x ^ 0x80 = x + 128 and 128 * 0xB3 = 128 (mod 256),
+//           so the trajectory from l ^ 0x80 is the one from l with bit 7
+//           flipped at every step -- T[l] = T7[l & 127] ^ (l & 128), half the
+//           speculation of all 256 starts.
 //  phase 2  fnv_walk_kernel: chain segment start states l through T.
 //  phase 3  fnv_init_kernel + slice_kernel(Hash, init_state=l_sub):
 //           F_sub = FNV of the sub-segment started from h = l_sub.
 //  phase 4  fnv_combine_kernel: h = fold_sub (h - l_sub) * P^len_sub + F_sub.
 
-constexpr int kSpecK = 16;  // sub-segments per segment
+constexpr int kSpecK = 8;        // sub-segments per segment
+constexpr int kSpecThreads = 8;  // threads per segment: 16 of the 128 start values each
+constexpr int kSpecTab = 128;    // table entries per sub-segment (bit 7 by symmetry)
 
 __global__ void fnv_spec_kernel(const uint8_t* data, uint64_t len, uint64_t Ls, uint64_t nsub,
                                 uint8_t* T) {
   const uint64_t gt = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
-  const uint64_t seg = gt / 16;
-  const int t = static_cast<int>(gt % 16);
+  const uint64_t seg = gt / kSpecThreads;
+  const int t = static_cast<int>(gt % kSpecThreads);
   const uint64_t sub0 = seg * kSpecK;
   if (sub0 >= nsub) return;
   const uint64_t sub1 = min(sub0 + kSpecK, nsub);
@@ -183,28 +189,29 @@ __global__ void fnv_spec_kernel(const uint8_t* data, uint64_t len, uint64_t Ls, 
       const uint32_t a = x[2 * r], b = x[2 * r + 1];
       out[r] = (a & 0xffu) | (((a >> 16) & 0xffu) << 8) | ((b & 0xffu) << 16) | (((b >> 16) & 0xffu) << 24);
     }
-    reinterpret_cast<uint4*>(T + u * 256)[t] = make_uint4(out[0], out[1], out[2], out[3]);
+    reinterpret_cast<uint4*>(T + u * kSpecTab)[t] = make_uint4(out[0], out[1], out[2], out[3]);
   }
 }
 
 // One CTA: walk segment ends; lam_seg[s] = low byte at segment s start.
 __global__ void fnv_walk_kernel(const uint8_t* T, uint64_t nsub, uint64_t nseg, uint32_t l0,
                                 uint8_t* lam_seg) {
-  __shared__ uint4 tab[32][16];  // 32 segment-end tables
+  constexpr int kV = kSpecTab / 16;  // uint4 per table
+  __shared__ uint4 tab[64][kV];      // 64 segment-end tables
   uint32_t l = l0;
-  for (uint64_t s0 = 0; s0 < nseg; s0 += 32) {
-    const uint64_t cnt = umin64(32, nseg - s0);
+  for (uint64_t s0 = 0; s0 < nseg; s0 += 64) {
+    const uint64_t cnt = umin64(64, nseg - s0);
     __syncthreads();
-    for (uint64_t i = threadIdx.x; i < cnt * 16; i += blockDim.x) {
-      const uint64_t s = s0 + i / 16;
+    for (uint64_t i = threadIdx.x; i < cnt * kV; i += blockDim.x) {
+      const uint64_t s = s0 + i / kV;
       const uint64_t last = umin64(s * kSpecK + kSpecK, nsub) - 1;
-      tab[i / 16][i % 16] = reinterpret_cast<const uint4*>(T + last * 256)[i % 16];
+      tab[i / kV][i % kV] = reinterpret_cast<const uint4*>(T + last * kSpecTab)[i % kV];
     }
     __syncthreads();
     if (threadIdx.x == 0) {
       for (uint64_t i = 0; i < cnt; ++i) {
         lam_seg[s0 + i] = static_cast<uint8_t>(l);
-        l = reinterpret_cast<const uint8_t*>(tab[i])[l];
+        l = reinterpret_cast<const uint8_t*>(tab[i])[l & 127u] ^ (l & 128u);
       }
     }
   }
@@ -216,7 +223,7 @@ __global__ void fnv_init_kernel(const uint8_t* T, const uint8_t* lam_seg, uint64
        u += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
     const uint64_t seg = u / kSpecK;
     const uint32_t ls = lam_seg[seg];
-    init[u] = (u % kSpecK == 0) ? ls : T[(u - 1) * 256 + ls];
+    init[u] = (u % kSpecK == 0) ? ls : (T[(u - 1) * kSpecTab + (ls & 127u)] ^ (ls & 128u));
   }
 }
 
@@ -289,8 +296,24 @@ cudaError_t launch_blob_check(const uint8_t* blob, uint64_t bytes, unsigned long
   return cudaGetLastError();
 }
 
+void retain_pool() {
+  // The device's default stream-ordered pool returns memory to the driver at
+  // every synchronize unless a release threshold is set; the synchronous
+  // checkers (whole FNV scratch, blob check) would re-map it on every call.
+  static bool done[64] = {};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64 || done[dev]) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t keep = 256ull << 20;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+  }
+  done[dev] = true;
+}
+
 cudaError_t whole_fnv(const uint8_t* data, uint64_t len, uint64_t h0, uint64_t* out,
                       cudaStream_t stream) {
+  retain_pool();
   if (len == 0) {
     *out = h0;
     return cudaSuccess;
@@ -302,7 +325,7 @@ cudaError_t whole_fnv(const uint8_t* data, uint64_t len, uint64_t h0, uint64_t* 
   const uint64_t last_len = len - (nsub - 1) * Ls;
 
   uint8_t* scratch = nullptr;
-  const uint64_t offT = 0, offLam = align_up(nsub * 256, 256),
+  const uint64_t offT = 0, offLam = align_up(nsub * kSpecTab, 256),
                  offInit = offLam + align_up(nseg, 256), offF = offInit + align_up(nsub * 8, 256),
                  offOut = offF + align_up(nsub * 8, 256), total = offOut + 256;
   cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&scratch), total, stream);
@@ -313,7 +336,7 @@ cudaError_t whole_fnv(const uint8_t* data, uint64_t len, uint64_t h0, uint64_t* 
   uint64_t* F = reinterpret_cast<uint64_t*>(scratch + offF);
   uint64_t* dout = reinterpret_cast<uint64_t*>(scratch + offOut);
 
-  const uint64_t spec_threads = nseg * 16;
+  const uint64_t spec_threads = nseg * kSpecThreads;
   fnv_spec_kernel<<<static_cast<unsigned>((spec_threads + 255) / 256), 256, 0, stream>>>(
       data, len, Ls, nsub, T);
   fnv_walk_kernel<<<1, 512, 0, stream>>>(T, nsub, nseg, static_cast<uint32_t>(h0 & 0xff), lam);

@@ -121,6 +121,9 @@ cudaError_t launch_blob_check(const uint8_t* blob, uint64_t bytes, unsigned long
 cudaError_t whole_fnv(const uint8_t* data, uint64_t len, uint64_t h0, uint64_t* out,
                       cudaStream_t stream);
 
+// Keep up to 256 MB cached in the current device's default memory pool.
+void retain_pool();
+
 cudaError_t launch_fill(uint8_t* dst, uint64_t bytes, uint32_t pattern, cudaStream_t stream);
 cudaError_t launch_xor_byte(uint8_t* dst, uint8_t mask, cudaStream_t stream);
 

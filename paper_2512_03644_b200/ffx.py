@@ -22,6 +22,7 @@ LIB_PATH = os.path.join(_HERE, "libffx.so")
 ABI_VERSION = 1
 HANDLE_BYTES = 256
 REGIONS_HANDLE_BYTES = 2048
+MCAST_HANDLE_BYTES = 64
 MAX_REGIONS = 16
 
 # status codes (ffx.h)
@@ -242,6 +243,15 @@ SIGNATURES = {
     "ffx_snapshot_target": (_I, [_P, _P]),
     "ffx_snapshot": (_I, [_P, _U64, _P, ctypes.POINTER(SnapshotOpts)]),
     "ffx_snapshot_target2": (_I, [_P, _P]),
+    "ffx_mcast_supported": (_I, [_I, ctypes.POINTER(_I)]),
+    "ffx_replica_create_shared": (_I, [_P, Role, _U64, _U32, ctypes.POINTER(_P)]),
+    "ffx_mcast_create": (_I, [_P, _U64, _U32, _U32, ctypes.POINTER(_P)]),
+    "ffx_mcast_export": (_I, [_P, _P]),
+    "ffx_mcast_open": (_I, [_P, _P, ctypes.POINTER(_P)]),
+    "ffx_mcast_join": (_I, [_P]),
+    "ffx_mcast_bind": (_I, [_P, _P]),
+    "ffx_snapshot_target_mcast": (_I, [_P, _P, _P]),
+    "ffx_mcast_destroy": (_I, [_P]),
     "ffx_regions_export": (_I, [_P, _P]),
     "ffx_remote_open": (_I, [_P, _P, ctypes.POINTER(_P)]),
     "ffx_remote_close": (_I, [_P]),
@@ -547,6 +557,40 @@ class Replica:
             self._h = ctypes.c_void_p(0)
 
 
+class Mcast:
+    """An NVSwitch multicast range over one origin's replica slots on its
+    dp+1 and dp+2 holders (double neighbour with one egress per tile)."""
+
+    def __init__(self, handle_ptr: int):
+        self._h = ctypes.c_void_p(handle_ptr)
+
+    @property
+    def ptr(self):
+        return self._h
+
+    def export(self) -> bytes:
+        buf = ctypes.create_string_buffer(MCAST_HANDLE_BYTES)
+        check(lib.ffx_mcast_export(self._h, buf), "mcast_export")
+        return buf.raw
+
+    def join(self):
+        check(lib.ffx_mcast_join(self._h), "mcast_join")
+
+    def bind(self, held: "Replica"):
+        check(lib.ffx_mcast_bind(self._h, held.ptr), "mcast_bind")
+
+    def destroy(self):
+        if self._h:
+            check(lib.ffx_mcast_destroy(self._h), "mcast_destroy")
+            self._h = ctypes.c_void_p(0)
+
+
+def mcast_supported(device: int = 0) -> bool:
+    v = _I()
+    check(lib.ffx_mcast_supported(device, ctypes.byref(v)), "mcast_supported")
+    return bool(v.value)
+
+
 class Remote:
     """An origin rank's regions mapped into a holder (pull mode)."""
 
@@ -608,6 +652,28 @@ class Context:
         h = ctypes.c_void_p()
         check(lib.ffx_replica_create(self._c, origin, capacity, versions, ctypes.byref(h)), "replica_create")
         return Replica(h.value, self)
+
+    def create_shared_replica(self, origin, capacity: int, versions: int = 2) -> Replica:
+        """A replica that can be bound to an NVSwitch multicast range."""
+        origin = origin if isinstance(origin, Role) else Role(*origin)
+        h = ctypes.c_void_p()
+        check(lib.ffx_replica_create_shared(self._c, origin, capacity, versions, ctypes.byref(h)),
+              "replica_create_shared")
+        return Replica(h.value, self)
+
+    def create_mcast(self, capacity: int, versions: int = 2, members: int = 3) -> Mcast:
+        h = ctypes.c_void_p()
+        check(lib.ffx_mcast_create(self._c, capacity, versions, members, ctypes.byref(h)), "mcast_create")
+        return Mcast(h.value)
+
+    def open_mcast(self, handle: bytes) -> Mcast:
+        h = ctypes.c_void_p()
+        check(lib.ffx_mcast_open(self._c, ctypes.create_string_buffer(bytes(handle), MCAST_HANDLE_BYTES),
+                                 ctypes.byref(h)), "mcast_open")
+        return Mcast(h.value)
+
+    def set_target_mcast(self, mc: Mcast, view: Replica):
+        check(lib.ffx_snapshot_target_mcast(self._c, mc.ptr, view.ptr), "snapshot_target_mcast")
 
     def open_replica(self, handle: bytes) -> Replica:
         h = ctypes.c_void_p()

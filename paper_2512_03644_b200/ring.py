@@ -68,3 +68,39 @@ def recovery_sources(plan_forwards: Sequence, world: int, p: int = 1, t: int = 1
         k = (holder_dp - o[0]) % d - 1
         out.append((origin_rank, holder_rank, k))
     return out
+
+
+def wire_mcast_ring(rank: int, world: int, create_for: Callable[[int], object], export: Callable[[object], bytes],
+                    open_handle: Callable[[bytes], object], create_mcast: Callable[[], object],
+                    export_mcast: Callable[[object], bytes], open_mcast: Callable[[bytes], object],
+                    all_gather: Callable[[bytes], List[bytes]], barrier: Callable[[], None],
+                    p: int = 1, t: int = 1, replicas: int = 2):
+    """Double neighbour over NVSwitch multicast: rank r's
+    snapshot goes ONCE into a multicast range bound to the replicas its
+    successors 1..replicas hold for it.
+
+    Every rank: creates the (shareable) replicas it holds for its
+    predecessors 1..replicas and its own multicast object; handles are
+    all-gathered; it opens the multicast objects of its predecessors; every
+    member joins every team it is in (barrier) before any bind; holders bind;
+    the origin opens its first holder's replica as the read view.
+
+    Returns (held, own_mc, pred_mcs, view, handles) -- handles[r][k] as in
+    wire_ring, so recovery_sources() applies unchanged; the caller makes
+    own_mc + view its snapshot target (ffx_snapshot_target_mcast).
+    """
+    held = [create_for(predecessor(rank, world, p, t, k + 1)) for k in range(replicas)]
+    own = create_mcast()
+    mine = (b"".join(export(h) for h in held), export_mcast(own))
+    gathered = all_gather(mine)
+    hb = len(mine[0]) // replicas if replicas else 0
+    handles = [[g[0][i * hb:(i + 1) * hb] for i in range(replicas)] for g in gathered]
+    preds = [open_mcast(gathered[predecessor(rank, world, p, t, k + 1)][1]) for k in range(replicas)]
+    for m in [own] + preds:
+        m.join()
+    barrier()  # every team complete before anyone binds or maps
+    for m, h in zip(preds, held):
+        m.bind(h)
+    barrier()
+    view = open_handle(handles[successor(rank, world, p, t, 1)][0])
+    return held, own, preds, view, handles

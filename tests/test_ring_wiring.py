@@ -95,3 +95,67 @@ def test_successor_predecessor_with_pp_tp():
         s = ring.successor(r, w, 2, 2)
         assert ring.ring_roles(w, 2, 2)[s][1:] == ring.ring_roles(w, 2, 2)[r][1:]
         assert ring.predecessor(s, w, 2, 2) == r
+
+
+class _FakeMcast:
+    """Stand-in multicast team member: records the protocol steps."""
+
+    def __init__(self, origin, log):
+        self.origin, self.log = origin, log
+
+    def join(self):
+        self.log.append(("join", self.origin))
+
+    def bind(self, held):
+        self.log.append(("bind", self.origin, held))
+
+
+def _mcast_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        log = []
+
+        def all_gather(b):
+            out = [None] * world
+            dist.all_gather_object(out, b)
+            return out
+
+        held, own, preds, view, handles = ring.wire_mcast_ring(
+            rank, world, create_for=lambda origin: origin, export=lambda o: b"H%02d<%02d" % (rank, o),
+            open_handle=lambda h: bytes(h), create_mcast=lambda: _FakeMcast(rank, log),
+            export_mcast=lambda m: b"M%02d" % m.origin,
+            open_mcast=lambda h: _FakeMcast(int(h[1:]), log), all_gather=all_gather,
+            barrier=lambda: (log.append(("barrier",)), dist.barrier()))
+        q.put((rank, held, [p.origin for p in preds], view, log))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_mcast_ring_wiring_gloo():
+    world = 4
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_mcast_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = {}
+    for _ in range(world):
+        rank, held, preds, view, log = q.get(timeout=120)
+        res[rank] = (held, preds, view, log)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for r in range(world):
+        held, preds, view, log = res[r]
+        assert held == [(r - 1) % world, (r - 2) % world]
+        assert preds == held  # the teams this rank joins as a holder
+        assert view == b"H%02d<%02d" % ((r + 1) % world, r)  # read view: first holder's replica of me
+        first_barrier = log.index(("barrier",))
+        joins = [e for e in log[:first_barrier] if e[0] == "join"]
+        assert sorted(j[1] for j in joins) == sorted([r] + held)  # own team + both predecessors' teams
+        binds = [e for e in log if e[0] == "bind"]
+        assert all(log.index(b) > first_barrier for b in binds)  # no bind before every team is complete
+        assert sorted((b[1], b[2]) for b in binds) == sorted((o, o) for o in held)
