@@ -237,6 +237,77 @@ void orc_state_next(const char* tag, const uint8_t* state, const uint8_t* grad, 
   orc_sha256(b, o, out);
 }
 
+/* ---- per-iteration state evolution (SURVEY 8(d) synthetic inputs) --------
+ * The optimizer digest of a rank at iteration n:
+ *   d_0 = optimizer_init(seed, role)                       evolution.cpp:26-31
+ *   d_n = optimizer_next(d_{n-1}, grad_digest(grad_contribution(seed, role, n,
+ *           window_fold(seed, window_of(assign, column, n)))))
+ * optimizer_next :38-41, grad_contribution :50-62, grad_digest :64-69,
+ * data_item_digest / data_item / item_fold :112-128 (8-byte items),
+ * window_of dataloader.cpp:36-49, window_fold :166-171, the assignment
+ * controller.cpp:127-140 (start 0: per_column = batch/world, base 0);
+ * column = the rank's global index (domain.cpp:18-30). */
+
+/* item_fold(data_item(seed, index, 8)) = the first expand() word of the item digest */
+uint64_t orc_item_fold(uint64_t data_seed, uint64_t index) {
+  uint8_t b[32], d[32];
+  size_t o = put_str(b, "D");
+  le64(b + o, data_seed); o += 8;
+  le64(b + o, index); o += 8;
+  orc_sha256(b, o, d);
+  return orc_mix64(orc_fold64(d) + ORC_GOLDEN);
+}
+
+uint64_t orc_window_fold(uint64_t seed, uint64_t first, uint32_t count) {
+  uint64_t acc = 0;
+  for (uint32_t i = 0; i < count; ++i) acc += orc_item_fold(seed, first + i);
+  return acc;
+}
+
+void orc_grad_contribution(uint64_t seed, uint16_t dp, uint16_t pp, uint16_t tp, uint64_t iteration,
+                           uint64_t data_fold, uint64_t lanes[8]) {
+  uint8_t b[64], d[32];
+  size_t o = put_str(b, "C");
+  le64(b + o, seed); o += 8;
+  le16(b + o, dp); o += 2;
+  le16(b + o, pp); o += 2;
+  le16(b + o, tp); o += 2;
+  le64(b + o, iteration); o += 8;
+  orc_sha256(b, o, d);
+  const uint64_t base = orc_fold64(d);
+  for (int j = 0; j < 8; ++j) {
+    const uint64_t off = (uint64_t)j * ORC_GOLDEN;
+    lanes[j] = orc_mix64(base + off) + orc_mix64(data_fold + off);
+  }
+}
+
+void orc_grad_digest(const uint64_t lanes[8], uint8_t* out) {
+  uint8_t b[80];
+  size_t o = put_str(b, "G");
+  for (int j = 0; j < 8; ++j) { le64(b + o, lanes[j]); o += 8; }
+  orc_sha256(b, o, out);
+}
+
+/* d_n for rank (dp,pp,tp) of a d x p x t grid with `batch` samples. */
+int orc_optimizer_at(uint64_t seed, uint16_t dp, uint16_t pp, uint16_t tp, uint32_t d, uint32_t p,
+                     uint32_t t, uint32_t batch, uint64_t n, int distributed, uint8_t* out) {
+  const uint32_t world = d * p * t;
+  if (world == 0 || batch % world != 0) return -1;  /* controller.cpp:131-132 SetupError */
+  const uint32_t per_column = batch / world;
+  const uint32_t column = ((uint32_t)dp * p + pp) * t + tp;
+  uint8_t dig[32], g[32];
+  uint64_t lanes[8];
+  orc_optimizer_init(seed, dp, pp, tp, distributed, dig);
+  for (uint64_t it = 1; it <= n; ++it) {
+    const uint64_t first = it * (uint64_t)world * per_column + (uint64_t)column * per_column;
+    orc_grad_contribution(seed, dp, pp, tp, it, orc_window_fold(seed, first, per_column), lanes);
+    orc_grad_digest(lanes, g);
+    orc_state_next("O", dig, g, dig);
+  }
+  memcpy(out, dig, 32);
+  return 0;
+}
+
 /* Bytes [lo, lo+len) of materialize(d, total) without building the whole
  * blob (evolution.cpp:88-97 is counter-based: byte i >= 32 is byte (i-32)%8
  * of word (i-32)/8 of the expansion).  For spot checks of GB-sized state. */

@@ -17,6 +17,7 @@ Reference functions exercised (proj/ paths):
   pack_blob / unpack    src/storage.cpp:45-101
   razor / optimizer_bytes  src/ckpt.cpp:13-21, src/evolution.cpp:15-19
   version_for_target    src/ckpt.cpp:27-33
+  per-iteration evolution  src/evolution.cpp:26-69, src/dataloader.cpp:36-49, :166-171
 """
 import ctypes
 import hashlib
@@ -62,6 +63,9 @@ def load():
     lib.ref_pack_blob.argtypes = [ctypes.c_uint16, ctypes.c_uint16, ctypes.c_uint16,
                                   ctypes.c_uint64, ctypes.c_int, ctypes.c_void_p,
                                   ctypes.c_uint64, ctypes.c_void_p]
+    lib.ref_optimizer_at.restype = ctypes.c_int
+    lib.ref_optimizer_at.argtypes = [ctypes.c_uint64] + [ctypes.c_uint16] * 3 + [ctypes.c_uint32] * 4 + \
+        [ctypes.c_uint64, ctypes.c_int, ctypes.c_void_p]
     lib.ref_unpack_ok.restype = ctypes.c_int
     lib.ref_unpack_ok.argtypes = [ctypes.c_void_p, ctypes.c_uint64]
     del u8p
@@ -121,6 +125,18 @@ def main():
     digests["w_42_p0t0"] = w_init(lib, 42, 0, 0).hex()
     digests["w_1_p1t0"] = w_init(lib, 1, 1, 0).hex()
     g["digests"] = digests
+
+    # Per-iteration optimizer digests: GPT-2 small d=2 ranks over
+    # iterations 0..10 (configs[0]), a d=8 rank, a p x t grid, a shared optimizer.
+    evolution = []
+    for (dp, pp, tp, d, p, t, batch, n, dist) in (
+            [(r, 0, 0, 2, 1, 1, 256, n, 1) for r in (0, 1) for n in range(11)] +
+            [(5, 0, 0, 8, 1, 1, 256, 4, 1), (1, 1, 1, 2, 2, 2, 256, 3, 1), (0, 0, 0, 2, 1, 1, 256, 2, 0)]):
+        b = buf(32)
+        assert lib.ref_optimizer_at(42, dp, pp, tp, d, p, t, batch, n, dist, b) == 0
+        evolution.append({"seed": 42, "role": [dp, pp, tp], "grid": [d, p, t], "batch": batch, "iteration": n,
+                          "distributed": dist, "digest": bytes(b).hex()})
+    g["evolution"] = evolution
 
     # Blobs: whole-payload FNV, slice tables at several slice sizes, SHA-256 of
     # the bytes (compact full-content pin), and the first/last bytes.

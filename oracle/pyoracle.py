@@ -42,6 +42,10 @@ def _load_oracle():
         "orc_optimizer_init": (None, [_u64] + [ctypes.c_uint16] * 3 + [ctypes.c_int, _P]),
         "orc_state_next": (None, [ctypes.c_char_p, _P, _P, _P]),
         "orc_materialize_range": (ctypes.c_int, [_P, _u64, _u64, _u64, _P]),
+        "orc_item_fold": (_u64, [_u64, _u64]),
+        "orc_window_fold": (_u64, [_u64, _u64, ctypes.c_uint32]),
+        "orc_optimizer_at": (ctypes.c_int, [_u64] + [ctypes.c_uint16] * 3 + [ctypes.c_uint32] * 4
+                             + [_u64, ctypes.c_int, _P]),
     }
     for n, (r, a) in sig.items():
         f = getattr(lib, n)
@@ -95,6 +99,15 @@ def blob_is_sound(blob: bytes) -> bool:
 def optimizer_init(seed, dp, pp, tp, distributed=True) -> bytes:
     b = _buf(32)
     lib.orc_optimizer_init(seed, dp, pp, tp, int(distributed), b)
+    return b.raw[:32]
+
+
+def optimizer_at(seed, dp, pp, tp, n, d, p=1, t=1, batch=256, distributed=True) -> bytes:
+    """Optimizer digest of rank (dp,pp,tp) after n iterations:
+    optimizer_next over the grad digest of the rank's data window."""
+    b = _buf(32)
+    if lib.orc_optimizer_at(seed, dp, pp, tp, d, p, t, batch, n, int(distributed), b) != 0:
+        raise ValueError("batch size must divide evenly over the workers")
     return b.raw[:32]
 
 
@@ -159,6 +172,8 @@ def ref_lib():
     r.ref_ring_run.argtypes = [_P, _u64, ctypes.POINTER(ctypes.c_double)]
     r.ref_ring_free.argtypes = [_P]
     r.ref_optimizer_init.argtypes = [_u64, ctypes.c_uint16, ctypes.c_uint16, ctypes.c_uint16, ctypes.c_int, _P]
+    r.ref_optimizer_at.restype = ctypes.c_int
+    r.ref_optimizer_at.argtypes = [_u64] + [ctypes.c_uint16] * 3 + [ctypes.c_uint32] * 4 + [_u64, ctypes.c_int, _P]
     return r
 
 

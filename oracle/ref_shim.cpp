@@ -14,6 +14,7 @@
 #include <vector>
 
 #include "ftsim/ckpt.hpp"
+#include "ftsim/dataloader.hpp"
 #include "ftsim/evolution.hpp"
 #include "ftsim/hash.hpp"
 #include "ftsim/storage.hpp"
@@ -28,6 +29,32 @@ void ref_optimizer_init(std::uint64_t seed, std::uint16_t dp, std::uint16_t pp,
                         std::uint16_t tp, int distributed, std::uint8_t* out) {
   const auto d = evo::optimizer_init(seed, Role{dp, pp, tp}, distributed != 0);
   std::memcpy(out, d.data(), 32);
+}
+
+// The rank's optimizer digest after n iterations, through the reference's
+// own evolution + data-window functions (evolution.cpp:26-69,
+// dataloader.cpp:36-49, :166-171); the assignment restates
+// controller.cpp:127-140 (that file drags in the network stack).
+int ref_optimizer_at(std::uint64_t seed, std::uint16_t dp, std::uint16_t pp, std::uint16_t tp, std::uint32_t d,
+                     std::uint32_t p, std::uint32_t t, std::uint32_t batch, std::uint64_t n, int distributed,
+                     std::uint8_t* out) {
+  const std::uint32_t world = d * p * t;
+  if (world == 0 || batch % world != 0) return -1;
+  wire::IndexAssign a;
+  a.start_iteration = 0;
+  a.per_column = batch / world;
+  a.columns = world;
+  a.base_index = 0;
+  const Role r{dp, pp, tp};
+  const std::uint32_t column = (static_cast<std::uint32_t>(dp) * p + pp) * t + tp;
+  auto dig = evo::optimizer_init(seed, r, distributed != 0);
+  for (std::uint64_t it = 1; it <= n; ++it) {
+    const auto w = data::window_of(a, column, it);
+    const auto lanes = evo::grad_contribution(seed, r, it, data::window_fold(seed, w));
+    dig = evo::optimizer_next(dig, evo::grad_digest(lanes));
+  }
+  std::memcpy(out, dig.data(), 32);
+  return 0;
 }
 
 void ref_weights_init(std::uint64_t seed, std::uint16_t pp, std::uint16_t tp, std::uint8_t* out) {

@@ -149,3 +149,20 @@ def ctypes_digest(ref, seed, dp):
     b = ctypes.create_string_buffer(32)
     ref.ref_optimizer_init(seed, dp, 0, 0, 1, b)
     return b.raw[:32]
+
+
+@pytest.mark.parametrize("e", GOLDEN["evolution"],
+                         ids=lambda e: "r%s-g%s-it%d" % ("".join(map(str, e["role"])), "".join(map(str, e["grid"])),
+                                                         e["iteration"]))
+def test_evolution_golden(e):
+    # optimizer_init -> optimizer_next(grad_digest(grad_contribution(window_fold)))
+    # per iteration, pinned to the reference's own functions (gen_golden.py)
+    dp, pp, tp = e["role"]
+    d, p, t = e["grid"]
+    assert orc.optimizer_at(e["seed"], dp, pp, tp, e["iteration"], d, p, t, e["batch"],
+                            bool(e["distributed"])).hex() == e["digest"]
+
+
+def test_evolution_uneven_batch_is_refused():
+    with pytest.raises(ValueError):
+        orc.optimizer_at(42, 0, 0, 0, 1, 3, batch=256)  # controller.cpp:131-132
