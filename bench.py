@@ -66,9 +66,10 @@ def parse():
     ap.add_argument("--no-70b", action="store_true", help="skip the 70B double-neighbour leg (N >= 3)")
     ap.add_argument("--prefix-70b", type=int, default=16 << 30, help="70B state prefix per rank (bytes)")
     ap.add_argument("--no-mcast", action="store_true", help="skip the NVSwitch-multicast double neighbour")
-    ap.add_argument("--mode", default="push", choices=["push", "pull"],
-                    help="N>1 ring stream: origin pushes into its successor's replica, or the holder "
-                         "pulls its predecessor's regions (NeighborBuffer::store side)")
+    ap.add_argument("--mode", default="push", choices=["push", "pull", "ce"],
+                    help="N>1 ring stream: origin pushes into its successor's replica (fused kernel), the holder "
+                         "pulls its predecessor's regions (NeighborBuffer::store side), or ce: copy engines + "
+                         "a concurrent checksum kernel (split policy)")
     return ap.parse_args()
 
 
@@ -207,7 +208,7 @@ class Ring:
     def __init__(self, ffx, torch, dist, world, rank, local, n, spec, slice_bytes, regions, versions=2):
         from paper_2512_03644_b200 import ring
         import pyoracle
-        self.ffx, self.n = ffx, n
+        self.ffx, self.n, self.torch, self.side = ffx, n, torch, None
         self.ctx = ffx.Context(local, spec, ffx.Role(rank, 0, 0), slice_bytes)
         self.holder = None
         if world == 1:
@@ -243,6 +244,19 @@ class Ring:
     def snapshot(self, it, stream, mode, max_ctas=0):
         if mode == "pull" and self.remote is not None:
             self.ctx.snapshot_pull(self.remote, self.held, it, stream=stream, max_ctas=max_ctas)
+        elif mode == "ce":
+            # split policy, unscheduled: the copy engines move the bytes on a
+            # side stream while the checksum kernel hashes the local state;
+            # the hash batch joins the copy and commits on `stream`
+            torch = self.torch
+            if self.side is None:
+                self.side = torch.cuda.Stream()
+            ev = torch.cuda.Event()
+            ev.record(stream)
+            self.side.wait_event(ev)
+            self.ctx.snapshot_begin(it, split=True, copy_engine=True, max_ctas=max_ctas)
+            self.ctx.snapshot_next(stream=self.side, kind=self.ffx.BATCH_COPY)
+            self.ctx.snapshot_next(stream=stream, kind=self.ffx.BATCH_HASH)
         else:
             self.ctx.snapshot(it, stream=stream, max_ctas=max_ctas)
 
@@ -333,22 +347,27 @@ def main():
     value = world * n * args.steps / (ms_max * 1e-3) / 1e9
     commit_ok = R.target.newest() == it
 
-    # the other ring-stream mode on the same buffers, for comparison
+    # the other ring-stream modes on the same buffers, for comparison
     alt = None
     if world > 1:
-        other = "push" if args.mode == "pull" else "pull"
-        barrier()
-        torch.cuda.synchronize()
-        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a0.record(stream)
-        for _ in range(args.steps):
-            it += 1
-            R.snapshot(it, stream, other, args.max_ctas)
-        a1.record(stream)
-        stream.synchronize()
-        barrier()
-        ams = max_over_ranks(a0.elapsed_time(a1))
-        alt = {"mode": other, "per_gpu_gbs": round(n * args.steps / (ams * 1e-3) / 1e9, 2)}
+        alt = []
+        for other in [m for m in ("push", "pull", "ce") if m != args.mode]:
+            barrier()
+            torch.cuda.synchronize()
+            for _ in range(2):
+                it += 1
+                R.snapshot(it, stream, other, args.max_ctas)
+            a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a0.record(stream)
+            for _ in range(args.steps):
+                it += 1
+                R.snapshot(it, stream, other, args.max_ctas)
+            a1.record(stream)
+            stream.synchronize()
+            barrier()
+            ams = max_over_ranks(a0.elapsed_time(a1))
+            alt.append({"mode": other, "per_gpu_gbs": round(n * args.steps / (ams * 1e-3) / 1e9, 2),
+                        "committed": R.target.newest() == it})
 
     # ---- recovery: rank (1 % world) loses its state and pulls it back --------
     fail_rank = 1 % world
