@@ -374,10 +374,18 @@ def main():
     rec = {}
     barrier()
     if rank == fail_rank:
-        R.ctx.inject(ffx.FAULT_POISON_STATE)
-        rpt = R.ctx.recover(R.target, it, stream=stream)
-        rec = {"recovery_s": rpt.seconds, "recovery_gbs": round(n / rpt.seconds / 1e9, 2),
-               "recovery_verified": bool(ffx.blob_is_sound(R.state[0]) and rpt.bad_slices == 0),
+        # three independent failures of the same rank (state poisoned each
+        # time, every restore verified); the median is reported
+        runs, ok = [], True
+        for _ in range(3):
+            R.ctx.inject(ffx.FAULT_POISON_STATE)
+            rpt = R.ctx.recover(R.target, it, stream=stream)
+            ok = ok and rpt.bad_slices == 0 and ffx.blob_is_sound(R.state[0])
+            runs.append(rpt.seconds)
+        t_rec = sorted(runs)[1]
+        rec = {"recovery_s": t_rec, "recovery_gbs": round(n / t_rec / 1e9, 2),
+               "recovery_runs_s": [round(x, 6) for x in runs],
+               "recovery_verified": bool(ok),
                "source": "local replica" if world == 1 else "ring successor over NVLink"}
     barrier()
     if world > 1:
