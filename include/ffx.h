@@ -261,6 +261,14 @@ int ffx_replica_clear(ffx_replica* r);
  * FFX_EINVAL when the payload exceeds the 4 GiB SNP1 limit (storage.cpp:48). */
 int ffx_replica_export_frame(ffx_replica* r, uint64_t iteration, void* host_dst, uint64_t cap,
                              uint64_t* framed_len, void* stream);
+/* The same for payloads of any size: part `part` of *parts SNP1 frames, each
+ * carrying FFX_FRAME_PART_BYTES (the last one the rest) of the concatenated
+ * regions with its own length and whole-payload FNV -- the split a caller of
+ * pack_blob must make above its 4 GiB limit (storage.cpp:48-49).  host_dst
+ * NULL = size query (*framed_len, *parts).  FFX_ERANGE past the last part. */
+#define FFX_FRAME_PART_BYTES 0xFFFFF000ull /* 4 GiB - 4 KiB: the largest slice-aligned SNP1 payload */
+int ffx_replica_export_frame_part(ffx_replica* r, uint64_t iteration, uint32_t part, void* host_dst,
+                                  uint64_t cap, uint64_t* framed_len, uint32_t* parts, void* stream);
 
 /* ---- snapshot (HostSnapshots::take + ring stream, ckpt.cpp:38-53) --------- */
 

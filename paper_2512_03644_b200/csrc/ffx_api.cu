@@ -1033,6 +1033,58 @@ extern "C" int ffx_replica_export_frame(ffx_replica* r, uint64_t iteration, void
   return FFX_OK;
 }
 
+// Payloads above the SNP1 length field (storage.cpp:48-49 throws) leave as
+// several frames: part i carries logical payload bytes
+// [i*FFX_FRAME_PART_BYTES, ...) of the concatenated regions, with its own
+// header (same role / iteration / kind, the part's length and FNV).
+extern "C" int ffx_replica_export_frame_part(ffx_replica* r, uint64_t iteration, uint32_t part, void* host_dst,
+                                             uint64_t cap, uint64_t* framed_len, uint32_t* parts, void* stream) {
+  if (!r || !framed_len) return fail(FFX_EINVAL, "export_frame_part: null argument");
+  DeviceGuard g(r->ctx ? r->ctx->device : r->device);
+  SlotMeta m;
+  const int v = find_slot(r, iteration, &m);
+  if (v == -2) return fail(FFX_ECUDA, "export_frame_part: cannot read slot metadata: %s", g_err.c_str());
+  if (v < 0 || m.state != kSlotCommitted)
+    return fail(FFX_ERESTORE, "no committed snapshot at iteration %llu", (unsigned long long)iteration);
+  const uint64_t F = FFX_FRAME_PART_BYTES;
+  const uint32_t n_parts = m.payload_len ? static_cast<uint32_t>((m.payload_len + F - 1) / F) : 1;
+  if (parts) *parts = n_parts;
+  if (part >= n_parts) return fail(FFX_ERANGE, "export_frame_part: part %u of %u", part, n_parts);
+  const uint64_t a = static_cast<uint64_t>(part) * F;
+  const uint64_t b = std::min<uint64_t>(m.payload_len, a + F);
+  *framed_len = 32 + (b - a);
+  if (!host_dst) return FFX_OK;  // size query
+  if (cap < *framed_len) return fail(FFX_ECONFIG, "export_frame_part: buffer of %llu < %llu bytes",
+                                     (unsigned long long)cap, (unsigned long long)*framed_len);
+  cudaStream_t s = as_stream(stream);
+  const uint8_t* pay = r->payload(static_cast<uint32_t>(v));
+  // the logical range [a, b) as pieces of the (256-byte aligned) regions
+  struct Piece { const uint8_t* p; uint64_t n; };
+  std::vector<Piece> pieces;
+  uint64_t phys = 0, logical = 0;
+  for (uint32_t i = 0; i < m.num_regions; ++i) {
+    const uint64_t lo = std::max(a, logical), hi = std::min(b, logical + m.region_bytes[i]);
+    if (lo < hi) pieces.push_back(Piece{pay + phys + (lo - logical), hi - lo});
+    logical += m.region_bytes[i];
+    phys = align_up(phys + m.region_bytes[i], kRegionAlign);
+  }
+  uint64_t h = kFnvBasis;
+  for (const Piece& pc : pieces) {
+    cudaError_t e = whole_fnv(pc.p, pc.n, h, &h, s);
+    if (e != cudaSuccess) return cuda_fail(e, "whole_fnv");
+  }
+  uint8_t* dst = static_cast<uint8_t*>(host_dst);
+  int st = ffx_pack_header(ffx_role{m.dp, m.pp, m.tp}, m.iteration, m.kind, b - a, h, dst);
+  if (st) return st;
+  uint64_t o = 32;
+  for (const Piece& pc : pieces) {
+    FFX_CUDA(cudaMemcpyAsync(dst + o, pc.p, pc.n, cudaMemcpyDeviceToHost, s));
+    o += pc.n;
+  }
+  FFX_CUDA(cudaStreamSynchronize(s));
+  return FFX_OK;
+}
+
 // ---------------------------------------------------------------------------
 // snapshot
 

@@ -240,6 +240,8 @@ SIGNATURES = {
     "ffx_replica_slot_ptrs": (_I, [_P, _U32, ctypes.POINTER(_P), ctypes.POINTER(_P)]),
     "ffx_replica_clear": (_I, [_P]),
     "ffx_replica_export_frame": (_I, [_P, _U64, _P, _U64, ctypes.POINTER(_U64), _P]),
+    "ffx_replica_export_frame_part": (_I, [_P, _U64, _U32, _P, _U64, ctypes.POINTER(_U64),
+                                           ctypes.POINTER(_U32), _P]),
     "ffx_snapshot_target": (_I, [_P, _P]),
     "ffx_snapshot": (_I, [_P, _U64, _P, ctypes.POINTER(SnapshotOpts)]),
     "ffx_snapshot_target2": (_I, [_P, _P]),
@@ -550,6 +552,22 @@ class Replica:
         check(lib.ffx_replica_export_frame(self._h, iteration, buf, n.value, ctypes.byref(n),
                                            _stream_ptr(stream)), "export_frame")
         return buf.raw
+
+    def export_frame_parts(self, iteration: int, stream=None):
+        """Every SNP1 frame of the snapshot at `iteration` (several above the
+        4 GiB SNP1 limit), as bytes objects."""
+        n, parts = ctypes.c_uint64(), ctypes.c_uint32()
+        check(lib.ffx_replica_export_frame_part(self._h, iteration, 0, None, 0, ctypes.byref(n),
+                                                ctypes.byref(parts), _stream_ptr(stream)), "export_frame_part")
+        out = []
+        for i in range(parts.value):
+            check(lib.ffx_replica_export_frame_part(self._h, iteration, i, None, 0, ctypes.byref(n), None,
+                                                    _stream_ptr(stream)), "export_frame_part")
+            buf = ctypes.create_string_buffer(n.value)
+            check(lib.ffx_replica_export_frame_part(self._h, iteration, i, buf, n.value, ctypes.byref(n), None,
+                                                    _stream_ptr(stream)), "export_frame_part")
+            out.append(buf.raw)
+        return out
 
     def destroy(self):
         if self._h:
