@@ -64,6 +64,8 @@ struct SliceJob {
   unsigned int* sched;            // [next task, CTAs done]: dynamic scheduling
                                   // (zero between launches; null = static)
   uint32_t proxy_fence;           // tensor path: generic->async proxy fence before each refill
+  uint32_t stagger_ns;            // start-up de-phasing: warp w sleeps (w % 8) * stagger_ns first
+  uint32_t pad2_;
   SlotCommit commit;
   SlotCommit commit2;             // second replica's slot (slot null = none)
 };

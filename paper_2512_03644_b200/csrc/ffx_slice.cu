@@ -236,6 +236,7 @@ __global__ void __launch_bounds__(W * 32) slice_kernel(const __grid_constant__ S
   }
 
   const uint64_t Sl = job.slice_bytes;
+  if (job.stagger_ns) __nanosleep(((blockIdx.x * W + warp) & 7u) * job.stagger_ns);
   uint64_t g_next = job.group_lo + static_cast<uint64_t>(blockIdx.x) * W + warp;
   const uint64_t g_stride = static_cast<uint64_t>(gridDim.x) * W;
   for (;;) {
@@ -607,6 +608,11 @@ cudaError_t launch_slices(const SliceJob& job_in, SliceMode mode, bool commit, u
   // generic writes read by the async proxy (kept per task, optional per step).
   static const bool fence = std::getenv("FFX_STEP_FENCE") != nullptr;
   job.proxy_fence = fence ? 1u : 0u;
+  static const uint32_t stagger = [] {
+    const char* e = std::getenv("FFX_STAGGER_NS");
+    return e ? static_cast<uint32_t>(std::strtoul(e, nullptr, 10)) : 0u;
+  }();
+  job.stagger_ns = stagger;
   switch (mode) {
     case SliceMode::Hash:
       return commit ? launch_mode<SliceMode::Hash, true>(job, max_ctas, stream)
