@@ -230,11 +230,14 @@ void finalize_copy_job(CopyJob& job) {
 }
 
 cudaError_t launch_copy(const CopyJob& job, uint32_t ctas, cudaStream_t stream) {
-  static bool attr = false;
-  if (!attr) {
+  static uint64_t set_on = 0;  // bit d: the shared-memory opt-in done on device d
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const uint64_t bit = 1ull << (dev & 63);
+  if (!(set_on & bit)) {
     cudaError_t e = cudaFuncSetAttribute(copy_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kCopySmem);
     if (e != cudaSuccess) return e;
-    attr = true;
+    set_on |= bit;
   }
   static const bool sm = std::getenv("FFX_COPY_SM") != nullptr;
   if (sm && job.chunk_lo == 0 && job.chunk_hi == job.total_chunks && job.mark.slot == nullptr) {

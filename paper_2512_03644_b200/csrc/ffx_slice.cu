@@ -440,13 +440,22 @@ template <int S, int W, int RPL, bool kStg, SliceMode M, bool kCommit, int KC = 
 cudaError_t launch_t(const SliceJob& job, uint32_t max_ctas, cudaStream_t stream) {
   auto kern = slice_kernel<S, W, RPL, KC, kStg, M, kCommit>;
   constexpr int smem = Cfg<S, W, RPL, KC>::SMEM;
+  // The dynamic shared-memory opt-in is per device: one process may drive
+  // several GPUs (single-process tests, the facade).
   static int occ = 0;
-  if (occ == 0) {
+  static uint64_t set_on = 0;  // bit d: attribute set on device d
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const uint64_t bit = 1ull << (dev & 63);
+  if (!(set_on & bit)) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, W * 32, smem);
-    if (e != cudaSuccess) return e;
-    if (occ < 1) occ = 1;
+    if (occ == 0) {
+      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, W * 32, smem);
+      if (e != cudaSuccess) return e;
+      if (occ < 1) occ = 1;
+    }
+    set_on |= bit;
   }
   const uint64_t want = (job.group_hi - job.group_lo + W - 1) / W;
   uint64_t cap = static_cast<uint64_t>(occ) * sm_count();
