@@ -66,7 +66,9 @@ def parse():
     ap.add_argument("--no-70b", action="store_true", help="skip the 70B double-neighbour leg (N >= 3)")
     ap.add_argument("--prefix-70b", type=int, default=16 << 30, help="70B state prefix per rank (bytes)")
     ap.add_argument("--no-mcast", action="store_true", help="skip the NVSwitch-multicast double neighbour")
-    ap.add_argument("--mode", default="push", choices=["push", "pull", "ce"],
+    ap.add_argument("--fused-permille", type=int, default=500,
+                    help="hybrid mode: share of the warp tasks the fused kernel pushes (the copy engines the rest)")
+    ap.add_argument("--mode", default="push", choices=["push", "pull", "ce", "hybrid"],
                     help="N>1 ring stream: origin pushes into its successor's replica (fused kernel), the holder "
                          "pulls its predecessor's regions (NeighborBuffer::store side), or ce: copy engines + "
                          "a concurrent checksum kernel (split policy)")
@@ -241,20 +243,23 @@ class Ring:
             dist.all_gather_object(exported, self.ctx.export_regions())
             self.remote = self.ctx.open_remote(exported[ring.predecessor(rank, world)])
 
-    def snapshot(self, it, stream, mode, max_ctas=0):
+    def snapshot(self, it, stream, mode, max_ctas=0, fused_permille=500):
         if mode == "pull" and self.remote is not None:
             self.ctx.snapshot_pull(self.remote, self.held, it, stream=stream, max_ctas=max_ctas)
-        elif mode == "ce":
+        elif mode in ("ce", "hybrid"):
             # split policy, unscheduled: the copy engines move the bytes on a
             # side stream while the checksum kernel hashes the local state;
-            # the hash batch joins the copy and commits on `stream`
+            # the hash batch joins the copy and commits on `stream`.  hybrid:
+            # the fused kernel pushes a share of the tasks itself (two NVLink
+            # write paths at once)
             torch = self.torch
             if self.side is None:
                 self.side = torch.cuda.Stream()
             ev = torch.cuda.Event()
             ev.record(stream)
             self.side.wait_event(ev)
-            self.ctx.snapshot_begin(it, split=True, copy_engine=True, max_ctas=max_ctas)
+            self.ctx.snapshot_begin(it, split=True, copy_engine=True, max_ctas=max_ctas,
+                                    fused_permille=fused_permille if mode == "hybrid" else 0)
             self.ctx.snapshot_next(stream=self.side, kind=self.ffx.BATCH_COPY)
             self.ctx.snapshot_next(stream=stream, kind=self.ffx.BATCH_HASH)
         else:
@@ -324,7 +329,7 @@ def main():
     it = 0
     for _ in range(args.warmup):
         it += 1
-        R.snapshot(it, stream, args.mode, args.max_ctas)
+        R.snapshot(it, stream, args.mode, args.max_ctas, args.fused_permille)
     stream.synchronize()
     launches0 = R.ctx.stats().kernel_launches
     barrier()
@@ -336,7 +341,7 @@ def main():
     e0.record(stream)
     for _ in range(args.steps):
         it += 1
-        R.snapshot(it, stream, args.mode, args.max_ctas)
+        R.snapshot(it, stream, args.mode, args.max_ctas, args.fused_permille)
     e1.record(stream)
     stream.synchronize()
     ck = clocks.stop()
@@ -351,23 +356,24 @@ def main():
     alt = None
     if world > 1:
         alt = []
-        for other in [m for m in ("push", "pull", "ce") if m != args.mode]:
+        for other in [m for m in ("push", "pull", "ce", "hybrid") if m != args.mode]:
             barrier()
             torch.cuda.synchronize()
             for _ in range(2):
                 it += 1
-                R.snapshot(it, stream, other, args.max_ctas)
+                R.snapshot(it, stream, other, args.max_ctas, args.fused_permille)
             a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a0.record(stream)
             for _ in range(args.steps):
                 it += 1
-                R.snapshot(it, stream, other, args.max_ctas)
+                R.snapshot(it, stream, other, args.max_ctas, args.fused_permille)
             a1.record(stream)
             stream.synchronize()
             barrier()
             ams = max_over_ranks(a0.elapsed_time(a1))
             alt.append({"mode": other, "per_gpu_gbs": round(n * args.steps / (ams * 1e-3) / 1e9, 2),
-                        "committed": R.target.newest() == it})
+                        "committed": R.target.newest() == it,
+                        **({"fused_permille": args.fused_permille} if other == "hybrid" else {})})
 
     # ---- recovery: rank (1 % world) loses its state and pulls it back --------
     fail_rank = 1 % world
@@ -410,7 +416,7 @@ def main():
                     f0.record(stream)
                 it += 1
                 R.state[0].copy_(host, non_blocking=True)        # take(it, host_ptr, len): H2D
-                R.snapshot(it, stream, args.mode, args.max_ctas)
+                R.snapshot(it, stream, args.mode, args.max_ctas, args.fused_permille)
                 R.ctx.read_sums(table_host, stream=stream)       # D2H of the step's result
             f1.record(stream)
         stream.synchronize()

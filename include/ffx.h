@@ -15,6 +15,9 @@
  *    `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
  *  - "dev" pointers are device (or peer-mapped) global memory on the context's
  *    device.  Region and replica pointers must be 16-byte aligned.
+ *  - Context calls run on the context's device.  The context-free device
+ *    primitives run on the device of `stream` when one is given, else on the
+ *    device owning their source pointer (one process may drive several GPUs).
  *  - Every call returns an ffx_status; ffx_last_error() gives the detail
  *    message of the last failure on the calling thread.
  *  - One ffx_ctx per rank (one process per GPU, or one thread per GPU).  Calls
@@ -336,7 +339,12 @@ typedef struct ffx_snapshot_opts {
   uint32_t hash_batches;   /* split: hash batches (0 = batches) */
   uint32_t hash_ctas;      /* split: SM budget of hash batches (0 = whole GPU) */
   uint32_t copy_engine;    /* split: copy batches by cudaMemcpyAsync (no SMs) */
-  uint32_t pad_;
+  /* split + copy_engine: the first fused_permille/1000 of the warp tasks go
+   * through the fused kernel (TMA stores to the target, checksummed on the
+   * way, issued with the first hash batch); the copy engines move only the
+   * rest.  Two NVLink write paths at once beat either alone
+   * (DESIGN.md section 6).  0 = copy engines move everything. */
+  uint32_t fused_permille;
   /* Measured gaps: relative sizes of the copy batches (`batches` entries,
    * e.g. the durations of the step's idle-link windows measured with events
    * in a calibration step).  NULL = equal batches.  Hash batches of the

@@ -290,6 +290,7 @@ SliceJob single_job(const void* src, void* dst, uint64_t len, uint64_t slice_byt
 
 extern "C" int ffx_checksum64(const void* dev, uint64_t len, uint64_t* host_out, void* stream) {
   if (!host_out || (len && !dev)) return fail(FFX_EINVAL, "checksum64: null argument");
+  DeviceGuard g(pick_device(stream, dev));
   cudaError_t e = whole_fnv(static_cast<const uint8_t*>(dev), len, kFnvBasis, host_out,
                             as_stream(stream));
   if (e != cudaSuccess) return cuda_fail(e, "whole_fnv");
@@ -301,6 +302,7 @@ extern "C" int ffx_slice_checksums(const void* dev, uint64_t len, uint64_t slice
   if (!slice_ok(slice_bytes)) return fail(FFX_EINVAL, "slice_bytes must be a multiple of 256");
   if (len == 0) return FFX_OK;
   if (!dev || !dev_out) return fail(FFX_EINVAL, "slice_checksums: null argument");
+  DeviceGuard g(pick_device(stream, dev));
   SliceJob job = single_job(dev, nullptr, len, slice_bytes);
   job.sums_out = dev_out;
   FFX_CUDA(launch_slices(job, SliceMode::Hash, false, 0, as_stream(stream)));
@@ -312,6 +314,7 @@ extern "C" int ffx_copy_checksums(void* dst, const void* src, uint64_t len, uint
   if (!slice_ok(slice_bytes)) return fail(FFX_EINVAL, "slice_bytes must be a multiple of 256");
   if (len == 0) return FFX_OK;
   if (!dst || !src) return fail(FFX_EINVAL, "copy_checksums: null argument");
+  DeviceGuard g(pick_device(stream, src));
   SliceJob job = single_job(src, dst, len, slice_bytes);
   job.sums_out = dev_out;
   FFX_CUDA(launch_slices(job, SliceMode::Copy, false, 0, as_stream(stream)));
@@ -322,6 +325,7 @@ extern "C" int ffx_copy_verify(void* dst, const void* src, uint64_t len, uint64_
                                const uint64_t* dev_expected, uint64_t* dev_result, void* stream) {
   if (!slice_ok(slice_bytes)) return fail(FFX_EINVAL, "slice_bytes must be a multiple of 256");
   if (!dev_result || !dev_expected) return fail(FFX_EINVAL, "copy_verify: null argument");
+  DeviceGuard g(pick_device(stream, dev_result));
   const unsigned long long init[2] = {~0ull, 0ull};
   FFX_CUDA(cudaMemcpyAsync(dev_result, init, sizeof init, cudaMemcpyHostToDevice, as_stream(stream)));
   if (len == 0) return FFX_OK;
@@ -336,6 +340,7 @@ extern "C" int ffx_copy_verify(void* dst, const void* src, uint64_t len, uint64_
 extern "C" int ffx_copy(void* dst, const void* src, uint64_t len, uint32_t ctas, void* stream) {
   if (len == 0) return FFX_OK;
   if (!dst || !src) return fail(FFX_EINVAL, "copy: null argument");
+  DeviceGuard g(pick_device(stream, src));
   CopyJob job{};
   job.nregions = 1;
   job.reg[0] = CopyRegion{static_cast<const uint8_t*>(src), static_cast<uint8_t*>(dst), len, 0, 0};
@@ -346,6 +351,7 @@ extern "C" int ffx_copy(void* dst, const void* src, uint64_t len, uint32_t ctas,
 
 extern "C" int ffx_expand(void* dst, const uint8_t digest[32], uint64_t bytes, void* stream) {
   if (!digest || (bytes && !dst)) return fail(FFX_EINVAL, "expand: null argument");
+  DeviceGuard g(pick_device(stream, dst));
   uint64_t fold = rd(digest, 8);
   FFX_CUDA(launch_expand(static_cast<uint8_t*>(dst), fold, bytes, nullptr, as_stream(stream)));
   return FFX_OK;
@@ -355,6 +361,7 @@ extern "C" int ffx_materialize(void* dst, const uint8_t digest[32], uint64_t byt
   if (!digest) return fail(FFX_EINVAL, "materialize: null digest");
   if (bytes < 32) return fail(FFX_EINVAL, "state blob smaller than its digest prefix");
   if (!dst) return fail(FFX_EINVAL, "materialize: null dst");
+  DeviceGuard g(pick_device(stream, dst));
   FFX_CUDA(launch_expand(static_cast<uint8_t*>(dst), rd(digest, 8), bytes, digest,
                          as_stream(stream)));
   return FFX_OK;
@@ -367,6 +374,7 @@ extern "C" int ffx_blob_check(const void* dev, uint64_t bytes, uint64_t* host_fi
     *host_first_bad = 0;
     return FFX_OK;
   }
+  DeviceGuard g(pick_device(stream, dev));
   unsigned long long* d = nullptr;
   cudaStream_t s = as_stream(stream);
   retain_pool();

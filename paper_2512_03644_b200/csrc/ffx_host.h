@@ -40,9 +40,9 @@ inline cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
 
 struct DeviceGuard {
   int prev = -1;
-  explicit DeviceGuard(int dev) {
+  explicit DeviceGuard(int dev) {  // dev < 0: leave the current device alone
     cudaGetDevice(&prev);
-    if (prev != dev) cudaSetDevice(dev);
+    if (dev >= 0 && prev != dev) cudaSetDevice(dev);
   }
   ~DeviceGuard() {
     int cur = -1;
@@ -62,11 +62,25 @@ inline uint64_t rd(const uint8_t* p, int n) {
 
 // ctx scratch words (ctx->done, 64 x u32): 0 commit counter, 4 second-replica
 // commit counter, 8-9 snapshot task counter, 12-13 verify task counter,
-// 16-17 split hash-batch task counter, 24-25 pull-mode ack (u64).
+// 16-17 split hash-batch task counter, 20-21 hybrid fused-share task
+// counter, 24-25 pull-mode ack (u64).
 constexpr uint32_t kAckWord = 24;
 
 inline bool valid_spec(const ffx_cluster_spec* s) {
   return s && s->data_parallel && s->pipeline_parallel && s->tensor_parallel && s->gpus_per_node;
+}
+
+// Device a context-free primitive runs on: the stream's device when a
+// stream is given, else the device that owns `p` (host / unknown: -1 = the
+// current device).  One process may drive several GPUs.
+inline int pick_device(void* stream, const void* p) {
+  int d = -1;
+  if (stream && cudaStreamGetDevice(static_cast<cudaStream_t>(stream), &d) == cudaSuccess) return d;
+  cudaGetLastError();
+  cudaPointerAttributes a{};
+  if (p && cudaPointerGetAttributes(&a, p) == cudaSuccess && a.type == cudaMemoryTypeDevice) return a.device;
+  cudaGetLastError();
+  return -1;
 }
 
 inline bool slice_ok(uint64_t s) { return s >= 256 && s % 256 == 0; }
@@ -154,6 +168,10 @@ struct PendingSnapshot {
   ffx_replica* tgt = nullptr;   // destination replica(s) of this snapshot
   ffx_replica* tgt2 = nullptr;
   uint32_t hbatches = 0, hnext = 0, hash_ctas = 0;
+  // hybrid (split + copy engines + fused_permille): warp tasks [0, gcut) are
+  // copied + hashed by the fused kernel (fjob), the copy engines move the rest
+  uint64_t gcut = 0;
+  SliceJob fjob{};
   std::vector<double> frac;  // cumulative batch boundaries in [0, 1] (measured-gap weights)
   uint64_t cut(uint64_t total, uint32_t b) const {
     return b >= batches ? total : static_cast<uint64_t>(static_cast<double>(total) * frac[b]);

@@ -104,6 +104,9 @@ cudaError_t launch_copy(const CopyJob& job, uint32_t ctas, cudaStream_t stream);
 // One-thread kernel writing the final meta + SNP1 header, then COMMITTED.
 cudaError_t launch_commit(const SlotCommit& c, cudaStream_t stream);
 
+// Slices per warp task of the active kernel variant (32 x slices per lane).
+int task_rows();
+
 // Fill job.reg[*].group_base / slice_base, job.total_groups and the group
 // range [0, total_groups).
 void finalize_job(SliceJob& job);

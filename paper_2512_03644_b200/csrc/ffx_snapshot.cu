@@ -186,6 +186,30 @@ int begin_impl(ffx_ctx* c, ffx_replica* t, ffx_replica* t2, const std::vector<Sr
     finalize_copy_job(cj);
     cj.mark = SlotMark{t->wslot(slot), iteration, seq};
     if (t2) cj.mark2 = SlotMark{t2->wslot(slot2), iteration, seq};
+    if (opts.fused_permille) {
+      if (!P.copy_engine) {
+        P.active = false;
+        return fail(FFX_EINVAL, "fused_permille needs copy_engine (the fused kernel shares NVLink with the DMA)");
+      }
+      // Warp tasks [0, gcut) go through the fused kernel; each region's CE
+      // range starts where its fused slices end.
+      const uint64_t G = job.total_groups;
+      P.gcut = G * std::min<uint32_t>(opts.fused_permille, 1000) / 1000;
+      const uint64_t rows = static_cast<uint64_t>(task_rows());
+      for (uint32_t i = 0; i < job.nregions; ++i) {
+        const SliceRegion& R = job.reg[i];
+        const uint64_t ns = slices_of(R.bytes, job.slice_bytes);
+        const uint64_t fs = P.gcut > R.group_base ? std::min(ns, (P.gcut - R.group_base) * rows) : 0;
+        const uint64_t fb = std::min(R.bytes, fs * job.slice_bytes);
+        CopyRegion& C = cj.reg[i];
+        C.src += fb;
+        C.dst += fb;
+        if (C.dst2) C.dst2 += fb;
+        C.bytes -= fb;
+      }
+      finalize_copy_job(cj);
+      P.fjob = job;  // copy + hash of the fused share, destinations kept
+    }
     // Hash batches: the local state hashed straight into the slot's table.
     for (uint32_t i = 0; i < job.nregions; ++i) job.reg[i].dst = nullptr;
     P.hbatches = std::max<uint32_t>(1, opts.hash_batches ? opts.hash_batches : P.batches);
@@ -403,7 +427,7 @@ int verify_landed(ffx_ctx* c, const PendingSnapshot& P, cudaStream_t s) {
   const ffx_replica* t = P.tgt;
   auto readable = [t](const uint8_t* p) { return t->wbase ? t->base + (p - t->wbase) : p; };
   for (uint32_t i = 0; i < vj.nregions; ++i) {
-    vj.reg[i].src = readable(P.split ? P.copy.reg[i].dst : vj.reg[i].dst);  // the landed payload
+    vj.reg[i].src = readable(P.gcut ? P.fjob.reg[i].dst : P.split ? P.copy.reg[i].dst : vj.reg[i].dst);  // landed payload
     vj.reg[i].dst = nullptr;
     vj.reg[i].dst2 = nullptr;
   }
@@ -464,10 +488,21 @@ int issue_copy_batch(ffx_ctx* c, PendingSnapshot& P, uint32_t b, cudaStream_t s)
 
 // Split policy: one hash batch (local state -> checksum table in the slot).
 int issue_hash_batch(ffx_ctx* c, PendingSnapshot& P, uint32_t b, cudaStream_t s) {
+  if (b == 0 && P.gcut) {
+    // hybrid: the fused share (marks the slot WRITING; the commit waits for both queues)
+    SliceJob fj = P.fjob;
+    fj.group_lo = 0;
+    fj.group_hi = P.gcut;
+    fj.commit.finalize = 0;
+    fj.commit2.finalize = 0;
+    fj.sched = c->done + 20;
+    FFX_CUDA(launch_slices(fj, SliceMode::Copy, true, P.hash_ctas, s));
+    c->stats.kernel_launches++;
+  }
   SliceJob hj = P.job;
-  const uint64_t G = P.job.total_groups;
-  hj.group_lo = G * b / P.hbatches;
-  hj.group_hi = G * (b + 1) / P.hbatches;
+  const uint64_t G0 = P.gcut, G = P.job.total_groups - P.gcut;
+  hj.group_lo = G0 + G * b / P.hbatches;
+  hj.group_hi = G0 + G * (b + 1) / P.hbatches;
   hj.commit.finalize = 0;
   hj.sched = c->done + 16;
   if (hj.group_lo == hj.group_hi) return FFX_OK;

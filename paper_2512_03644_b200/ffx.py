@@ -144,7 +144,7 @@ class SnapshotOpts(ctypes.Structure):
                 ("gate_events", ctypes.c_void_p), ("verify_on_store", ctypes.c_uint32),
                 ("weights_kind", ctypes.c_uint32), ("split", ctypes.c_uint32),
                 ("hash_batches", ctypes.c_uint32), ("hash_ctas", ctypes.c_uint32),
-                ("copy_engine", ctypes.c_uint32), ("pad_", ctypes.c_uint32),
+                ("copy_engine", ctypes.c_uint32), ("fused_permille", ctypes.c_uint32),
                 ("batch_weights", ctypes.POINTER(ctypes.c_double))]
 
 
@@ -730,9 +730,11 @@ class Context:
 
     def snapshot(self, iteration: int, stream=None, max_ctas: int = 0, batches: int = 1,
                  gate_events=None, verify_on_store: bool = False, weights_kind: bool = False,
-                 split: bool = False, hash_batches: int = 0, hash_ctas: int = 0, copy_engine: bool = False):
+                 split: bool = False, hash_batches: int = 0, hash_ctas: int = 0, copy_engine: bool = False,
+                 fused_permille: int = 0):
         o = SnapshotOpts()
         o.split = int(split)
+        o.fused_permille = fused_permille
         o.hash_batches = hash_batches
         o.hash_ctas = hash_ctas
         o.copy_engine = int(copy_engine)
@@ -749,8 +751,10 @@ class Context:
 
     def snapshot_begin(self, iteration: int, batches: int = 1, max_ctas: int = 0,
                        verify_on_store: bool = False, split: bool = False, hash_batches: int = 0,
-                       hash_ctas: int = 0, copy_engine: bool = False, batch_weights=None) -> int:
+                       hash_ctas: int = 0, copy_engine: bool = False, batch_weights=None,
+                       fused_permille: int = 0) -> int:
         o = SnapshotOpts()
+        o.fused_permille = fused_permille
         if batch_weights is not None:
             self._weights = (ctypes.c_double * len(batch_weights))(*batch_weights)  # kept alive
             o.batch_weights = self._weights

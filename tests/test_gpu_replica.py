@@ -369,6 +369,40 @@ def test_split_policy_copy_and_hash_batches(ffx, copy_engine):
     assert rep.export_frame(41) == orc.pack_blob((1, 0, 0), 41, 1, concat)
 
 
+@pytest.mark.parametrize("permille", [1, 300, 500, 999, 1000])
+def test_hybrid_fused_share_plus_copy_engines(ffx, permille):
+    # Hybrid split (opts.fused_permille): the first share of the warp tasks is
+    # copied + hashed by the fused kernel, the copy engines move the rest and
+    # the hash kernel checksums it; the cut falls inside and between regions.
+    n = (1 << 22) + 12345
+    spec, holder, origin, rep, view = ring_pair(ffx, 2 * n + 8000)
+    state, want = blob_for(ffx, 1, n)
+    state2, want2 = blob_for(ffx, 1, n, seed=7)
+    extra = torch.arange(1000, dtype=torch.int32, device="cuda")
+    origin.register(ffx.REGION_BLOB, state)
+    origin.register(ffx.REGION_PARAMS, state2)
+    origin.register(ffx.REGION_RNG, extra)
+    a, b = torch.cuda.Stream(), torch.cuda.Stream()
+    origin.snapshot_begin(50, batches=2, split=True, hash_batches=2, copy_engine=True, fused_permille=permille)
+    origin.snapshot_next(stream=a, kind=ffx.BATCH_COPY)
+    origin.snapshot_next(stream=b, kind=ffx.BATCH_HASH)
+    origin.snapshot_next(stream=a, kind=ffx.BATCH_COPY)
+    origin.snapshot_next(stream=b, kind=ffx.BATCH_HASH)
+    torch.cuda.synchronize()
+    concat = want + want2 + bytes(extra.cpu().numpy().tobytes())
+    assert rep.newest() == 50
+    assert rep.export_frame(50) == orc.pack_blob((1, 0, 0), 50, 1, concat)
+    origin.inject(ffx.FAULT_POISON_STATE)
+    assert origin.recover(view, 50).bad_slices == 0
+    assert host(state) == want and host(state2) == want2
+    # blocking form with the holder-side re-verify
+    origin.snapshot(51, split=True, copy_engine=True, fused_permille=permille, verify_on_store=True)
+    torch.cuda.synchronize()
+    assert rep.export_frame(51) == orc.pack_blob((1, 0, 0), 51, 1, concat)
+    with pytest.raises(ffx.InvalidArgument):
+        origin.snapshot(52, split=True, copy_engine=False, fused_permille=permille)
+
+
 @pytest.mark.parametrize("split", [False, True])
 def test_double_neighbour_dual_store(ffx, split):
     # Replicas at dp+1 and dp+2: one kernel, two stores per tile.

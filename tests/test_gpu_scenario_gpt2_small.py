@@ -64,7 +64,8 @@ def test_gpt2_small_ring_ten_iterations_then_single_rank_failure(ffx):
             for r in range(D):
                 ffx.materialize(state[r], orc.optimizer_at(42, r, 0, 0, it, D))
                 ctx[r].snapshot(it)
-            torch.cuda.synchronize()
+            for d in set(devs):
+                torch.cuda.synchronize(d)
         for r in range(D):  # two-version window (ckpt.cpp:46-52): 9 and 10 held
             assert held[r].newest() == 10
         # rank d1 dies; its shard comes back from the holder plan_recovery names
@@ -96,7 +97,8 @@ def test_gpt2_small_ring_ten_iterations_then_single_rank_failure(ffx):
         assert frame[:32] == ref[:32], who   # header incl. the whole-payload FNV
         assert frame == ref, who
     finally:
-        torch.cuda.synchronize()
+        for d in set(devs):
+            torch.cuda.synchronize(d)
         for v in views:
             v.destroy()
         for h in held:
