@@ -258,10 +258,28 @@ class Ring:
             ev = torch.cuda.Event()
             ev.record(stream)
             self.side.wait_event(ev)
+            # the checksum kernel is capped (96 CTAs): at full occupancy its HBM
+            # stream starves the copy engines (631 vs 769 GB/s per GPU at N=2,
+            # profiles/r1_bench_n2_ce_hash_ctas.txt)
             self.ctx.snapshot_begin(it, split=True, copy_engine=True, max_ctas=max_ctas,
+                                    hash_ctas=int(os.environ.get("FFX_BENCH_HASH_CTAS", "96")),
                                     fused_permille=fused_permille if mode == "hybrid" else 0)
+            trace = os.environ.get("FFX_BENCH_TRACE") and it % 7 == 0
+            if trace:
+                ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+                ev[0].record(self.side)
             self.ctx.snapshot_next(stream=self.side, kind=self.ffx.BATCH_COPY)
+            if trace:
+                ev[1].record(self.side)
+                ev[2].record(stream)
             self.ctx.snapshot_next(stream=stream, kind=self.ffx.BATCH_HASH)
+            if trace:
+                ev[3].record(stream)
+                torch.cuda.synchronize()
+                print(json.dumps({"trace": mode, "it": it, "copy_ms": round(ev[0].elapsed_time(ev[1]), 3),
+                                  "hash_ms": round(ev[2].elapsed_time(ev[3]), 3),
+                                  "hash_start_after_copy_start_ms": round(ev[0].elapsed_time(ev[2]), 3)}),
+                      file=sys.stderr, flush=True)
         else:
             self.ctx.snapshot(it, stream=stream, max_ctas=max_ctas)
 
