@@ -66,7 +66,7 @@ def parse():
     ap.add_argument("--no-70b", action="store_true", help="skip the 70B double-neighbour leg (N >= 3)")
     ap.add_argument("--prefix-70b", type=int, default=16 << 30, help="70B state prefix per rank (bytes)")
     ap.add_argument("--no-mcast", action="store_true", help="skip the NVSwitch-multicast double neighbour")
-    ap.add_argument("--fused-permille", type=int, default=500,
+    ap.add_argument("--fused-permille", type=int, default=50,
                     help="hybrid mode: share of the warp tasks the fused kernel pushes (the copy engines the rest)")
     ap.add_argument("--mode", default="push", choices=["push", "pull", "ce", "hybrid"],
                     help="N>1 ring stream: origin pushes into its successor's replica (fused kernel), the holder "
