@@ -3,23 +3,26 @@
 //
 // Work unit: one warp task = 32*RPL consecutive slices of one region; lane l
 // owns slices l, l+32, ... (FNV-1a is byte-serial, hash.cpp:102-110, so the
-// parallelism is independent slice chains).  Each step moves 128 bytes of
-// every slice of the task:
+// parallelism is independent slice chains).  Each step moves KC x 128 bytes
+// of every slice of the task:
 //
-//   full, aligned task (the bulk of any payload) -- 2-D tensor TMA: the
-//     region is viewed as {slice_bytes, nslices} with row pitch slice_bytes;
-//     one cp.async.bulk.tensor load brings a 128 x (32*RPL) box (row j =
-//     slice j) into shared memory with 128-byte swizzle (S stages, mbarrier
-//     complete_tx), one tensor store writes it to the destination (local HBM
-//     or the NVLink peer's replica; twice for double-neighbour replication),
-//     and each lane hashes its rows from shared memory, reading chunk w of
-//     row j at (w ^ (j & 7)) so every LDS.128 phase is conflict-free.  No
-//     payload byte passes through registers on the copy path.
+//   full, aligned task (the bulk of any payload) -- tensor TMA: the region
+//     is viewed as {128, nslices, slice_bytes/128} (3-D, KC > 1; the default
+//     KC = 2) or {slice_bytes, nslices} (2-D, KC = 1) with row pitch
+//     slice_bytes; one cp.async.bulk.tensor load brings a box of KC planes of
+//     128 x (32*RPL) bytes (row j = slice j) into shared memory with 128-byte
+//     swizzle (S stages, mbarrier complete_tx), one tensor store writes it to
+//     the destination (local HBM, the NVLink peer's replica, or an NVSwitch
+//     multicast range; twice for the dual-store double neighbour), and each
+//     lane hashes its rows from shared memory, reading chunk w of row j at
+//     (w ^ (j & 7)) so every LDS.128 phase is conflict-free.  No payload byte
+//     passes through registers on the copy path.
 //   ragged task (region tail, unaligned pointers) -- register path: 16-byte
 //     loads / stores and a padded shared-memory transpose.
 //
-// Tasks are handed out dynamically (one atomic per task) so the last wave
-// does not idle SMs.
+// Tasks are handed out dynamically (one atomic per task), last task first,
+// so the latency-bound ragged tails overlap the bulk and the last wave does
+// not idle SMs.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -281,7 +284,7 @@ __global__ void __launch_bounds__(W * 32) slice_kernel(const __grid_constant__ S
     __syncwarp();
 
     if (R.tmap >= 0 && s0 + K::ROWS <= R.nfull) {
-      // ---- 2-D tensor TMA: one 128 x ROWS box per step, 128 B swizzle ---------------
+      // ---- tensor TMA: one box of KC planes of 128 x ROWS per step, 128 B swizzle ----
       const CUtensorMap* msrc = &job.maps[3 * R.tmap];
       const CUtensorMap* mdst = &job.maps[3 * R.tmap + 1];
       const CUtensorMap* mdst2 = &job.maps[3 * R.tmap + 2];
