@@ -617,59 +617,97 @@ def seventy_mcast(args, ffx, torch, dist, world, rank, local, barrier, all_gathe
     """The same double neighbour with one egress per tile: each origin's
     snapshot kernel stores into an NVSwitch multicast range bound to the
     replica slots of dp+1 and dp+2 (ring.wire_mcast_ring), then the same
-    adjacent-pair loss is recovered from the dp+2 holders."""
+    adjacent-pair loss is recovered from the dp+2 holders.  Every step that
+    can fail ends in an agreement round, so a failure on one rank cannot
+    leave the others waiting in a collective."""
     from paper_2512_03644_b200 import ring
     ctx = ffx.Context(local, spec, ffx.Role(rank, 0, 0), args.slice_bytes)
     ctx.register(ffx.REGION_BLOB, state)
-    held, own, preds, view, handles = ring.wire_mcast_ring(
-        rank, world, lambda origin: ctx.create_shared_replica(ffx.Role(origin, 0, 0), prefix, 2),
-        lambda r: r.export(), ctx.open_replica, lambda: ctx.create_mcast(prefix, 2, members=3),
-        lambda m: m.export(), ctx.open_mcast, all_gather, barrier)
-    ctx.set_target_mcast(own, view)
-    s = torch.cuda.Stream()
-    for it in (1, 2):
-        ctx.snapshot(it, stream=s)
-    s.synchronize()
-    barrier()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(s)
-    for it in range(3, 3 + k):
-        ctx.snapshot(it, stream=s)
-    e1.record(s)
-    s.synchronize()
-    t = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device="cuda")
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    unique = prefix * k / (float(t.item()) * 1e-3) / 1e9
-    last = 2 + k
-    plan = ffx.plan_recovery(spec, [], [ffx.Role(1, 0, 0), ffx.Role(2, 0, 0)], last, 0, replicas=2)
-    sources = {o: (h, kk) for o, h, kk in ring.recovery_sources(plan.forwards, world)}
-    rec = None
-    barrier()
-    if rank in sources:
-        h, kk = sources[rank]
-        src = ctx.open_replica(handles[h][kk])
-        ctx.inject(ffx.FAULT_POISON_STATE)
-        rpt = ctx.recover(src, last, stream=s)
-        rec = {"holder": h, "recovery_s": round(rpt.seconds, 5),
-               "recovery_gbs": round(prefix / rpt.seconds / 1e9, 1),
-               "bit_exact": bool(rpt.bad_slices == 0 and ffx.blob_is_sound(state))}
-        src.destroy()
-    recs = all_gather(rec)
-    torch.cuda.synchronize()
-    barrier()
-    view.destroy()
-    own.destroy()  # the origin's mapping goes before any holder unbinds
-    barrier()
-    for m in preds:
-        m.destroy()
-    barrier()
-    for r in held:
-        r.destroy()
-    ctx.close()
-    return {"unique_state_gbs_per_gpu": round(unique, 1),
-            "replica_bytes_delivered_gbs_per_gpu": round(2 * unique, 1),
-            "vs_dual_store": "each tile leaves the origin once; the NVSwitch writes both replicas",
-            "adjacent_pair_recovery": [x for x in recs if x]}
+    objs = {}
+
+    def cleanup():
+        torch.cuda.synchronize()
+        for o in [objs.get("view"), objs.get("src")]:
+            if o is not None:
+                o.destroy()
+        if objs.get("own") is not None:
+            objs["own"].destroy()  # the origin's mapping goes before any holder unbinds
+        barrier()
+        for m in objs.get("preds", []):
+            m.destroy()
+        barrier()
+        for r in objs.get("held", []):
+            r.destroy()
+        ctx.close()
+
+    def step(what, fn):
+        ok, err, out = True, "", None
+        try:
+            out = fn()
+        except Exception as ex:  # agreed on below
+            ok, err = False, repr(ex)
+        res = all_gather((ok, err))
+        bad = [i for i, (o, _) in enumerate(res) if not o]
+        if bad:
+            raise ring.WiringError("%s failed on ranks %s: %s" % (what, bad, [e for o, e in res if not o][0]))
+        return out
+
+    try:
+        try:
+            held, own, preds, view, handles = ring.wire_mcast_ring(
+                rank, world, lambda origin: ctx.create_shared_replica(ffx.Role(origin, 0, 0), prefix, 2),
+                lambda r: r.export(), ctx.open_replica, lambda: ctx.create_mcast(prefix, 2, members=3),
+                lambda m: m.export(), ctx.open_mcast, all_gather, barrier)
+        except ring.WiringError as ex:
+            objs.update({kk: v for kk, v in getattr(ex, "created", {}).items() if v is not None})
+            raise
+        objs.update(held=held, own=own, preds=preds, view=view)
+        s = torch.cuda.Stream()
+
+        def warm():
+            ctx.set_target_mcast(own, view)
+            for it in (1, 2):
+                ctx.snapshot(it, stream=s)
+            s.synchronize()
+
+        step("multicast target + warm-up snapshots", warm)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+
+        def timed():
+            e0.record(s)
+            for it in range(3, 3 + k):
+                ctx.snapshot(it, stream=s)
+            e1.record(s)
+            s.synchronize()
+            return e0.elapsed_time(e1)
+
+        ms = step("timed multicast snapshots", timed)
+        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        unique = prefix * k / (float(t.item()) * 1e-3) / 1e9
+        last = 2 + k
+        plan = ffx.plan_recovery(spec, [], [ffx.Role(1, 0, 0), ffx.Role(2, 0, 0)], last, 0, replicas=2)
+        sources = {o: (h, kk) for o, h, kk in ring.recovery_sources(plan.forwards, world)}
+
+        def recover():
+            if rank not in sources:
+                return None
+            h, kk = sources[rank]
+            objs["src"] = ctx.open_replica(handles[h][kk])
+            ctx.inject(ffx.FAULT_POISON_STATE)
+            rpt = ctx.recover(objs["src"], last, stream=s)
+            return {"holder": h, "recovery_s": round(rpt.seconds, 5),
+                    "recovery_gbs": round(prefix / rpt.seconds / 1e9, 1),
+                    "bit_exact": bool(rpt.bad_slices == 0 and ffx.blob_is_sound(state))}
+
+        rec = step("adjacent-pair recovery", recover)
+        recs = all_gather(rec)
+        return {"unique_state_gbs_per_gpu": round(unique, 1),
+                "replica_bytes_delivered_gbs_per_gpu": round(2 * unique, 1),
+                "vs_dual_store": "each tile leaves the origin once; the NVSwitch writes both replicas",
+                "adjacent_pair_recovery": [x for x in recs if x]}
+    finally:
+        cleanup()
 
 
 def llama_dfail_leg(args, ffx, torch, dist, world, rank, local, barrier):

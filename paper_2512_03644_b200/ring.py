@@ -70,6 +70,19 @@ def recovery_sources(plan_forwards: Sequence, world: int, p: int = 1, t: int = 1
     return out
 
 
+class WiringError(RuntimeError):
+    """A step failed on some rank; every rank raises it at the same point, so
+    no rank is left waiting in a collective (or in a multicast bind, which
+    blocks until every member joined)."""
+
+
+def _agree(all_gather, ok: bool, what: str, err: str = ""):
+    results = all_gather((bool(ok), err))
+    bad = [(i, e) for i, (o, e) in enumerate(results) if not o]
+    if bad:
+        raise WiringError("%s failed on ranks %s: %s" % (what, [i for i, _ in bad], bad[0][1]))
+
+
 def wire_mcast_ring(rank: int, world: int, create_for: Callable[[int], object], export: Callable[[object], bytes],
                     open_handle: Callable[[bytes], object], create_mcast: Callable[[], object],
                     export_mcast: Callable[[object], bytes], open_mcast: Callable[[bytes], object],
@@ -83,24 +96,55 @@ def wire_mcast_ring(rank: int, world: int, create_for: Callable[[int], object], 
     predecessors 1..replicas and its own multicast object; handles are
     all-gathered; it opens the multicast objects of its predecessors; every
     member joins every team it is in (barrier) before any bind; holders bind;
-    the origin opens its first holder's replica as the read view.
+    the origin opens its first holder's replica as the read view.  Each
+    phase ends with an agreement round: a failure anywhere raises
+    WiringError on every rank (objects created so far are returned through
+    the exception's `created` attribute for cleanup).
 
     Returns (held, own_mc, pred_mcs, view, handles) -- handles[r][k] as in
     wire_ring, so recovery_sources() applies unchanged; the caller makes
     own_mc + view its snapshot target (ffx_snapshot_target_mcast).
     """
-    held = [create_for(predecessor(rank, world, p, t, k + 1)) for k in range(replicas)]
-    own = create_mcast()
+    created = {"held": [], "own": None, "preds": [], "view": None}
+
+    def phase(what, fn):
+        err, ok = "", True
+        try:
+            fn()
+        except Exception as ex:  # reported collectively below
+            ok, err = False, repr(ex)
+        try:
+            _agree(all_gather, ok, what, err)
+        except WiringError as ex:
+            ex.created = created
+            raise
+
+    def make():
+        for k in range(replicas):
+            created["held"].append(create_for(predecessor(rank, world, p, t, k + 1)))
+        created["own"] = create_mcast()
+
+    phase("replica / multicast creation", make)
+    held, own = created["held"], created["own"]
     mine = (b"".join(export(h) for h in held), export_mcast(own))
     gathered = all_gather(mine)
     hb = len(mine[0]) // replicas if replicas else 0
     handles = [[g[0][i * hb:(i + 1) * hb] for i in range(replicas)] for g in gathered]
-    preds = [open_mcast(gathered[predecessor(rank, world, p, t, k + 1)][1]) for k in range(replicas)]
-    for m in [own] + preds:
-        m.join()
+
+    def join():
+        for k in range(replicas):
+            created["preds"].append(open_mcast(gathered[predecessor(rank, world, p, t, k + 1)][1]))
+        for m in [own] + created["preds"]:
+            m.join()
+
+    phase("multicast join", join)
     barrier()  # every team complete before anyone binds or maps
-    for m, h in zip(preds, held):
-        m.bind(h)
-    barrier()
-    view = open_handle(handles[successor(rank, world, p, t, 1)][0])
-    return held, own, preds, view, handles
+    preds = created["preds"]
+
+    def bind():
+        for m, h in zip(preds, held):
+            m.bind(h)
+        created["view"] = open_handle(handles[successor(rank, world, p, t, 1)][0])
+
+    phase("multicast bind", bind)
+    return held, own, preds, created["view"], handles

@@ -159,3 +159,54 @@ def test_mcast_ring_wiring_gloo():
         binds = [e for e in log if e[0] == "bind"]
         assert all(log.index(b) > first_barrier for b in binds)  # no bind before every team is complete
         assert sorted((b[1], b[2]) for b in binds) == sorted((o, o) for o in held)
+
+
+def _mcast_fail_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        log = []
+
+        def all_gather(b):
+            out = [None] * world
+            dist.all_gather_object(out, b)
+            return out
+
+        def create_mcast():
+            if rank == 1:
+                raise RuntimeError("no multicast here")
+            return _FakeMcast(rank, log)
+
+        try:
+            ring.wire_mcast_ring(rank, world, create_for=lambda o: o, export=lambda o: b"H%02d<%02d" % (rank, o),
+                                 open_handle=bytes, create_mcast=create_mcast, export_mcast=lambda m: b"M00",
+                                 open_mcast=lambda h: _FakeMcast(0, log), all_gather=all_gather,
+                                 barrier=dist.barrier)
+            q.put((rank, "no error", log))
+        except ring.WiringError as ex:
+            dist.barrier()  # every rank got here: nobody is stuck in a collective
+            q.put((rank, str(ex), log))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_mcast_ring_failure_is_collective():
+    world = 4
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_mcast_fail_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = {}
+    for _ in range(world):
+        rank, msg, log = q.get(timeout=120)
+        res[rank] = (msg, log)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for r in range(world):
+        msg, log = res[r]
+        assert "failed on ranks [1]" in msg and "no multicast here" in msg
+        assert not any(e[0] in ("join", "bind") for e in log)  # nothing joined or bound
