@@ -569,6 +569,19 @@ def seventy_leg(args, ffx, torch, dist, world, rank, local, barrier):
     t = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device="cuda")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     egress = 2 * prefix * k / (float(t.item()) * 1e-3) / 1e9
+    # the same two replicas written by the DMA engines (split policy, checksum
+    # kernel capped at 96 CTAs): two peer copies per iteration
+    barrier()
+    d0, d1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    d0.record(s)
+    for it in range(3 + k, 3 + 2 * k):
+        ctx.snapshot(it, stream=s, split=True, copy_engine=True, hash_ctas=96)
+    d1.record(s)
+    s.synchronize()
+    t2 = torch.tensor([d0.elapsed_time(d1)], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t2, op=dist.ReduceOp.MAX)
+    egress_dma = 2 * prefix * k / (float(t2.item()) * 1e-3) / 1e9
+    k = 2 * k
     last = 2 + k
     # adjacent pair (ranks 1 and 2) lost: the reference falls back
     # (controller.cpp:162-167); with replicas at dp+1 and dp+2 both recover.
@@ -607,6 +620,7 @@ def seventy_leg(args, ffx, torch, dist, world, rank, local, barrier):
     return {"sizing": sizing, "prefix_bytes_per_rank": prefix,
             "multicast": mc,
             "dual_store_egress_gbs_per_gpu": round(egress, 1),
+            "dual_store_dma_egress_gbs_per_gpu": round(egress_dma, 1),
             "plan_reference_rule": ffx.plan_recovery(spec, [], [ffx.Role(1, 0, 0), ffx.Role(2, 0, 0)],
                                                      last, 0, replicas=1).kind,
             "plan_double_neighbour": plan.kind,

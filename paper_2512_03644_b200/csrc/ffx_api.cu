@@ -129,23 +129,51 @@ extern "C" int ffx_plan_recovery(const ffx_cluster_spec* s, const uint32_t* pods
   if (out->failed_pods) std::copy(fp.begin(), fp.end(), out->failed_pods);
   if (out->failed_roles) std::copy(lost.begin(), lost.end(), out->failed_roles);
 
-  // Serving holder per lost role: first survivor among dp+1 .. dp+replicas.
+  // Serving holder per lost role among the survivors of dp+1 .. dp+replicas.
+  // replicas = 1: the ring successor (the reference rule).  replicas > 1:
+  // spread the gathers over the surviving holders -- roles with the fewest
+  // candidates first, each to its least-loaded candidate (ties: the nearest)
+  // -- so an adjacent pair does not share one holder's NVLink egress.
   const uint32_t d = s->data_parallel;
   const uint32_t k = std::min<uint32_t>(replicas, d > 1 ? d - 1 : 1);
   bool neighbor_ok = d > 1;
   std::vector<uint32_t> holder(lost.size(), 0);
+  std::vector<std::vector<uint32_t>> cand(lost.size());
   for (size_t i = 0; i < lost.size() && neighbor_ok; ++i) {
-    bool found = false;
     for (uint32_t j = 1; j <= k; ++j) {
       ffx_role h = lost[i];
       h.dp = static_cast<uint16_t>((lost[i].dp + j) % d);
-      if (!is_lost(h)) {
-        holder[i] = h.dp;
-        found = true;
-        break;
-      }
+      if (!is_lost(h)) cand[i].push_back(h.dp);
     }
-    if (!found) neighbor_ok = false;
+    if (cand[i].empty()) neighbor_ok = false;
+  }
+  if (neighbor_ok) {
+    std::vector<size_t> order(lost.size());
+    std::iota(order.begin(), order.end(), size_t{0});
+    std::stable_sort(order.begin(), order.end(),
+                     [&](size_t a, size_t b) { return cand[a].size() < cand[b].size(); });
+    std::vector<uint32_t> load;  // per (holder dp, pp, tp) key, linear scan (small)
+    std::vector<uint64_t> load_key;
+    auto load_of = [&](uint64_t kk) -> uint32_t& {
+      for (size_t x = 0; x < load_key.size(); ++x)
+        if (load_key[x] == kk) return load[x];
+      load_key.push_back(kk);
+      load.push_back(0);
+      return load.back();
+    };
+    for (size_t i : order) {
+      uint32_t best = cand[i][0];
+      for (uint32_t c : cand[i]) {
+        ffx_role hc = lost[i], hb = lost[i];
+        hc.dp = static_cast<uint16_t>(c);
+        hb.dp = static_cast<uint16_t>(best);
+        if (load_of(key(hc)) < load_of(key(hb))) best = c;
+      }
+      ffx_role h = lost[i];
+      h.dp = static_cast<uint16_t>(best);
+      load_of(key(h))++;
+      holder[i] = best;
+    }
   }
   ffx_uniqueness_plan up;
   ffx_razor(s, &up);

@@ -185,12 +185,15 @@ def test_plan_recovery_vs_oracle(d, p, gpn, dist):
 
 def test_plan_recovery_double_neighbour_extension():
     # Adjacent pair on an 8-ring: the reference falls back (controller.cpp:162-167);
-    # with replicas at dp+1 and dp+2 the lost dp=2 is served by dp=4.
+    # with replicas at dp+1 and dp+2 the lost dp=2 is served by dp=4 (its only
+    # surviving holder) and dp=3 by dp=5, so the two gathers use two holders.
     spec = _shape(8, 1, 8, 1)
     spec.distributed_optimizer = 1
     assert ffx.plan_recovery(spec, [2, 3], [], 11, 5, replicas=1).kind == "fallback"
     p = ffx.plan_recovery(spec, [2, 3], [], 11, 5, replicas=2)
     assert p.kind == "neighbor"
     holders = {f[0].dp: f[3] for f in p.forwards}
-    assert holders == {2: 4, 3: 4}
+    assert holders == {2: 4, 3: 5}
+    # a single loss keeps the reference's ring successor
+    assert {f[0].dp: f[3] for f in ffx.plan_recovery(spec, [6], [], 11, 5, replicas=2).forwards} == {6: 7}
     assert ffx.plan_recovery(spec, [2, 3, 4], [], 11, 5, replicas=2).kind == "fallback"

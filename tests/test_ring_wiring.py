@@ -85,7 +85,7 @@ def test_recovery_sources_follow_plan():
     plan = ffx.plan_recovery(spec, [3], [], 10, 0)
     assert ring.recovery_sources(plan.forwards, 8) == [(3, 4, 0)]
     plan2 = ffx.plan_recovery(spec, [3, 4], [], 10, 0, replicas=2)
-    assert sorted(ring.recovery_sources(plan2.forwards, 8)) == [(3, 5, 1), (4, 5, 0)]
+    assert sorted(ring.recovery_sources(plan2.forwards, 8)) == [(3, 5, 1), (4, 6, 1)]
 
 
 def test_successor_predecessor_with_pp_tp():
