@@ -65,7 +65,7 @@ struct SliceJob {
                                   // (zero between launches; null = static)
   uint32_t proxy_fence;           // tensor path: generic->async proxy fence before each refill
   uint32_t stagger_ns;            // start-up de-phasing: warp w sleeps (w % 8) * stagger_ns first
-  uint32_t pad2_;
+  uint32_t claim_order;           // 0: last task first, then backwards; 1: last task first, then forwards
   SlotCommit commit;
   SlotCommit commit2;             // second replica's slot (slot null = none)
 };

@@ -254,7 +254,7 @@ __global__ void __launch_bounds__(W * 32) slice_kernel(const __grid_constant__ S
       if (lane == 0) t = atomicAdd(&job.sched[0], 1u);
       t = __shfl_sync(0xffffffffu, t, 0);
       if (t >= job.group_hi - job.group_lo) break;
-      g = job.group_hi - 1 - t;
+      g = (job.claim_order == 0 || t == 0) ? job.group_hi - 1 - t : job.group_lo + t - 1;
     } else {
       g = g_next;
       g_next += g_stride;
@@ -625,6 +625,11 @@ cudaError_t launch_slices(const SliceJob& job_in, SliceMode mode, bool commit, u
     return e ? static_cast<uint32_t>(std::strtoul(e, nullptr, 10)) : 0u;
   }();
   job.stagger_ns = stagger;
+  static const uint32_t order = [] {
+    const char* e = std::getenv("FFX_CLAIM_ORDER");
+    return e ? static_cast<uint32_t>(std::atoi(e)) : 0u;
+  }();
+  job.claim_order = order;
   switch (mode) {
     case SliceMode::Hash:
       return commit ? launch_mode<SliceMode::Hash, true>(job, max_ctas, stream)
