@@ -101,8 +101,10 @@ typedef struct ffx_redundant_source { /* RedundantSource, controller.hpp:151-154
 
 /* RecoveryPlan (controller.hpp:156-169).  The caller provides the arrays,
  * each with room for `capacity` entries (world size suffices). */
+enum ffx_plan_kind { FFX_PLAN_NEIGHBOR = 0, FFX_PLAN_FALLBACK = 1 }; /* ctl::RestoreKind */
+
 typedef struct ffx_recovery_plan {
-  uint32_t kind; /* 0 Neighbor, 1 Fallback (RestoreKind) */
+  uint32_t kind; /* ffx_plan_kind */
   uint32_t capacity;
   uint64_t resume_iteration;
   uint32_t* failed_pods;
