@@ -54,22 +54,29 @@ __device__ __forceinline__ void store16(uint8_t* base, uint64_t o, uint64_t byte
 // either all prefix or exactly words 2u, 2u+1 (u = (16t - word_base) / 16).
 __global__ void expand_kernel(uint8_t* dst, uint64_t fold, uint64_t bytes, uint64_t word_base,
                               uint4 p0, uint4 p1) {
+  // Vector t (bytes [16t, 16t+16)) holds words w, w+1 with w = 2t - word_base/8,
+  // i.e. mix64(fold + (w+1)G), mix64(fold + (w+2)G): the argument advances
+  // by 2G per vector, so by a constant per grid-stride step (mod 2^64).
   const uint64_t nvec = (bytes + 15) / 16;
+  const uint64_t nfull = bytes / 16;
   const bool al = aligned16(dst);
-  for (uint64_t t = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; t < nvec;
-       t += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  const uint64_t t_first = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+  uint64_t s = fold + (2 * t_first - word_base / 8 + 1) * kGolden;
+  const uint64_t dS = 2 * stride * kGolden;
+  for (uint64_t t = t_first; t < nvec; t += stride, s += dS) {
     const uint64_t o = 16 * t;
     uint4 v;
     if (o < word_base) {
       v = (o == 0) ? p0 : p1;
     } else {
-      const uint64_t w = (o - word_base) / 8;
-      const uint64_t a = mix64(fold + (w + 1) * kGolden);
-      const uint64_t b = mix64(fold + (w + 2) * kGolden);
+      const uint64_t a = mix64(s);
+      const uint64_t b = mix64(s + kGolden);
       v = make_uint4(static_cast<uint32_t>(a), static_cast<uint32_t>(a >> 32),
                      static_cast<uint32_t>(b), static_cast<uint32_t>(b >> 32));
     }
-    store16(dst, o, bytes, al, v);
+    if (al && t < nfull) st_stream(dst + o, v);
+    else store16(dst, o, bytes, al, v);
   }
 }
 
