@@ -1,0 +1,167 @@
+"""ZeRO-1 data-parallel training with per-iteration neighbour backup and a
+rank failure in the middle -- the FFTrainer path end to end on real state.
+
+    python -m torch.distributed.run --nproc-per-node 2 --master-addr 127.0.0.1 \\
+        examples/ring_train.py [--iters 12] [--fail-at 6] [--fail-rank 1]
+
+Every rank holds the full (bf16-free, fp32) MLP parameters, computes
+gradients on its own data, and owns one shard of the optimizer state
+(ZeRO-1): the fp32 master shard, Adam m / v for that shard, and the data
+cursor.  Those four regions are registered with ffx and snapshotted into the
+ring successor's replica after every optimizer update (NVLink, one kernel).
+At --fail-at the failing rank loses all four regions (poisoned), the plan
+names its holder, it pulls and verifies the replica, the ring re-gathers
+the parameters from the shards, and training continues.  The script then
+replays the run without the failure and prints one JSON line comparing the
+two: losses and final parameters must be bit-identical.
+"""
+import argparse
+import json
+import os
+import sys
+
+import torch
+import torch.distributed as dist
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2512_03644_b200 import ffx, ring  # noqa: E402
+
+IN, HID, OUT, BATCH = 512, 1024, 16, 256
+SHAPES = [(IN, HID), (HID,), (HID, OUT), (OUT,)]
+NPARAM = sum(torch.Size(s).numel() for s in SHAPES)
+
+
+class Rank:
+    def __init__(self, rank, world, seed=3):
+        self.rank, self.world = rank, world
+        self.shard = (NPARAM + world - 1) // world
+        total = self.shard * world
+        g = torch.Generator(device="cuda").manual_seed(seed)
+        self.params = torch.zeros(total, device="cuda")
+        self.params[:NPARAM] = torch.randn(NPARAM, device="cuda", generator=g) * 0.05
+        lo = rank * self.shard
+        self.master = self.params[lo:lo + self.shard].clone()  # this rank's fp32 master shard
+        self.m = torch.zeros(self.shard, device="cuda")
+        self.v = torch.zeros(self.shard, device="cuda")
+        self.cursor = torch.zeros(2, dtype=torch.int64, device="cuda")  # [step, data position]
+
+    def regions(self):
+        return [(ffx.REGION_MASTER, self.master), (ffx.REGION_ADAM_M, self.m), (ffx.REGION_ADAM_V, self.v),
+                (ffx.REGION_CURSOR, self.cursor)]
+
+    def views(self):
+        out, o = [], 0
+        for s in SHAPES:
+            n = torch.Size(s).numel()
+            out.append(self.params[o:o + n].view(s))
+            o += n
+        return out
+
+    def step(self, lr=1e-3, b1=0.9, b2=0.999, eps=1e-8):
+        pos = int(self.cursor[1].item())
+        g = torch.Generator(device="cuda").manual_seed(10_000 * pos + self.rank)
+        x = torch.randn(BATCH, IN, device="cuda", generator=g)
+        y = torch.randint(0, OUT, (BATCH,), device="cuda", generator=g)
+        p = self.params.detach().requires_grad_(True)
+        self.params = p
+        w1, c1, w2, c2 = self.views()
+        loss = torch.nn.functional.cross_entropy(torch.relu(x @ w1 + c1) @ w2 + c2, y)
+        loss.backward()
+        with torch.no_grad():
+            grad = p.grad
+            gshard = torch.empty(self.shard, device="cuda")
+            dist.reduce_scatter_tensor(gshard, grad, op=dist.ReduceOp.SUM)  # ZeRO-1: my shard's grads
+            gshard /= self.world
+            t = int(self.cursor[0].item()) + 1
+            self.m.mul_(b1).add_(gshard, alpha=1 - b1)
+            self.v.mul_(b2).addcmul_(gshard, gshard, value=1 - b2)
+            self.master.sub_(lr * (self.m / (1 - b1 ** t)) / ((self.v / (1 - b2 ** t)).sqrt() + eps))
+            self.cursor += 1
+            self.regather()
+        lsum = loss.detach().clone()
+        dist.all_reduce(lsum)
+        return float(lsum.item()) / self.world
+
+    def regather(self):
+        params = torch.empty(self.shard * self.world, device="cuda")
+        dist.all_gather_into_tensor(params, self.master)
+        self.params = params
+
+
+def run(args, rank, world, local, fail):
+    me = Rank(rank, world)
+    spec = ffx.make_spec(d=world, phi=NPARAM, distributed=True)
+    ctx = ffx.Context(local, spec, ffx.Role(rank, 0, 0))
+    for kind, t in me.regions():
+        ctx.register(kind, t)
+    nbytes = sum(t.numel() * t.element_size() for _, t in me.regions())
+
+    def all_gather(b):
+        out = [None] * world
+        dist.all_gather_object(out, b)
+        return out
+
+    held, targets, handles = ring.wire_ring(rank, world,
+                                            lambda origin: ctx.create_replica(ffx.Role(origin, 0, 0),
+                                                                              nbytes + 4096, 2),
+                                            lambda r: r.export(), ctx.open_replica, all_gather)
+    ctx.set_target(targets[0])
+    losses, recovered = [], None
+    try:
+        for it in range(1, args.iters + 1):
+            losses.append(me.step())
+            ctx.snapshot(it)  # after the optimizer update: master / m / v / cursor of iteration `it`
+            torch.cuda.synchronize()
+            dist.barrier()
+            if fail and it == args.fail_at:
+                plan = ffx.plan_recovery(spec, [], [ffx.Role(args.fail_rank, 0, 0)], it, 0)
+                if rank == args.fail_rank:
+                    _, holder, k = ring.recovery_sources(plan.forwards, world)[0]
+                    ctx.inject(ffx.FAULT_POISON_STATE)  # the rank's optimizer shard is gone
+                    src = ctx.open_replica(handles[holder][k])
+                    rpt = ctx.recover(src, it)
+                    recovered = {"iteration": it, "holder": holder, "bytes": rpt.bytes,
+                                 "seconds": rpt.seconds, "bad_slices": rpt.bad_slices}
+                    src.destroy()
+                dist.barrier()
+                with torch.no_grad():
+                    me.regather()  # the replacement's parameters come back from the shards
+        final = me.params.detach().clone()
+    finally:
+        torch.cuda.synchronize()
+        for r in targets + held:
+            r.destroy()
+        ctx.close()
+    return losses, final, recovered
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--iters", type=int, default=12)
+    ap.add_argument("--fail-at", type=int, default=6)
+    ap.add_argument("--fail-rank", type=int, default=1)
+    args = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    torch.backends.cuda.matmul.allow_tf32 = False
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    args.fail_rank %= world
+    l_fail, p_fail, rec = run(args, rank, world, local, fail=True)
+    l_ref, p_ref, _ = run(args, rank, world, local, fail=False)
+    same = torch.tensor([int(torch.equal(p_fail, p_ref) and l_fail == l_ref)], device="cuda")
+    dist.all_reduce(same, op=dist.ReduceOp.MIN)
+    recs = [None] * world
+    dist.all_gather_object(recs, rec)
+    if rank == 0:
+        print(json.dumps({"world": world, "iters": args.iters, "fail_at": args.fail_at,
+                          "fail_rank": args.fail_rank, "recovery": recs[args.fail_rank],
+                          "losses": [round(x, 6) for x in l_fail],
+                          "bit_identical_to_uninterrupted_run": bool(same.item())}))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
