@@ -2,7 +2,7 @@
 rank failure in the middle -- the FFTrainer path end to end on real state.
 
     python -m torch.distributed.run --nproc-per-node 2 --master-addr 127.0.0.1 \\
-        examples/ring_train.py [--iters 12] [--fail-at 6] [--fail-rank 1]
+        examples/ring_train.py [--iters 12] [--fail-at 6] [--fail-rank 1] [--overlap]
 
 Every rank holds the full (bf16-free, fp32) MLP parameters, computes
 gradients on its own data, and owns one shard of the optimizer state
@@ -57,7 +57,7 @@ class Rank:
             o += n
         return out
 
-    def step(self, lr=1e-3, b1=0.9, b2=0.999, eps=1e-8):
+    def step(self, lr=1e-3, b1=0.9, b2=0.999, eps=1e-8, before_update=None):
         pos = int(self.cursor[1].item())
         g = torch.Generator(device="cuda").manual_seed(10_000 * pos + self.rank)
         x = torch.randn(BATCH, IN, device="cuda", generator=g)
@@ -72,6 +72,8 @@ class Rank:
             gshard = torch.empty(self.shard, device="cuda")
             dist.reduce_scatter_tensor(gshard, grad, op=dist.ReduceOp.SUM)  # ZeRO-1: my shard's grads
             gshard /= self.world
+            if before_update is not None:
+                before_update()  # overlap: the previous snapshot must have read master / m / v
             t = int(self.cursor[0].item()) + 1
             self.m.mul_(b1).add_(gshard, alpha=1 - b1)
             self.v.mul_(b2).addcmul_(gshard, gshard, value=1 - b2)
@@ -107,13 +109,28 @@ def run(args, rank, world, local, fail):
                                             lambda r: r.export(), ctx.open_replica, all_gather)
     ctx.set_target(targets[0])
     losses, recovered = [], None
+    snap_stream = torch.cuda.Stream()
+    snap_done = None
     try:
         for it in range(1, args.iters + 1):
-            losses.append(me.step())
-            ctx.snapshot(it)  # after the optimizer update: master / m / v / cursor of iteration `it`
-            torch.cuda.synchronize()
-            dist.barrier()
+            if args.overlap:
+                # the snapshot of iteration it-1 streams from the live buffers while
+                # this iteration's forward / backward runs; only the optimizer
+                # update waits for it (no staging copy)
+                wait = (lambda ev=snap_done: torch.cuda.current_stream().wait_event(ev)) if snap_done else None
+                losses.append(me.step(before_update=wait))
+                ready = torch.cuda.Event()
+                ready.record()  # the update of iteration `it` is done
+                snap_stream.wait_event(ready)
+                ctx.snapshot(it, stream=snap_stream)
+                snap_done = torch.cuda.Event()
+                snap_done.record(snap_stream)
+            else:
+                losses.append(me.step())
+                ctx.snapshot(it)  # after the optimizer update: master / m / v / cursor of iteration `it`
             if fail and it == args.fail_at:
+                torch.cuda.synchronize()  # the snapshot of `it` has committed everywhere
+                dist.barrier()
                 plan = ffx.plan_recovery(spec, [], [ffx.Role(args.fail_rank, 0, 0)], it, 0)
                 if rank == args.fail_rank:
                     _, holder, k = ring.recovery_sources(plan.forwards, world)[0]
@@ -140,6 +157,8 @@ def main():
     ap.add_argument("--iters", type=int, default=12)
     ap.add_argument("--fail-at", type=int, default=6)
     ap.add_argument("--fail-rank", type=int, default=1)
+    ap.add_argument("--overlap", action="store_true",
+                    help="snapshot iteration n while iteration n+1 computes; the optimizer update waits")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -155,7 +174,7 @@ def main():
     recs = [None] * world
     dist.all_gather_object(recs, rec)
     if rank == 0:
-        print(json.dumps({"world": world, "iters": args.iters, "fail_at": args.fail_at,
+        print(json.dumps({"world": world, "iters": args.iters, "fail_at": args.fail_at, "overlap": args.overlap,
                           "fail_rank": args.fail_rank, "recovery": recs[args.fail_rank],
                           "losses": [round(x, 6) for x in l_fail],
                           "bit_identical_to_uninterrupted_run": bool(same.item())}))

@@ -23,12 +23,15 @@ def _port():
     return p
 
 
-def test_ring_train_example_two_ranks():
+@pytest.mark.parametrize("overlap", [False, True])
+def test_ring_train_example_two_ranks(overlap):
     if torch.cuda.device_count() < 2:
         pytest.skip("needs 2 GPUs")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
            "--master-addr", "127.0.0.1", "--master-port", str(_port()),
            os.path.join(ROOT, "examples", "ring_train.py"), "--iters", "10", "--fail-at", "5"]
+    if overlap:  # snapshot of iteration n during iteration n+1; only the optimizer update waits
+        cmd.append("--overlap")
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
     assert r.returncode == 0, r.stderr[-3000:]
     line = [x for x in r.stdout.splitlines() if x.startswith("{")][-1]
