@@ -6,7 +6,11 @@ import time
 
 import torch
 
-from paper_2512_03644_b200 import ffx
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2512_03644_b200 import ffx  # noqa: E402
 
 
 def main(n=2_336_416_800):

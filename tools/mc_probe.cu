@@ -9,7 +9,9 @@
 //   mm_st    : multimem.st.v4 into the multicast range (every member receives it)
 //   st_mc    : a plain st.global.v4 to the multicast range
 //   tma_mc   : cp.async.bulk (shared -> global) to the multicast range
-// and checks bit-exactly what landed in every member's memory.  Groups:
+// and checks bit-exactly what landed in every member's memory.
+//   build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 \
+//            -o tools/mc_probe tools/mc_probe.cu -lcuda  Groups:
 // {0,1}; {0,1,2}; {0,1,2} with the origin binding no memory; shareable-handle
 // round trips (POSIX fd, fabric).  Prints one JSON line per group.  Not part
 // of libffx.so.

@@ -1,6 +1,6 @@
 """Kernel decomposition probe (measurement tooling, not product code).
 
-    python -m paper_2512_03644_b200.probe [--bytes N] [--peer]
+    python tools/probe.py [--bytes N] [--peer]
 
 Times, on the same buffers and with CUDA events, the pieces the snapshot
 kernel fuses so its roofline fraction can be explained:
@@ -16,7 +16,11 @@ import json
 
 import torch
 
-from paper_2512_03644_b200 import ffx
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2512_03644_b200 import ffx  # noqa: E402
 
 
 def timed(fn, reps=10, warm=3, stream=None):

@@ -1,6 +1,6 @@
 """Copy-engine ring-shift probe (measurement tooling, not product code).
 
-    python -m paper_2512_03644_b200.probe_ce
+    python tools/probe_ce.py
 
 Two GPUs, both directions at once (a 2-rank ring shift by the DMA engines
 alone): GB/s per GPU of a peer cudaMemcpyAsync of ~2.3 GB as a function of
@@ -12,7 +12,11 @@ import json
 
 import torch
 
-from paper_2512_03644_b200 import ffx
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2512_03644_b200 import ffx  # noqa: E402
 
 
 def main(n=2_336_416_800 // 4096 * 4096):

@@ -1,6 +1,6 @@
 """Ring-shift mechanism probe (measurement tooling, not product code).
 
-    python -m paper_2512_03644_b200.probe_mix [--bytes N]
+    python tools/probe_mix.py [--bytes N]
 
 Two GPUs driven from one process, both directions at once (the ring shift
 of a 2-rank ring).  Times moving N bytes per GPU to the other GPU (with the
@@ -17,7 +17,11 @@ import json
 
 import torch
 
-from paper_2512_03644_b200 import ffx
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2512_03644_b200 import ffx  # noqa: E402
 
 
 def main():
