@@ -68,7 +68,7 @@ def parse():
     ap.add_argument("--no-mcast", action="store_true", help="skip the NVSwitch-multicast double neighbour")
     ap.add_argument("--fused-permille", type=int, default=50,
                     help="hybrid mode: share of the warp tasks the fused kernel pushes (the copy engines the rest)")
-    ap.add_argument("--mode", default="push", choices=["push", "pull", "ce", "hybrid"],
+    ap.add_argument("--mode", default="push", choices=["push", "pull", "ce", "hybrid", "nccl", "nccl-copy"],
                     help="N>1 ring stream: origin pushes into its successor's replica (fused kernel), the holder "
                          "pulls its predecessor's regions (NeighborBuffer::store side), or ce: copy engines + "
                          "a concurrent checksum kernel (split policy)")
@@ -211,6 +211,8 @@ class Ring:
         from paper_2512_03644_b200 import ring
         import pyoracle
         self.ffx, self.n, self.torch, self.side = ffx, n, torch, None
+        self.dist, self.rank, self.world, self.slice_bytes = dist, rank, world, slice_bytes
+        self.nccl_buf = self.nccl_sums = None
         self.ctx = ffx.Context(local, spec, ffx.Role(rank, 0, 0), slice_bytes)
         self.holder = None
         if world == 1:
@@ -246,6 +248,24 @@ class Ring:
     def snapshot(self, it, stream, mode, max_ctas=0, fused_permille=500):
         if mode == "pull" and self.remote is not None:
             self.ctx.snapshot_pull(self.remote, self.held, it, stream=stream, max_ctas=max_ctas)
+        elif mode in ("nccl", "nccl-copy"):
+            # SURVEY 8(e)'s baseline: a grouped ncclSend/ncclRecv ring shift of
+            # the state into a receive buffer, with the per-slice checksum by
+            # our hash kernel alongside (no replica slot / commit protocol)
+            from paper_2512_03644_b200 import ring
+            torch, dist = self.torch, self.dist
+            if self.nccl_buf is None:
+                self.nccl_buf = torch.empty(self.n, dtype=torch.uint8, device="cuda")
+                self.nccl_sums = torch.empty((self.n + self.slice_bytes - 1) // self.slice_bytes,
+                                             dtype=torch.int64, device="cuda")
+            with torch.cuda.stream(stream):
+                ops = [dist.P2POp(dist.isend, self.state[0], ring.successor(self.rank, self.world)),
+                       dist.P2POp(dist.irecv, self.nccl_buf, ring.predecessor(self.rank, self.world))]
+                reqs = dist.batch_isend_irecv(ops)
+                if mode == "nccl":  # nccl-copy: the transfer alone, no checksum
+                    self.ffx.slice_checksums(self.state[0], self.slice_bytes, self.nccl_sums, stream=stream)
+                for r in reqs:
+                    r.wait()
         elif mode in ("ce", "hybrid"):
             # split policy, unscheduled: the copy engines move the bytes on a
             # side stream while the checksum kernel hashes the local state;
@@ -374,7 +394,7 @@ def main():
     alt = None
     if world > 1:
         alt = []
-        for other in [m for m in ("push", "pull", "ce", "hybrid") if m != args.mode]:
+        for other in [m for m in ("push", "pull", "ce", "hybrid", "nccl", "nccl-copy") if m != args.mode]:
             barrier()
             torch.cuda.synchronize()
             for _ in range(2):
@@ -390,7 +410,7 @@ def main():
             barrier()
             ams = max_over_ranks(a0.elapsed_time(a1))
             alt.append({"mode": other, "per_gpu_gbs": round(n * args.steps / (ams * 1e-3) / 1e9, 2),
-                        "committed": R.target.newest() == it,
+                        "committed": R.target.newest() == it if not other.startswith("nccl") else None,
                         **({"fused_permille": args.fused_permille} if other == "hybrid" else {})})
 
     # ---- recovery: rank (1 % world) loses its state and pulls it back --------
@@ -403,7 +423,7 @@ def main():
         runs, ok = [], True
         for _ in range(3):
             R.ctx.inject(ffx.FAULT_POISON_STATE)
-            rpt = R.ctx.recover(R.target, it, stream=stream)
+            rpt = R.ctx.recover(R.target, R.target.newest(), stream=stream)  # the last committed snapshot
             ok = ok and rpt.bad_slices == 0 and ffx.blob_is_sound(R.state[0])
             runs.append(rpt.seconds)
         t_rec = sorted(runs)[1]
