@@ -834,6 +834,7 @@ def llama_leg(args, ffx, torch, dist, world, rank, local, barrier):
                                  ("split", {"copy_ctas": 8, "hash_ctas": 0, "copy_engine": True}, 50)):
             sched = SliceScheduler(R.ctx, step, policy=policy, **kw)
             runs.append(measure_overhead(step, sched, steps=n_ab, warmup=2, it0=10 + 1000 * len(runs)))
+            sched.close()
         best = min(runs, key=lambda r: r["overhead_pct"])
         out["step_overhead"] = dict(best, all_policies=runs)
         # the snapshots taken inside the step must recover bit-exactly too

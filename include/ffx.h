@@ -376,6 +376,41 @@ int ffx_snapshot_next(ffx_ctx* ctx, void* stream, void* gate_event, uint32_t* re
  * FFX_BATCH_HASH; fused snapshots only have copy batches). */
 int ffx_snapshot_next_kind(ffx_ctx* ctx, int kind, void* stream, void* gate_event, uint32_t* remaining);
 
+/* ---- the slice scheduler as a native object ---------------------------------
+ * TRAIN > STATE (sim_net.cpp:401-454): the training step reports its gaps and
+ * the scheduler issues one snapshot batch per gap on its own low-priority
+ * streams, gated on an event recorded on the step's stream, so STATE work
+ * only starts where TRAIN leaves the resource idle and can delay TRAIN by
+ * at most one batch (its CTA cap).
+ *   FFX_GAP_LINK_IDLE   a collective just finished (NVLink idle while the
+ *                       step computes): copy batches go here
+ *   FFX_GAP_SM_IDLE     a collective is about to start (SMs idle behind
+ *                       NCCL): split-policy checksum batches go here
+ * ffx_sched_finish() issues whatever is left and makes the step's stream
+ * wait for the slot commit -- call it before the optimizer mutates the
+ * registered state. */
+enum ffx_sched_policy {
+  FFX_SCHED_FUSED = 0,     /* copy + checksum batches in the link-idle gaps */
+  FFX_SCHED_SPLIT = 1,     /* TMA copy batches (link-idle) + checksum batches (SM-idle) */
+  FFX_SCHED_SPLIT_CE = 2   /* copy-engine batches (link-idle) + checksum batches (SM-idle) */
+};
+enum ffx_gap_kind { FFX_GAP_LINK_IDLE = 0, FFX_GAP_SM_IDLE = 1 };
+typedef struct ffx_sched_opts {
+  uint32_t policy;         /* ffx_sched_policy */
+  uint32_t link_gaps;      /* FFX_GAP_LINK_IDLE reports per step (copy batches) */
+  uint32_t sm_gaps;        /* FFX_GAP_SM_IDLE reports per step (checksum batches; split) */
+  uint32_t copy_ctas;      /* CTA cap of fused / TMA copy batches (0 = 32 / 8) */
+  uint32_t hash_ctas;      /* CTA cap of checksum batches (0 = 96) */
+  uint32_t pad_;
+  const double* gap_ms;    /* measured link-idle gap durations, link_gaps entries (NULL = equal) */
+} ffx_sched_opts;
+typedef struct ffx_sched ffx_sched;
+int ffx_sched_create(ffx_ctx* ctx, const ffx_sched_opts* opts, ffx_sched** out);
+int ffx_sched_begin(ffx_sched* s, uint64_t iteration);
+int ffx_sched_gap(ffx_sched* s, int gap_kind, void* train_stream);
+int ffx_sched_finish(ffx_sched* s, void* train_stream);
+int ffx_sched_destroy(ffx_sched* s);
+
 /* Copy the checksum table written by this ctx's most recent snapshot into
  * host memory (async on `stream`; pinned memory for true overlap).
  * *n_out = entries copied (min(table, max_entries)). */

@@ -6,6 +6,7 @@
 //   ffx_snapshot.cu  snapshot issue, pull mode, slice scheduler batches
 //   ffx_recover.cu   recovery gather/verify, CUDA IPC, failure injection
 //   ffx_mcast.cu     shareable replicas + NVSwitch multicast
+//   ffx_sched.cu     the slice scheduler (gap-driven batches)
 // No CPU compute path exists for any payload byte: every copy, checksum and
 // verification runs on the GPU; the host only sizes, chooses slots and
 // launches.

@@ -148,6 +148,16 @@ class SnapshotOpts(ctypes.Structure):
                 ("batch_weights", ctypes.POINTER(ctypes.c_double))]
 
 
+class SchedOpts(ctypes.Structure):
+    _fields_ = [("policy", ctypes.c_uint32), ("link_gaps", ctypes.c_uint32), ("sm_gaps", ctypes.c_uint32),
+                ("copy_ctas", ctypes.c_uint32), ("hash_ctas", ctypes.c_uint32), ("pad_", ctypes.c_uint32),
+                ("gap_ms", ctypes.POINTER(ctypes.c_double))]
+
+
+SCHED_FUSED, SCHED_SPLIT, SCHED_SPLIT_CE = 0, 1, 2
+GAP_LINK_IDLE, GAP_SM_IDLE = 0, 1
+
+
 class RecoverReport(ctypes.Structure):
     _fields_ = [("bytes", ctypes.c_uint64), ("first_bad_slice", ctypes.c_uint64),
                 ("bad_slices", ctypes.c_uint64), ("slot", ctypes.c_uint32), ("pad_", ctypes.c_uint32),
@@ -246,6 +256,11 @@ SIGNATURES = {
     "ffx_snapshot": (_I, [_P, _U64, _P, ctypes.POINTER(SnapshotOpts)]),
     "ffx_snapshot_target2": (_I, [_P, _P]),
     "ffx_mcast_supported": (_I, [_I, ctypes.POINTER(_I)]),
+    "ffx_sched_create": (_I, [_P, ctypes.POINTER(SchedOpts), ctypes.POINTER(_P)]),
+    "ffx_sched_begin": (_I, [_P, _U64]),
+    "ffx_sched_gap": (_I, [_P, _I, _P]),
+    "ffx_sched_finish": (_I, [_P, _P]),
+    "ffx_sched_destroy": (_I, [_P]),
     "ffx_replica_create_shared": (_I, [_P, Role, _U64, _U32, ctypes.POINTER(_P)]),
     "ffx_mcast_create": (_I, [_P, _U64, _U32, _U32, ctypes.POINTER(_P)]),
     "ffx_mcast_export": (_I, [_P, _P]),
@@ -607,6 +622,37 @@ def mcast_supported(device: int = 0) -> bool:
     v = _I()
     check(lib.ffx_mcast_supported(device, ctypes.byref(v)), "mcast_supported")
     return bool(v.value)
+
+
+class Sched:
+    """The native slice scheduler (ffx_sched_*): one snapshot batch per gap
+    the training step reports."""
+
+    def __init__(self, ctx: "Context", policy: int, link_gaps: int, sm_gaps: int = 0, copy_ctas: int = 0,
+                 hash_ctas: int = 0, gap_ms=None):
+        o = SchedOpts()
+        o.policy, o.link_gaps, o.sm_gaps = policy, link_gaps, sm_gaps
+        o.copy_ctas, o.hash_ctas = copy_ctas, hash_ctas
+        if gap_ms is not None:
+            self._gaps = (ctypes.c_double * len(gap_ms))(*gap_ms)
+            o.gap_ms = self._gaps
+        self._h = ctypes.c_void_p()
+        self._ctx = ctx
+        check(lib.ffx_sched_create(ctx.ptr, ctypes.byref(o), ctypes.byref(self._h)), "sched_create")
+
+    def begin(self, iteration: int):
+        check(lib.ffx_sched_begin(self._h, iteration), "sched_begin")
+
+    def gap(self, kind: int, train_stream=None):
+        check(lib.ffx_sched_gap(self._h, kind, _stream_ptr(train_stream)), "sched_gap")
+
+    def finish(self, train_stream=None):
+        check(lib.ffx_sched_finish(self._h, _stream_ptr(train_stream)), "sched_finish")
+
+    def destroy(self):
+        if self._h:
+            check(lib.ffx_sched_destroy(self._h), "sched_destroy")
+            self._h = ctypes.c_void_p(0)
 
 
 class Remote:

@@ -94,10 +94,7 @@ class SliceScheduler:
         self.copy_ctas = copy_ctas
         self.hash_ctas = hash_ctas
         self.copy_engine = copy_engine
-        self.low = torch.cuda.Stream(priority=0)
-        self.hash_stream = torch.cuda.Stream(priority=0)
-        self.done = torch.cuda.Event()
-        self.copies = self.hashes = 0
+        self.native = None  # ffx.Sched, built on first use / after calibrate()
 
     weights = None  # measured idle-link window per copy gap (calibrate())
 
@@ -119,48 +116,42 @@ class SliceScheduler:
             if kind in ("fwd", "bwd") and i + 1 < len(marks):
                 w.append(max(ev.elapsed_time(marks[i + 1][1]), 1e-3))
         self.weights = w
+        self._make()
         return w
 
-    def begin(self, iteration: int):
-        # one batch per all-gather gap, forward and backward (2L gaps)
+    def _make(self):
+        """(Re)build the native scheduler (ffx_sched_*) for this policy and
+        the measured gaps: one copy batch per link-idle gap (after each
+        all-gather, 2L per step) and, split policies, one checksum batch per
+        SM-idle gap (before each all-gather)."""
+        if self.native is not None:
+            self.native.destroy()
         G = 2 * self.step.layers
-        weights = self.weights if self.weights and len(self.weights) == G else None
-        if self.policy == "fused":
-            self.copies = self.ctx.snapshot_begin(iteration, batches=G, max_ctas=self.copy_ctas,
-                                                  batch_weights=weights)
-            self.hashes = 0
-        else:
-            self.copies = self.ctx.snapshot_begin(iteration, batches=G, max_ctas=self.copy_ctas, split=True,
-                                                  hash_batches=G, hash_ctas=self.hash_ctas,
-                                                  copy_engine=self.copy_engine, batch_weights=weights)
-            self.hashes = G
+        ffx = self.ffx
+        pol = ffx.SCHED_FUSED if self.policy == "fused" else (ffx.SCHED_SPLIT_CE if self.copy_engine
+                                                               else ffx.SCHED_SPLIT)
+        gaps = self.weights if self.weights and len(self.weights) == G else None
+        self.native = ffx.Sched(self.ctx, pol, link_gaps=G, sm_gaps=0 if pol == ffx.SCHED_FUSED else G,
+                                copy_ctas=self.copy_ctas or (1 << 20), hash_ctas=self.hash_ctas or (1 << 20),
+                                gap_ms=gaps)
 
-    def _issue(self, kind, stream, gate=None):
-        left = self.ctx.snapshot_next(stream=stream, gate_event=gate,
-                                      kind=None if self.policy == "fused" else kind)
-        if kind == self.ffx.BATCH_COPY:
-            self.copies = left
-        else:
-            self.hashes = left
-        if self.copies == 0 and self.hashes == 0:
-            self.done.record(stream)  # this stream carried the commit
-
-    def _gap(self):
-        ev = torch.cuda.Event()
-        ev.record(self.step.train)
-        return ev
+    def begin(self, iteration: int):
+        if self.native is None:
+            self._make()
+        self.native.begin(iteration)
 
     def hook(self, kind, layer):
-        if kind == "pre_ag" and self.hashes:
-            self._issue(self.ffx.BATCH_HASH, self.hash_stream, self._gap())
-        elif kind in ("fwd", "bwd") and self.copies:
-            self._issue(self.ffx.BATCH_COPY, self.low, self._gap())
-        elif kind == "opt":
-            while self.copies:  # more batches than gaps: flush now
-                self._issue(self.ffx.BATCH_COPY, self.low)
-            while self.hashes:
-                self._issue(self.ffx.BATCH_HASH, self.hash_stream)
-            self.step.train.wait_event(self.done)  # optimizer mutates the snapshotted state
+        if kind == "pre_ag":      # NCCL about to run: SMs idle
+            self.native.gap(self.ffx.GAP_SM_IDLE, self.step.train)
+        elif kind in ("fwd", "bwd"):  # collective done: NVLink idle while the GEMMs run
+            self.native.gap(self.ffx.GAP_LINK_IDLE, self.step.train)
+        elif kind == "opt":       # flush, and the optimizer waits for the commit
+            self.native.finish(self.step.train)
+
+    def close(self):
+        if self.native is not None:
+            self.native.destroy()
+            self.native = None
 
 
 def time_steps(step: SyntheticStep, n: int, sched: SliceScheduler | None = None, it0: int = 0):

@@ -118,6 +118,7 @@ def main():
     for i, (policy, kw) in enumerate(variants):
         sched = SliceScheduler(ctx, step, policy=policy, **kw)
         r = measure_overhead(step, sched, steps=args.steps, warmup=2, it0=10 + 1000 * i)
+        sched.close()
         out.append({"policy": r["policy"], "copy_ctas": kw.get("copy_ctas"), "hash_ctas": kw.get("hash_ctas"),
                     "overhead_pct": r["overhead_pct"], "step_ms_without": r["step_ms_without"]})
     if rank == 0:
