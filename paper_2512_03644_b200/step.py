@@ -63,7 +63,7 @@ class SyntheticStep:
     def run(self, hook=None):
         """One step on self.train.  hook(kind, layer) marks the gaps:
         'pre_ag' before an all-gather, 'fwd'/'bwd' once it completed,
-        'opt' before the optimizer update."""
+        'pre_rs' before a reduce-scatter, 'opt' before the optimizer update."""
         h = hook or (lambda kind, layer: None)
         with torch.cuda.stream(self.train):
             for l in range(self.layers):
@@ -76,6 +76,7 @@ class SyntheticStep:
                 dist.all_gather_into_tensor(self.full, self.shard)
                 h("bwd", l)
                 self._gemms(2 * self.fwd_gemms)
+                h("pre_rs", l)
                 dist.reduce_scatter_tensor(self.grad_shard, self.grad_full)
             h("opt", None)
             self.shard.add_(self.grad_shard, alpha=-1e-6)  # the optimizer update
@@ -85,7 +86,7 @@ class SliceScheduler:
     """Drives one ffx snapshot per step through the gaps of a SyntheticStep."""
 
     def __init__(self, ctx, step: SyntheticStep, policy: str = "split", copy_ctas: int = 8,
-                 hash_ctas: int = 96, copy_engine: bool = False):
+                 hash_ctas: int = 96, copy_engine: bool = False, front: float = 1.0, rs_gaps: bool = False):
         from paper_2512_03644_b200 import ffx
         self.ffx = ffx
         self.ctx = ctx
@@ -94,6 +95,12 @@ class SliceScheduler:
         self.copy_ctas = copy_ctas
         self.hash_ctas = hash_ctas
         self.copy_engine = copy_engine
+        # Only the first `front` share of the step's gaps carries batches: the
+        # idle-link windows hold several times what the copy needs, and a batch
+        # that overruns the last gaps delays the optimizer (which waits for
+        # the commit).
+        self.front = front
+        self.rs_gaps = rs_gaps  # checksum batches also before each reduce-scatter
         self.native = None  # ffx.Sched, built on first use / after calibrate()
 
     weights = None  # measured idle-link window per copy gap (calibrate())
@@ -131,7 +138,13 @@ class SliceScheduler:
         pol = ffx.SCHED_FUSED if self.policy == "fused" else (ffx.SCHED_SPLIT_CE if self.copy_engine
                                                                else ffx.SCHED_SPLIT)
         gaps = self.weights if self.weights and len(self.weights) == G else None
-        self.native = ffx.Sched(self.ctx, pol, link_gaps=G, sm_gaps=0 if pol == ffx.SCHED_FUSED else G,
+        k = max(1, min(G, int(round(G * self.front))))
+        if k < G:
+            gaps = [x if i < k else 0.0 for i, x in enumerate(gaps or [1.0] * G)]
+        # SM-idle gaps: before every all-gather and, if enabled, every reduce-scatter
+        S = G + (self.step.layers if self.rs_gaps else 0)
+        ks = max(1, min(S, int(round(S * self.front))))
+        self.native = ffx.Sched(self.ctx, pol, link_gaps=G, sm_gaps=0 if pol == ffx.SCHED_FUSED else ks,
                                 copy_ctas=self.copy_ctas or (1 << 20), hash_ctas=self.hash_ctas or (1 << 20),
                                 gap_ms=gaps)
 
@@ -141,7 +154,7 @@ class SliceScheduler:
         self.native.begin(iteration)
 
     def hook(self, kind, layer):
-        if kind == "pre_ag":      # NCCL about to run: SMs idle
+        if kind == "pre_ag" or (kind == "pre_rs" and self.rs_gaps):  # NCCL about to run: SMs idle
             self.native.gap(self.ffx.GAP_SM_IDLE, self.step.train)
         elif kind in ("fwd", "bwd"):  # collective done: NVLink idle while the GEMMs run
             self.native.gap(self.ffx.GAP_LINK_IDLE, self.step.train)

@@ -27,7 +27,12 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
-    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    opts = None
+    if os.environ.get("FFX_NCCL_HIGH_PRIORITY"):
+        # TRAIN > STATE for the collectives too: NCCL's kernels on a
+        # high-priority stream outrank the snapshot's low-priority batches
+        opts = dist.ProcessGroupNCCL.Options(is_high_priority_stream=True)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local), pg_options=opts)
     from paper_2512_03644_b200 import ffx, ring
     from paper_2512_03644_b200.step import SliceScheduler, SyntheticStep, measure_overhead
     phi, d_ref = 8_030_261_248, 8
@@ -49,8 +54,10 @@ def main():
     ctx.set_target(targets[0])
     step = SyntheticStep(world)
     variants = [("fused", dict(copy_ctas=32)),
-                ("split", dict(copy_ctas=8, hash_ctas=64, copy_engine=True)),
-                ("split", dict(copy_ctas=8, hash_ctas=96, copy_engine=True))]
+                ("split", dict(copy_ctas=8, hash_ctas=96, copy_engine=True)),
+                ("split", dict(copy_ctas=8, hash_ctas=148, copy_engine=True)),
+                ("split", dict(copy_ctas=8, hash_ctas=0, copy_engine=True)),
+                ("split", dict(copy_ctas=8, hash_ctas=96, copy_engine=True, rs_gaps=True))]
     if os.environ.get("FFX_SWEEP_ALL"):
         variants = [("fused", dict(copy_ctas=c)) for c in (16, 32, 64)] + \
                    [("split", dict(copy_ctas=8, hash_ctas=h, copy_engine=True)) for h in (32, 48, 64, 96, 148)]
@@ -120,6 +127,7 @@ def main():
         r = measure_overhead(step, sched, steps=args.steps, warmup=2, it0=10 + 1000 * i)
         sched.close()
         out.append({"policy": r["policy"], "copy_ctas": kw.get("copy_ctas"), "hash_ctas": kw.get("hash_ctas"),
+                    "front": kw.get("front", 1.0), "rs_gaps": kw.get("rs_gaps", False),
                     "overhead_pct": r["overhead_pct"], "step_ms_without": r["step_ms_without"]})
     if rank == 0:
         print(json.dumps({"world": world, "steps_each": args.steps, "variants": out}))
