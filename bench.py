@@ -155,18 +155,21 @@ def cpu_ring(threads, bytes_per_thread, iters):
     return out
 
 
-def cpu_baseline_line(threads, bytes_per_thread, iters=2):
+def cpu_baseline_line(threads, bytes_per_thread, iters=4):
+    """The reference's own CPU path on a bounded sample (threads x bytes per
+    iteration, `iters` iterations: ~10-30 thread-seconds of work); medians."""
     res = cpu_ring(threads, bytes_per_thread, iters)
     if res is None:
         return None
-    take = min(r[0] for r in res)
-    store = min(r[1] for r in res)
-    restore = min(r[2] for r in res)
+    take = statistics.median(r[0] for r in res)
+    store = statistics.median(r[1] for r in res)
+    restore = statistics.median(r[2] for r in res)
     agg = threads * bytes_per_thread
     return {
         "value": round(agg / (take + store) / 1e9, 3), "unit": "GB/s", "cores": threads, "kind": "reference",
-        "sample": "%d threads x %d MiB per rank: HostSnapshots::take + NeighborBuffer::store (the snapshot); "
-                  "reference proj/src compiled -O3 into oracle/_ref" % (threads, bytes_per_thread >> 20),
+        "sample": "%d threads x %d MiB per rank x %d iterations (median): HostSnapshots::take + "
+                  "NeighborBuffer::store (the snapshot); reference proj/src compiled -O3 into oracle/_ref"
+                  % (threads, bytes_per_thread >> 20, iters),
         "stages_gbs": {"take": round(agg / take / 1e9, 3), "store": round(agg / store / 1e9, 3),
                        "restore": round(agg / restore / 1e9, 3)},
     }
@@ -508,7 +511,7 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            cpu = cpu_baseline_line(min(8, os.cpu_count() or 1), 128 << 20)
+            cpu = cpu_baseline_line(min(8, os.cpu_count() or 1), 256 << 20)
         except Exception as ex:  # reported, never fatal
             cpu = {"error": str(ex)}
 
