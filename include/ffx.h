@@ -291,6 +291,10 @@ int ffx_snapshot_target2(ffx_ctx* ctx, ffx_replica* target);
  * the switch fans out to both holders' slots (egress N instead of 2N).  The
  * reference has no double neighbour; this extends NeighborBuffer
  * (ckpt.cpp:77-105) and the adjacent-pair fallback (controller.cpp:162-167).
+ * Measured: a lone writer delivers both replicas at
+ * ~560 GB/s vs ~350 per copy for two unicast stores, but with every rank
+ * snapshotting at once the writer's own team copy loads its NVLink ingress
+ * (3N per GPU vs 2N), so ffx_snapshot_target2 is the faster ring default.
  * Sequence (one process per GPU; handles travel like replica handles, the
  * fds behind them are fetched from the exporting process by libffx):
  *   holders : ffx_replica_create_shared(origin)  -> export handle
