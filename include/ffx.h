@@ -117,7 +117,9 @@ typedef struct ffx_recovery_plan {
 
 /* replicas = 1 is the reference rule (neighbour path iff no lost role's ring
  * successor is lost).  replicas = 2 is the double-neighbour extension: a lost
- * role is served by the first surviving holder among dp+1, dp+2. */
+ * role is served by a surviving holder among dp+1, dp+2 -- roles with the
+ * fewest surviving holders first, each to its least-loaded one (ties: the
+ * nearest), so concurrent recoveries spread over the holders' NVLink. */
 int ffx_plan_recovery(const ffx_cluster_spec* spec, const uint32_t* failed_pods, uint32_t n_pods,
                       const ffx_role* failed_roles, uint32_t n_roles, uint64_t global_consistent,
                       uint64_t latest_fallback_round, uint32_t replicas, ffx_recovery_plan* out);
