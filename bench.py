@@ -440,6 +440,15 @@ def main():
         dist.all_gather_object(recs, rec)
         rec = recs[fail_rank]
 
+    # ---- ZeRO-1 full-state restore (configs[1], ckpt.cpp:140-167): the unique
+    # Adam shard from the holder + the redundant bf16 weights from a live peer
+    full = None
+    if world > 1:
+        try:
+            full = zero1_full_restore(ffx, torch, dist, R, world, rank, local, spec, barrier, stream)
+        except Exception as ex:  # reported, never fatal
+            full = {"error": repr(ex)}
+
     # ---- e2e: the reference-facing call with host buffers ---------------------
     e2e = None
     if not args.no_e2e:
@@ -530,7 +539,8 @@ def main():
                        "ring_stream": args.mode if world > 1 else "local"},
             "per_gpu_gbs": round(value / world, 3),
             "nvlink_frac_per_gpu": round(value / world / NVLINK_MEASURED_GBS, 4) if world > 1 else None,
-            "roofline": roof, "recovery": rec, "alt_ring_stream": alt, "llama3_8b": llama,
+            "roofline": roof, "recovery": rec, "full_state_restore": full, "alt_ring_stream": alt,
+            "llama3_8b": llama,
             "llama3_8b_failure_at_d": dfail,
             "llama3_70b_double_neighbour": seventy,
             "cpu_baseline": cpu, "e2e": e2e,
@@ -648,6 +658,66 @@ def seventy_leg(args, ffx, torch, dist, world, rank, local, barrier):
                                                      last, 0, replicas=1).kind,
             "plan_double_neighbour": plan.kind,
             "adjacent_pair_recovery": [x for x in recs if x]}
+
+
+def zero1_full_restore(ffx, torch, dist, R, world, rank, local, spec, barrier, stream):
+    """GPT-2 XL ZeRO-1: the weights (2 phi bf16 = 3.1 GB) are redundant across
+    the DP ring, so a replacement takes them from a live peer (plan
+    redundant_from) and only the unique Adam shard from its holder; one
+    CopyVerify launch gathers both, each part checked against its own
+    source's slice table (ffx_recover_full)."""
+    import pyoracle
+    wbytes = 2 * PHI_GPT2_XL
+    wdig = pyoracle.weights_init(42, 0, 0)
+    wptr, sptr = ctypes.c_void_p(), ctypes.c_void_p()
+    nsl = (wbytes + 4095) // 4096
+    ffx.check(ffx.lib.ffx_device_alloc(local, wbytes, ctypes.byref(wptr)), "device_alloc")
+    ffx.check(ffx.lib.ffx_device_alloc(local, nsl * 8, ctypes.byref(sptr)), "device_alloc")
+    w, sums = wptr.value, sptr.value
+    opened = []
+    try:
+        ffx.materialize(w, wdig, wbytes)
+        R.ctx.register(ffx.REGION_PARAMS, w, unique=False, nbytes=wbytes)
+        ffx.slice_checksums(w, 4096, sums, nbytes=wbytes)  # this rank as a live peer
+        torch.cuda.synchronize()
+        handles = [None] * world
+        dist.all_gather_object(handles, (ffx.ipc_export(w), ffx.ipc_export(sums)))
+        fail_rank = 1 % world
+        plan = ffx.plan_recovery(spec, [], [ffx.Role(fail_rank, 0, 0)], R.target.newest(), 0)
+        out = None
+        barrier()
+        if rank == fail_rank:
+            src = plan.redundant_from[0][1].dp  # the lowest live DP rank (controller.cpp:182-189)
+            pw, ps = ffx.ipc_open(handles[src][0]), ffx.ipc_open(handles[src][1])
+            opened = [pw, ps]
+            R.ctx.inject(ffx.FAULT_POISON_STATE)                  # the unique shard is gone
+            ffx.materialize(w, pyoracle.weights_init(7, 0, 0), wbytes)  # and so are the weights
+            it = R.target.newest()
+            index = 1  # registration order: the Adam blob, then the weights
+            runs = []
+            for _ in range(3):
+                rpt = R.ctx.recover_full([R.target], it, redundant=[(index, pw, ps)], stream=stream)
+                runs.append(rpt.seconds)
+            nb = R.n + wbytes
+            ok = (rpt.bad_slices == 0 and ffx.blob_is_sound(R.state[0]) and
+                  ffx.blob_first_bad(w, wbytes) == ffx.U64_MAX)
+            t = sorted(runs)[1]
+            out = {"unique_bytes": R.n, "redundant_bytes": wbytes, "weights_source_rank": src,
+                   "recovery_s": round(t, 5), "recovery_gbs": round(nb / t / 1e9, 1), "verified_bit_exact": bool(ok)}
+        barrier()
+        outs = [None] * world
+        dist.all_gather_object(outs, out)
+        return outs[fail_rank]
+    finally:
+        torch.cuda.synchronize()
+        for p in opened:
+            ffx.ipc_close(p)
+        barrier()
+        R.ctx.clear_regions()
+        for kind, t in zip([ffx.REGION_BLOB], R.state):
+            R.ctx.register(kind, t)
+        ffx.lib.ffx_device_free(local, ctypes.c_void_p(w))
+        ffx.lib.ffx_device_free(local, ctypes.c_void_p(sums))
 
 
 def seventy_mcast(args, ffx, torch, dist, world, rank, local, barrier, all_gather, spec, prefix, state, k):
