@@ -83,3 +83,30 @@ def test_small_snapshot_is_one_part_equal_to_the_single_frame(ffx):
         rep.destroy()
         me.close()
         holder.close()
+
+
+def test_frame_part_boundary_exactly_one_part(ffx):
+    # a payload of exactly FFX_FRAME_PART_BYTES is one frame; one byte more is two
+    spec = ffx.make_spec(d=2, phi=1 << 30, distributed=True)
+    holder = ffx.Context(0, spec, (1, 0, 0))
+    me = ffx.Context(0, spec, (0, 0, 0))
+    rep = holder.create_replica((0, 0, 0), PART + 1, 1)
+    view = me.open_replica(rep.export())
+    me.set_target(view)
+    t = torch.empty(PART + 1, dtype=torch.uint8, device="cuda")
+    ffx.materialize(t, orc.optimizer_init(9, 0, 0, 0, True))
+    try:
+        for n, parts in ((PART, 1), (PART + 1, 2)):
+            me.clear_regions()
+            me.register(ffx.REGION_BLOB, t, nbytes=n)
+            me.snapshot(n)
+            torch.cuda.synchronize()
+            n_out, p_out = ffx.ctypes.c_uint64(), ffx.ctypes.c_uint32()
+            ffx.check(ffx.lib.ffx_replica_export_frame_part(rep.ptr, n, 0, None, 0, ffx.ctypes.byref(n_out),
+                                                            ffx.ctypes.byref(p_out), None), "size query")
+            assert p_out.value == parts and n_out.value == 32 + min(n, PART)
+    finally:
+        view.destroy()
+        rep.destroy()
+        me.close()
+        holder.close()

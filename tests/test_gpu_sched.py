@@ -74,3 +74,42 @@ def test_sched_policies_commit_the_reference_frame(ffx, policy, weights):
         rep.destroy()
         origin.close()
         holder.close()
+
+
+def test_sched_zero_weight_gaps_and_idle_calls(ffx):
+    # measured gaps that are all but one empty: every byte goes through the one
+    # non-empty batch; finish() / gap() outside a step are no-ops
+    spec = ffx.make_spec(d=2, phi=64, distributed=True)
+    holder = ffx.Context(0, spec, (0, 0, 0))
+    origin = ffx.Context(0, spec, (1, 0, 0))
+    n = (1 << 20) + 5
+    rep = holder.create_replica((1, 0, 0), n, 2)
+    view = origin.open_replica(rep.export())
+    origin.set_target(view)
+    d = orc.optimizer_init(5, 1, 0, 0, True)
+    state = torch.empty(n, dtype=torch.uint8, device="cuda")
+    ffx.materialize(state, d)
+    origin.register(ffx.REGION_BLOB, state)
+    train = torch.cuda.Stream()
+    sched = ffx.Sched(origin, ffx.SCHED_SPLIT_CE, link_gaps=4, sm_gaps=4, gap_ms=[0.0, 0.0, 2.0, 0.0])
+    try:
+        sched.finish(train)                      # nothing in flight: no-op
+        sched.gap(ffx.GAP_LINK_IDLE, train)      # no step: no-op
+        sched.begin(3)
+        for _ in range(4):
+            sched.gap(ffx.GAP_SM_IDLE, train)
+            sched.gap(ffx.GAP_LINK_IDLE, train)
+        sched.finish(train)
+        train.synchronize()
+        assert rep.export_frame(3) == orc.pack_blob((1, 0, 0), 3, 1, orc.materialize(d, n))
+        with pytest.raises(ffx.InvalidArgument):
+            ffx.Sched(origin, 7, link_gaps=4)
+        with pytest.raises(ffx.InvalidArgument):
+            ffx.Sched(origin, ffx.SCHED_SPLIT, link_gaps=4, sm_gaps=0)
+    finally:
+        sched.destroy()
+        torch.cuda.synchronize()
+        view.destroy()
+        rep.destroy()
+        origin.close()
+        holder.close()
