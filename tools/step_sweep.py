@@ -53,11 +53,22 @@ def main():
                                       lambda r: r.export(), ctx.open_replica, all_gather)
     ctx.set_target(targets[0])
     step = SyntheticStep(world)
-    variants = [("fused", dict(copy_ctas=32)),
-                ("split", dict(copy_ctas=8, hash_ctas=96, copy_engine=True)),
-                ("split", dict(copy_ctas=8, hash_ctas=148, copy_engine=True)),
-                ("split", dict(copy_ctas=8, hash_ctas=0, copy_engine=True)),
-                ("split", dict(copy_ctas=8, hash_ctas=96, copy_engine=True, rs_gaps=True))]
+    variants = [("split", dict(copy_ctas=8, hash_ctas=96, copy_engine=True)),
+                ("split", dict(copy_ctas=8, hash_ctas=16, copy_engine=True, hash_in_gemm=True)),
+                ("split", dict(copy_ctas=8, hash_ctas=32, copy_engine=True, hash_in_gemm=True)),
+                ("split", dict(copy_ctas=8, hash_ctas=8, copy_engine=True, hash_in_gemm=True)),
+                ("split", dict(copy_ctas=8, hash_ctas=96, copy_engine=True))]
+
+    class GemmHash(SliceScheduler):
+        """Checksum batches alongside the GEMMs (link-idle gaps) on few SMs,
+        instead of in the SM-idle windows before the collectives."""
+
+        def hook(self, kind, layer):
+            if kind in ("fwd", "bwd"):
+                self.native.gap(self.ffx.GAP_SM_IDLE, self.step.train)
+                self.native.gap(self.ffx.GAP_LINK_IDLE, self.step.train)
+            elif kind == "opt":
+                self.native.finish(self.step.train)
     if os.environ.get("FFX_SWEEP_ALL"):
         variants = [("fused", dict(copy_ctas=c)) for c in (16, 32, 64)] + \
                    [("split", dict(copy_ctas=8, hash_ctas=h, copy_engine=True)) for h in (32, 48, 64, 96, 148)]
@@ -123,11 +134,14 @@ def main():
         out.append({"policy": what + " only (raw)", "overhead_pct": round(100 * (m - b) / b, 3),
                     "step_ms_without": round(b, 3)})
     for i, (policy, kw) in enumerate(variants):
-        sched = SliceScheduler(ctx, step, policy=policy, **kw)
+        kw = dict(kw)
+        cls = GemmHash if kw.pop("hash_in_gemm", False) else SliceScheduler
+        sched = cls(ctx, step, policy=policy, **kw)
         r = measure_overhead(step, sched, steps=args.steps, warmup=2, it0=10 + 1000 * i)
         sched.close()
         out.append({"policy": r["policy"], "copy_ctas": kw.get("copy_ctas"), "hash_ctas": kw.get("hash_ctas"),
                     "front": kw.get("front", 1.0), "rs_gaps": kw.get("rs_gaps", False),
+                    "hash_in_gemm": cls is GemmHash,
                     "overhead_pct": r["overhead_pct"], "step_ms_without": r["step_ms_without"]})
     if rank == 0:
         print(json.dumps({"world": world, "steps_each": args.steps, "variants": out}))
