@@ -9,13 +9,15 @@ rides in its gaps.
 
 Scheduling (reference semantics: STATE traffic only when no TRAIN chunk is
 queued, inversion bounded by one chunk -- sim_net.cpp:401-454,
-test_transport.cpp:173-197):
+test_transport.cpp:173-197), carried out by the native scheduler in libffx
+(ffx_sched_*; this module only reports the step's gaps to it):
   * the step runs on a high-priority stream, snapshot batches on a
     low-priority one with a capped CTA count, so the block scheduler prefers
     the step and a batch can delay TRAIN by at most its in-flight tasks;
-  * policy "fused": one fused copy+checksum batch per forward layer, gated on
-    an event recorded right after that layer's all-gather (NVLink goes quiet
-    while the GEMMs run);
+  * policy "fused": one fused copy+checksum batch per all-gather gap
+    (forward and backward), gated on an event recorded right after the
+    all-gather (NVLink goes quiet while the GEMMs run), sized by the measured
+    gap durations (calibrate());
   * policy "split": the copy (TMA copy-only kernel, few SMs -- or the copy
     engines) goes into those same compute gaps, while the checksum work
     (SM-heavy, HBM-only) is gated on events recorded right *before* each
