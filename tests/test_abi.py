@@ -197,3 +197,17 @@ def test_plan_recovery_double_neighbour_extension():
     # a single loss keeps the reference's ring successor
     assert {f[0].dp: f[3] for f in ffx.plan_recovery(spec, [6], [], 11, 5, replicas=2).forwards} == {6: 7}
     assert ffx.plan_recovery(spec, [2, 3, 4], [], 11, 5, replicas=2).kind == "fallback"
+
+
+def test_plain_c_host_compiles_against_the_abi(tmp_path):
+    # include/ffx.h is a C header: examples/c_snapshot.c (the whole backup /
+    # failure / recovery path from C99) builds and links against libffx.so
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = tmp_path / "c_snapshot"
+    r = subprocess.run(["gcc", "-std=c99", "-O2", "-Wall", "-Werror", "-I" + os.path.join(root, "include"),
+                        os.path.join(root, "examples", "c_snapshot.c"),
+                        "-L" + os.path.join(root, "paper_2512_03644_b200"), "-lffx",
+                        "-Wl,-rpath," + os.path.join(root, "paper_2512_03644_b200"), "-o", str(out)],
+                       capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
