@@ -488,11 +488,18 @@ struct Variant {
 constexpr Variant kVariants[] = {{3, 4, 1, 0, 2}, {2, 4, 2, 0, 1}, {3, 4, 2, 0, 1}, {6, 4, 1, 0, 1},
                                  {3, 4, 1, 0, 1}, {2, 8, 2, 0, 1}, {4, 4, 1, 1, 1}, {3, 4, 2, 1, 1},
                                  {6, 4, 1, 1, 1}, {2, 4, 1, 0, 2}, {4, 4, 1, 0, 1}, {2, 4, 1, 0, 4},
-                                 {2, 8, 1, 0, 2}};
+                                 {2, 8, 1, 0, 2}, {2, 4, 1, 0, 1}};
+
+// Checksum-only launches (split-policy hash batches, HashVerify, the whole
+// FNV's sub-segment pass) may use another configuration than the fused
+// kernel (FFX_HASH_VARIANT): no store traffic, so fewer stages / planes and
+// more resident warps; the warp task must stay the same size (RPL).
+int hash_variant();
 
 template <SliceMode M, bool kCommit>
 cudaError_t launch_mode(const SliceJob& job, uint32_t max_ctas, cudaStream_t stream) {
-  switch (variant()) {
+  const bool hash_only = M == SliceMode::Hash || M == SliceMode::HashVerify;
+  switch (hash_only ? hash_variant() : variant()) {
     case 1: return launch_t<2, 4, 2, false, M, kCommit>(job, max_ctas, stream);
     case 2: return launch_t<3, 4, 2, false, M, kCommit>(job, max_ctas, stream);
     case 3: return launch_t<6, 4, 1, false, M, kCommit>(job, max_ctas, stream);
@@ -505,6 +512,7 @@ cudaError_t launch_mode(const SliceJob& job, uint32_t max_ctas, cudaStream_t str
     case 10: return launch_t<4, 4, 1, false, M, kCommit>(job, max_ctas, stream);
     case 11: return launch_t<2, 4, 1, false, M, kCommit, 4>(job, max_ctas, stream);
     case 12: return launch_t<2, 8, 1, false, M, kCommit, 2>(job, max_ctas, stream);
+    case 13: return launch_t<2, 4, 1, false, M, kCommit>(job, max_ctas, stream);
     default: return launch_t<3, 4, 1, false, M, kCommit, 2>(job, max_ctas, stream);
   }
 }
@@ -529,6 +537,22 @@ const Variant& active_variant() {
 }  // namespace
 
 int task_rows() { return 32 * active_variant().RPL; }
+
+namespace {
+int hash_variant() {
+  static const int v = [] {
+    const char* e = std::getenv("FFX_HASH_VARIANT");
+    // default: 2 stages instead of 3 -- the checksum-only pipeline has no
+    // store to wait for; +10% hash-only throughput (3.63 vs 3.29 TB/s,
+    // profiles/r1_hash_variant_sweep.txt)
+    const int h = e ? std::atoi(e) : (variant() == 0 ? 9 : variant());
+    const int n = static_cast<int>(sizeof kVariants / sizeof kVariants[0]);
+    // same warp-task size as the fused kernel's jobs (finalize_job), else the fused variant
+    return (h >= 0 && h < n && kVariants[h].RPL == active_variant().RPL) ? h : variant();
+  }();
+  return v;
+}
+}  // namespace
 
 void finalize_job(SliceJob& job) {
   const uint64_t rows = static_cast<uint64_t>(task_rows());
@@ -588,7 +612,7 @@ bool encode_rows(CUtensorMap* map, const void* base, uint64_t slice_bytes, uint6
 }  // namespace
 
 // Give the (up to kTmaRegions) largest eligible regions 2-D tensor maps.
-void attach_tensor_maps(SliceJob& job, bool copy) {
+void attach_tensor_maps(SliceJob& job, bool copy, int kc_planes) {
   for (uint32_t r = 0; r < kMaxRegions; ++r) job.reg[r].tmap = -1;
   if (job.slice_bytes % 128 != 0 || job.slice_bytes > (1ull << 31)) return;
   int used = 0;
@@ -600,7 +624,7 @@ void attach_tensor_maps(SliceJob& job, bool copy) {
     const uint32_t rows = static_cast<uint32_t>(task_rows());
     if (!al || R.nfull < rows || R.nfull > (1ull << 31)) continue;
     if (R.dst2 != nullptr && reinterpret_cast<uintptr_t>(R.dst2) % 16 != 0) continue;
-    const uint32_t kc = static_cast<uint32_t>(active_variant().KC);
+    const uint32_t kc = static_cast<uint32_t>(kc_planes);
     if (job.slice_bytes % (128ull * kc) != 0) continue;
     if (!encode_rows(&job.maps[3 * used], R.src, job.slice_bytes, R.nfull, rows, kc)) continue;
     if (copy && !encode_rows(&job.maps[3 * used + 1], R.dst, job.slice_bytes, R.nfull, rows, kc)) continue;
@@ -614,7 +638,11 @@ void attach_tensor_maps(SliceJob& job, bool copy) {
 cudaError_t launch_slices(const SliceJob& job_in, SliceMode mode, bool commit, uint32_t max_ctas,
                           cudaStream_t stream) {
   SliceJob job = job_in;
-  attach_tensor_maps(job, mode == SliceMode::Copy || mode == SliceMode::CopyVerify);
+  const bool hash_only = mode == SliceMode::Hash || mode == SliceMode::HashVerify;
+  // the tensor maps' box depth follows the configuration this launch uses
+  const int vi = hash_only ? hash_variant() : variant();
+  const int nv = static_cast<int>(sizeof kVariants / sizeof kVariants[0]);
+  attach_tensor_maps(job, !hash_only, kVariants[(vi >= 0 && vi < nv) ? vi : 0].KC);
   // The refill of a stage is a generic-read -> async-write (WAR) sequence,
   // ordered by the warp barrier; the proxy fence is only required for
   // generic writes read by the async proxy (kept per task, optional per step).
