@@ -53,10 +53,9 @@ def main():
                                       lambda r: r.export(), ctx.open_replica, all_gather)
     ctx.set_target(targets[0])
     step = SyntheticStep(world)
-    variants = [("split", dict(copy_ctas=8, hash_ctas=96, copy_engine=True)),
-                ("split", dict(copy_ctas=8, hash_ctas=16, copy_engine=True, hash_in_gemm=True)),
-                ("split", dict(copy_ctas=8, hash_ctas=32, copy_engine=True, hash_in_gemm=True)),
-                ("split", dict(copy_ctas=8, hash_ctas=8, copy_engine=True, hash_in_gemm=True)),
+    variants = [("fused", dict(copy_ctas=32)),
+                ("split", dict(copy_ctas=8, hash_ctas=96, copy_engine=True)),
+                ("split", dict(copy_ctas=8, hash_ctas=64, copy_engine=True)),
                 ("split", dict(copy_ctas=8, hash_ctas=96, copy_engine=True))]
 
     class GemmHash(SliceScheduler):
