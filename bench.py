@@ -660,6 +660,30 @@ def seventy_leg(args, ffx, torch, dist, world, rank, local, barrier):
             "adjacent_pair_recovery": [x for x in recs if x]}
 
 
+def _restore_failed_rank(ffx, pyoracle, R, plan, handles, w, wbytes, stream, opened):
+    """The replacement's side of zero1_full_restore (returns a dict, never raises)."""
+    try:
+        src = plan.redundant_from[0][1].dp  # the lowest live DP rank (controller.cpp:182-189)
+        pw, ps = ffx.ipc_open(handles[src][0]), ffx.ipc_open(handles[src][1])
+        opened += [pw, ps]
+        R.ctx.inject(ffx.FAULT_POISON_STATE)                        # the unique shard is gone
+        ffx.materialize(w, pyoracle.weights_init(7, 0, 0), wbytes)  # and so are the weights
+        it = R.target.newest()
+        index = 1  # registration order: the Adam blob, then the weights
+        runs = []
+        for _ in range(3):
+            rpt = R.ctx.recover_full([R.target], it, redundant=[(index, pw, ps)], stream=stream)
+            runs.append(rpt.seconds)
+        ok = (rpt.bad_slices == 0 and ffx.blob_is_sound(R.state[0]) and
+              ffx.blob_first_bad(w, wbytes) == ffx.U64_MAX)
+        t = sorted(runs)[1]
+        return {"unique_bytes": R.n, "redundant_bytes": wbytes, "weights_source_rank": src,
+                "recovery_s": round(t, 5), "recovery_gbs": round((R.n + wbytes) / t / 1e9, 1),
+                "verified_bit_exact": bool(ok)}
+    except Exception as ex:
+        return {"error": repr(ex)}
+
+
 def zero1_full_restore(ffx, torch, dist, R, world, rank, local, spec, barrier, stream):
     """GPT-2 XL ZeRO-1: the weights (2 phi bf16 = 3.1 GB) are redundant across
     the DP ring, so a replacement takes them from a live peer (plan
@@ -687,23 +711,8 @@ def zero1_full_restore(ffx, torch, dist, R, world, rank, local, spec, barrier, s
         out = None
         barrier()
         if rank == fail_rank:
-            src = plan.redundant_from[0][1].dp  # the lowest live DP rank (controller.cpp:182-189)
-            pw, ps = ffx.ipc_open(handles[src][0]), ffx.ipc_open(handles[src][1])
-            opened = [pw, ps]
-            R.ctx.inject(ffx.FAULT_POISON_STATE)                  # the unique shard is gone
-            ffx.materialize(w, pyoracle.weights_init(7, 0, 0), wbytes)  # and so are the weights
-            it = R.target.newest()
-            index = 1  # registration order: the Adam blob, then the weights
-            runs = []
-            for _ in range(3):
-                rpt = R.ctx.recover_full([R.target], it, redundant=[(index, pw, ps)], stream=stream)
-                runs.append(rpt.seconds)
-            nb = R.n + wbytes
-            ok = (rpt.bad_slices == 0 and ffx.blob_is_sound(R.state[0]) and
-                  ffx.blob_first_bad(w, wbytes) == ffx.U64_MAX)
-            t = sorted(runs)[1]
-            out = {"unique_bytes": R.n, "redundant_bytes": wbytes, "weights_source_rank": src,
-                   "recovery_s": round(t, 5), "recovery_gbs": round(nb / t / 1e9, 1), "verified_bit_exact": bool(ok)}
+            # errors stay on this rank: every rank still meets the collectives below
+            out = _restore_failed_rank(ffx, pyoracle, R, plan, handles, w, wbytes, stream, opened)
         barrier()
         outs = [None] * world
         dist.all_gather_object(outs, out)
