@@ -136,6 +136,19 @@ __device__ __forceinline__ void tensor_store3(const CUtensorMap* map, int y, int
                ::"l"(reinterpret_cast<uint64_t>(map)), "r"(0), "r"(y), "r"(z), "r"(src)
                : "memory");
 }
+// The same store with an L2 eviction-priority hint (evict_first: the payload
+// is written once and not read back soon) -- FFX_STORE_HINT experiment.
+__device__ __forceinline__ void tensor_store3_hint(const CUtensorMap* map, int y, int z, uint32_t src,
+                                                   uint64_t policy) {
+  asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.tile.bulk_group.L2::cache_hint [%0, {%1, %2, %3}], [%4], %5;"
+               ::"l"(reinterpret_cast<uint64_t>(map)), "r"(0), "r"(y), "r"(z), "r"(src), "l"(policy)
+               : "memory");
+}
+__device__ __forceinline__ uint64_t evict_first_policy() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_read_all() {
   asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
@@ -312,8 +325,14 @@ __global__ void __launch_bounds__(W * 32) slice_kernel(const __grid_constant__ S
               tensor_store(mdst, k * C, y, tile);
               if (dual) tensor_store(mdst2, k * C, y, tile);  // double neighbour: read once, write twice
             } else {
-              tensor_store3(mdst, y, k * KC, tile);
-              if (dual) tensor_store3(mdst2, y, k * KC, tile);
+              if (job.store_hint) {
+                const uint64_t pol = evict_first_policy();
+                tensor_store3_hint(mdst, y, k * KC, tile, pol);
+                if (dual) tensor_store3_hint(mdst2, y, k * KC, tile, pol);
+              } else {
+                tensor_store3(mdst, y, k * KC, tile);
+                if (dual) tensor_store3(mdst2, y, k * KC, tile);
+              }
             }
             bulk_commit();
           }
@@ -658,6 +677,8 @@ cudaError_t launch_slices(const SliceJob& job_in, SliceMode mode, bool commit, u
     return e ? static_cast<uint32_t>(std::atoi(e)) : 0u;
   }();
   job.claim_order = order;
+  static const uint32_t hint = std::getenv("FFX_STORE_HINT") != nullptr ? 1u : 0u;
+  job.store_hint = hint;
   switch (mode) {
     case SliceMode::Hash:
       return commit ? launch_mode<SliceMode::Hash, true>(job, max_ctas, stream)
