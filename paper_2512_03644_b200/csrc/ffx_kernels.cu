@@ -156,39 +156,66 @@ __global__ void check_kernel(const uint8_t* blob, uint64_t bytes, unsigned long 
 // and h_{i+1} = h_i * P + ((l_i ^ b_i) - l_i) * P, so once the low-byte
 // trajectory is known each sub-segment is an affine map h -> A*h + B.
 //  phase 1  fnv_spec_kernel: per segment (K sub-segments), start values
-//           l = 0..127 simulated in parallel (two per 32-bit lane), recording
-//           the state at every sub-segment end -> T[sub][start].  Bit 7 never
-//           feeds lower bits: x ^ 0x80 = x + 128 and 128 * 0xB3 = 128 (mod 256),
-//           so the trajectory from l ^ 0x80 is the one from l with bit 7
-//           flipped at every step -- T[l] = T7[l & 127] ^ (l & 128), half the
-//           speculation of all 256 starts.
+//           l = 0..63 simulated in parallel (two per 32-bit lane), recording
+//           the state at every sub-segment end -> T[sub][start] and the
+//           running parity of bit 6 of the data.  Bit 7 never feeds lower
+//           bits: x ^ 0x80 = x + 128 and 128 * 0xB3 = 128 (mod 256), so the
+//           trajectory from l ^ 0x80 is the one from l with bit 7 flipped at
+//           every step.  Bit 6 only feeds bit 7: from l ^ 0x40 the trajectory
+//           keeps bits 0-5, complements bit 6, and flips bit 7 whenever
+//           bit6(l_i ^ b_i) == bit6(l_{i+1}); those flips telescope to
+//           (n & 1) ^ bit6(l_0) ^ bit6(l_n) ^ parity(bit 6 of the n bytes), so
+//           64 simulated starts give all 256 (spec_lookup): a quarter of the
+//           naive speculation.
 //  phase 2  fnv_walk_kernel: chain segment start states l through T.
 //  phase 3  fnv_init_kernel + slice_kernel(Hash, init_state=l_sub):
 //           F_sub = FNV of the sub-segment started from h = l_sub.
 //  phase 4  fnv_combine_kernel: h = fold_sub (h - l_sub) * P^len_sub + F_sub.
 
 constexpr int kSpecK = 8;        // sub-segments per segment
-constexpr int kSpecThreads = 8;  // threads per segment: 16 of the 128 start values each
-constexpr int kSpecTab = 128;    // table entries per sub-segment (bit 7 by symmetry)
+constexpr int kSpecRegs = 8;     // packed registers per thread: 2 start values each (4 threads: 7.5 ms; 8: 9.1)
+constexpr int kSpecThreads = 64 / (2 * kSpecRegs);  // threads per segment (64 simulated starts)
+constexpr int kSpecTab = 64;     // table entries per sub-segment (bits 6 and 7 derived)
+
+// Full end state for start l from the 64-entry table of starts l & 63:
+// bit 7 is symmetric (see above); for bit 6 the trajectory from l0 ^ 0x40
+// is that from l0 with bit 6 complemented and bit 7 flipped d times, and the
+// flips telescope to d = (n & 1) ^ bit6(end state) ^ (parity of bit 6 over
+// the n data bytes) -- so 64 simulated starts give all 256.
+__device__ __forceinline__ uint32_t spec_lookup(const uint8_t* Tu, uint32_t odd, uint32_t l) {
+  const uint32_t a = Tu[l & 63u];
+  uint32_t r = a;
+  if (l & 0x40u) r ^= 0x40u ^ (((odd ^ (a >> 6)) & 1u) << 7);
+  return r ^ (l & 0x80u);
+}
+
+// bytes from the start of sub-segment u's segment through the end of u
+__device__ __forceinline__ uint64_t spec_span(uint64_t u, uint64_t Ls, uint64_t len) {
+  const uint64_t seg0 = (u / kSpecK) * kSpecK * Ls;
+  return umin64((u + 1) * Ls, len) - seg0;
+}
 
 __global__ void fnv_spec_kernel(const uint8_t* data, uint64_t len, uint64_t Ls, uint64_t nsub,
-                                uint8_t* T) {
+                                uint8_t* T, uint8_t* P) {
   const uint64_t gt = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
   const uint64_t seg = gt / kSpecThreads;
   const int t = static_cast<int>(gt % kSpecThreads);
   const uint64_t sub0 = seg * kSpecK;
   if (sub0 >= nsub) return;
   const uint64_t sub1 = min(sub0 + kSpecK, nsub);
-  uint32_t x[8];
+  constexpr int R = kSpecRegs;
+  uint32_t x[R];
 #pragma unroll
-  for (int r = 0; r < 8; ++r)
-    x[r] = static_cast<uint32_t>(t * 16 + 2 * r) | (static_cast<uint32_t>(t * 16 + 2 * r + 1) << 16);
+  for (int r = 0; r < R; ++r)
+    x[r] = static_cast<uint32_t>(t * 2 * R + 2 * r) | (static_cast<uint32_t>(t * 2 * R + 2 * r + 1) << 16);
   const bool al = aligned16(data);
+  uint32_t par = 0;  // thread 0: running parity of bit 6 of the data bytes (bits 6, 14, 22, 30)
   for (uint64_t u = sub0; u < sub1; ++u) {
     const uint64_t b0 = u * Ls;
     const uint64_t b1 = min(b0 + Ls, len);
     for (uint64_t o = b0; o < b1; o += 16) {
-      const uint4 v = load16(data, o, b1, al);
+      const uint4 v = load16(data, o, b1, al);  // zero-filled past b1: parity unaffected
+      if (t == 0) par ^= v.x ^ v.y ^ v.z ^ v.w;
       const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
       const int n = static_cast<int>(umin64(16, b1 - o));
       if (n == 16) {
@@ -196,57 +223,62 @@ __global__ void fnv_spec_kernel(const uint8_t* data, uint64_t len, uint64_t Ls, 
         for (int q = 0; q < 16; ++q) {
           const uint32_t bb = __byte_perm(w4[q >> 2], 0u, 0x4040 + 0x0101 * (q & 3));
 #pragma unroll
-          for (int r = 0; r < 8; ++r) x[r] = ((x[r] & 0x00FF00FFu) ^ bb) * 0xB3u;
+          for (int r = 0; r < R; ++r) x[r] = ((x[r] & 0x00FF00FFu) ^ bb) * 0xB3u;
         }
       } else {
         for (int q = 0; q < n; ++q) {
           const uint32_t bb = __byte_perm(w4[q >> 2], 0u, 0x4040 + 0x0101 * (q & 3));
 #pragma unroll
-          for (int r = 0; r < 8; ++r) x[r] = ((x[r] & 0x00FF00FFu) ^ bb) * 0xB3u;
+          for (int r = 0; r < R; ++r) x[r] = ((x[r] & 0x00FF00FFu) ^ bb) * 0xB3u;
         }
       }
     }
-    uint32_t out[4];
+    uint32_t out[R / 2];
 #pragma unroll
-    for (int r = 0; r < 4; ++r) {
+    for (int r = 0; r < R / 2; ++r) {
       const uint32_t a = x[2 * r], b = x[2 * r + 1];
       out[r] = (a & 0xffu) | (((a >> 16) & 0xffu) << 8) | ((b & 0xffu) << 16) | (((b >> 16) & 0xffu) << 24);
     }
-    reinterpret_cast<uint4*>(T + u * kSpecTab)[t] = make_uint4(out[0], out[1], out[2], out[3]);
+#pragma unroll
+    for (int r = 0; r < R / 2; ++r) reinterpret_cast<uint32_t*>(T + u * kSpecTab)[t * (R / 2) + r] = out[r];
+    // P[u] = (n & 1) ^ parity of bit 6 through the end of u: the "odd" input of spec_lookup
+    if (t == 0) P[u] = static_cast<uint8_t>((__popc(par & 0x40404040u) ^ spec_span(u, Ls, len)) & 1u);
   }
 }
 
 // One CTA: walk segment ends; lam_seg[s] = low byte at segment s start.
-__global__ void fnv_walk_kernel(const uint8_t* T, uint64_t nsub, uint64_t nseg, uint32_t l0,
+__global__ void fnv_walk_kernel(const uint8_t* T, const uint8_t* P, uint64_t nsub, uint64_t nseg, uint32_t l0,
                                 uint8_t* lam_seg) {
   constexpr int kV = kSpecTab / 16;  // uint4 per table
-  __shared__ uint4 tab[64][kV];      // 64 segment-end tables
+  __shared__ uint4 tab[128][kV];     // 128 segment-end tables
+  __shared__ uint8_t odd[128];
   uint32_t l = l0;
-  for (uint64_t s0 = 0; s0 < nseg; s0 += 64) {
-    const uint64_t cnt = umin64(64, nseg - s0);
+  for (uint64_t s0 = 0; s0 < nseg; s0 += 128) {
+    const uint64_t cnt = umin64(128, nseg - s0);
     __syncthreads();
     for (uint64_t i = threadIdx.x; i < cnt * kV; i += blockDim.x) {
       const uint64_t s = s0 + i / kV;
       const uint64_t last = umin64(s * kSpecK + kSpecK, nsub) - 1;
       tab[i / kV][i % kV] = reinterpret_cast<const uint4*>(T + last * kSpecTab)[i % kV];
+      if (i % kV == 0) odd[i / kV] = P[last];
     }
     __syncthreads();
     if (threadIdx.x == 0) {
       for (uint64_t i = 0; i < cnt; ++i) {
         lam_seg[s0 + i] = static_cast<uint8_t>(l);
-        l = reinterpret_cast<const uint8_t*>(tab[i])[l & 127u] ^ (l & 128u);
+        l = spec_lookup(reinterpret_cast<const uint8_t*>(tab[i]), odd[i], l);
       }
     }
   }
 }
 
-__global__ void fnv_init_kernel(const uint8_t* T, const uint8_t* lam_seg, uint64_t nsub,
+__global__ void fnv_init_kernel(const uint8_t* T, const uint8_t* P, const uint8_t* lam_seg, uint64_t nsub,
                                 uint64_t* init) {
   for (uint64_t u = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; u < nsub;
        u += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
     const uint64_t seg = u / kSpecK;
     const uint32_t ls = lam_seg[seg];
-    init[u] = (u % kSpecK == 0) ? ls : (T[(u - 1) * kSpecTab + (ls & 127u)] ^ (ls & 128u));
+    init[u] = (u % kSpecK == 0) ? ls : spec_lookup(T + (u - 1) * kSpecTab, P[u - 1], ls);
   }
 }
 
@@ -348,12 +380,13 @@ cudaError_t whole_fnv(const uint8_t* data, uint64_t len, uint64_t h0, uint64_t* 
   const uint64_t last_len = len - (nsub - 1) * Ls;
 
   uint8_t* scratch = nullptr;
-  const uint64_t offT = 0, offLam = align_up(nsub * kSpecTab, 256),
+  const uint64_t offT = 0, offP = align_up(nsub * kSpecTab, 256), offLam = offP + align_up(nsub, 256),
                  offInit = offLam + align_up(nseg, 256), offF = offInit + align_up(nsub * 8, 256),
                  offOut = offF + align_up(nsub * 8, 256), total = offOut + 256;
   cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&scratch), total, stream);
   if (e != cudaSuccess) return e;
   uint8_t* T = scratch + offT;
+  uint8_t* P = scratch + offP;
   uint8_t* lam = scratch + offLam;
   uint64_t* init = reinterpret_cast<uint64_t*>(scratch + offInit);
   uint64_t* F = reinterpret_cast<uint64_t*>(scratch + offF);
@@ -361,9 +394,9 @@ cudaError_t whole_fnv(const uint8_t* data, uint64_t len, uint64_t h0, uint64_t* 
 
   const uint64_t spec_threads = nseg * kSpecThreads;
   fnv_spec_kernel<<<static_cast<unsigned>((spec_threads + 255) / 256), 256, 0, stream>>>(
-      data, len, Ls, nsub, T);
-  fnv_walk_kernel<<<1, 512, 0, stream>>>(T, nsub, nseg, static_cast<uint32_t>(h0 & 0xff), lam);
-  fnv_init_kernel<<<grid_for(nsub, 256), 256, 0, stream>>>(T, lam, nsub, init);
+      data, len, Ls, nsub, T, P);
+  fnv_walk_kernel<<<1, 512, 0, stream>>>(T, P, nsub, nseg, static_cast<uint32_t>(h0 & 0xff), lam);
+  fnv_init_kernel<<<grid_for(nsub, 256), 256, 0, stream>>>(T, P, lam, nsub, init);
   // The high bits of the true state enter only through the affine combine, so
   // each sub-segment starts from its low byte alone.
   SliceJob job{};
