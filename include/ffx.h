@@ -124,6 +124,55 @@ int ffx_plan_recovery(const ffx_cluster_spec* spec, const uint32_t* failed_pods,
                       const ffx_role* failed_roles, uint32_t n_roles, uint64_t global_consistent,
                       uint64_t latest_fallback_round, uint32_t replicas, ffx_recovery_plan* out);
 
+/* ---- controller state that drives recovery -----------
+ * Host-only (no GPU needed), thread-safe per object.  Timestamps are
+ * caller-supplied nanoseconds (rt::Nanos): simulated or ffx_now_ns(). */
+
+int64_t ffx_now_ns(void); /* CLOCK_MONOTONIC */
+
+/* ctl::HeartbeatTable (controller.hpp:56-101, controller.cpp:16-77). */
+typedef struct ffx_heartbeats ffx_heartbeats;
+typedef struct ffx_heartbeat_slot {
+  uint32_t enrolled, failed;
+  int64_t last_seen_ns;
+  uint64_t last_iteration;
+} ffx_heartbeat_slot;
+/* ControllerConfig{heartbeat_interval, miss_threshold} (controller.hpp:31-34) */
+int ffx_heartbeats_create(uint32_t pods, int64_t interval_ns, uint32_t miss_threshold, ffx_heartbeats** out);
+int ffx_heartbeats_destroy(ffx_heartbeats* h);
+/* enroll: registration / substitution re-activates the slot (FFX_ERANGE past
+ * the pod count, as slots_.at throws). */
+int ffx_heartbeats_enroll(ffx_heartbeats* h, uint32_t node, uint64_t iteration, int64_t now_ns);
+/* observe: unknown / already-failed senders and regressed iterations are
+ * counted (ffx_heartbeats_counters), never an error. */
+int ffx_heartbeats_observe(ffx_heartbeats* h, uint32_t node, uint64_t iteration, int64_t now_ns);
+/* sweep: pods silent for more than interval * miss_threshold, newly marked
+ * failed, in node order.  Writes min(n, cap) ids; *n_dead = n. */
+int ffx_heartbeats_sweep(ffx_heartbeats* h, int64_t now_ns, uint32_t* dead, uint32_t cap, uint32_t* n_dead);
+int ffx_heartbeats_mark_failed(ffx_heartbeats* h, uint32_t node);
+int ffx_heartbeats_query(ffx_heartbeats* h, uint32_t node, ffx_heartbeat_slot* out);
+int ffx_heartbeats_counters(ffx_heartbeats* h, uint64_t* unknown, uint64_t* late, uint64_t* regressed);
+
+/* ctl::IterationLedger (controller.hpp:106-130, controller.cpp:81-121). */
+struct ffx_replica;
+typedef struct ffx_ledger ffx_ledger;
+int ffx_ledger_create(const ffx_cluster_spec* spec, ffx_ledger** out);
+int ffx_ledger_destroy(ffx_ledger* g);
+/* Monotone per worker; FFX_ERANGE for a role outside the grid (ProtocolError). */
+int ffx_ledger_record(ffx_ledger* g, ffx_role role, uint64_t iteration);
+/* Minimum over the whole grid; 0 until every worker has recorded. */
+uint64_t ffx_ledger_global_consistent(ffx_ledger* g);
+/* Minimum over DP group pp * tensor_parallel + tp (absent members = 0). */
+uint64_t ffx_ledger_group_latest(ffx_ledger* g, uint32_t dp_group);
+uint64_t ffx_ledger_worker_latest(ffx_ledger* g, ffx_role role);
+/* Post-recovery reset: every worker at `iteration`. */
+int ffx_ledger_rebase(ffx_ledger* g, uint64_t iteration);
+/* The CkptRecord after a completed replica (wire.hpp:85-90): record the
+ * origin of the replica `held` at its newest COMMITTED iteration (a slot
+ * still being written never counts).  *recorded = that iteration, or 0 when
+ * nothing is committed yet (no record made). */
+int ffx_ledger_record_replica(ffx_ledger* g, struct ffx_replica* held, uint64_t* recorded);
+
 /* ---- sizing: the state partitioner's rules ------------------------------- */
 
 int ffx_razor(const ffx_cluster_spec* spec, ffx_uniqueness_plan* out); /* ckpt.cpp:13-21 */

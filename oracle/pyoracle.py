@@ -174,7 +174,142 @@ def ref_lib():
     r.ref_optimizer_init.argtypes = [_u64, ctypes.c_uint16, ctypes.c_uint16, ctypes.c_uint16, ctypes.c_int, _P]
     r.ref_optimizer_at.restype = ctypes.c_int
     r.ref_optimizer_at.argtypes = [_u64] + [ctypes.c_uint16] * 3 + [ctypes.c_uint32] * 4 + [_u64, ctypes.c_int, _P]
+    if hasattr(r, "ref_hb_create"):  # controller state machines (controller.cpp:16-121, :144-209)
+        i64, u32, u16 = ctypes.c_int64, ctypes.c_uint32, ctypes.c_uint16
+        r.ref_hb_create.restype = _P
+        r.ref_hb_create.argtypes = [u32, i64, u32]
+        r.ref_hb_free.argtypes = [_P]
+        r.ref_hb_enroll.argtypes = [_P, u32, _u64, i64]
+        r.ref_hb_observe.argtypes = [_P, u32, _u64, i64]
+        r.ref_hb_sweep.restype = u32
+        r.ref_hb_sweep.argtypes = [_P, i64, ctypes.POINTER(u32), u32]
+        r.ref_hb_mark_failed.argtypes = [_P, u32]
+        r.ref_hb_query.argtypes = [_P, u32, ctypes.POINTER(i64)]
+        r.ref_hb_counters.argtypes = [_P, ctypes.POINTER(_u64)]
+        r.ref_ledger_create.restype = _P
+        r.ref_ledger_create.argtypes = [u32] * 5
+        r.ref_ledger_free.argtypes = [_P]
+        r.ref_ledger_record.argtypes = [_P, u16, u16, u16, _u64]
+        r.ref_ledger_global.restype = _u64
+        r.ref_ledger_global.argtypes = [_P]
+        r.ref_ledger_group.restype = _u64
+        r.ref_ledger_group.argtypes = [_P, u32]
+        r.ref_ledger_worker.restype = _u64
+        r.ref_ledger_worker.argtypes = [_P, u16, u16, u16]
+        r.ref_ledger_rebase.argtypes = [_P, _u64]
+        r.ref_plan_recovery.restype = ctypes.c_long
+        r.ref_plan_recovery.argtypes = [u32] * 5 + [ctypes.c_int, _u64, ctypes.POINTER(u32), u32,
+                                                    ctypes.POINTER(u16), u32, _u64, _u64,
+                                                    ctypes.POINTER(i64), ctypes.c_long]
     return r
+
+
+def ref_plan_recovery(r, nodes, gpn, d, p, t, distributed, phi, failed_pods, failed_roles,
+                      global_consistent, latest_fallback):
+    """The reference's own ctl::plan_recovery through ref_shim, decoded into
+    the dict layout of plan_recovery() below."""
+    pods = (ctypes.c_uint32 * max(1, len(failed_pods)))(*failed_pods)
+    flat = [x for role in failed_roles for x in role]
+    roles = (ctypes.c_uint16 * max(1, len(flat)))(*flat)
+    cap = 64 + 16 * (nodes * gpn + len(failed_roles) + len(failed_pods) * gpn)
+    out = (ctypes.c_int64 * cap)()
+    n = r.ref_plan_recovery(nodes, gpn, d, p, t, int(distributed), phi, pods, len(failed_pods), roles,
+                            len(failed_roles), global_consistent, latest_fallback, out, cap)
+    if n < 0:
+        raise RuntimeError("reference plan_recovery threw")
+    w = list(out[:n])
+    pos = 2
+
+    def take(k):
+        nonlocal pos
+        cnt = w[pos]
+        pos += 1
+        items = [tuple(w[pos + i * k:pos + (i + 1) * k]) for i in range(cnt)]
+        pos += cnt * k
+        return items
+
+    plan = {"kind": "fallback" if w[0] else "neighbor", "resume": w[1]}
+    plan["failed_pods"] = [x[0] for x in take(1)]
+    plan["failed_roles"] = take(3)
+    plan["lazy"] = take(3)
+    plan["forwards"] = [((f[0], f[1], f[2]), f[3], f[4]) for f in take(5)]
+    plan["redundant_from"] = [((x[0], x[1], x[2]), (x[3], x[4], x[5])) for x in take(6)]
+    return plan
+
+
+# ---- controller.cpp:16-121, restated (HeartbeatTable, IterationLedger) ------
+
+class HeartbeatTable:
+    """controller.cpp:16-77: one slot per pod; sweep declares pods silent for
+    more than interval * miss_threshold."""
+
+    def __init__(self, pods, interval=1_000_000_000, miss_threshold=3):
+        self.slots = [dict(enrolled=False, failed=False, last_seen=0, last_iteration=0) for _ in range(pods)]
+        self.limit = interval * miss_threshold
+        self.unknown = self.late = self.regressed = 0
+
+    def enroll(self, node, it, now):  # :21-28 (slots_.at)
+        s = self.slots[node]
+        s.update(enrolled=True, failed=False, last_seen=now, last_iteration=it)
+
+    def observe(self, node, it, now):  # :30-44
+        if node >= len(self.slots) or not self.slots[node]["enrolled"]:
+            self.unknown += 1
+            return
+        s = self.slots[node]
+        if s["failed"]:
+            self.late += 1
+            return
+        if it < s["last_iteration"]:
+            self.regressed += 1
+        s.update(last_iteration=it, last_seen=now)
+
+    def sweep(self, now):  # :46-58
+        dead = []
+        for i, s in enumerate(self.slots):
+            if not s["enrolled"] or s["failed"]:
+                continue
+            if now - s["last_seen"] > self.limit:
+                s["failed"] = True
+                dead.append(i)
+        return dead
+
+    def mark_failed(self, node):  # :60-62
+        self.slots[node]["failed"] = True
+
+
+class IterationLedger:
+    """controller.cpp:81-121: per-worker latest recoverable iteration; the
+    global consistent one is the minimum over world_size() workers."""
+
+    def __init__(self, nodes, gpn, d, p, t):
+        self.world, self.d, self.p, self.t = nodes * gpn, d, p, t
+        self.latest = {}
+
+    def record(self, role, it):  # :83-90 (ProtocolError -> ValueError)
+        dp, pp, tp = role
+        if dp >= self.d or pp >= self.p or tp >= self.t:
+            raise ValueError("role outside the grid")
+        self.latest[role] = max(self.latest.get(role, 0), it)
+
+    def global_consistent(self):  # :92-97
+        if len(self.latest) < self.world:
+            return 0
+        return min(self.latest.values())
+
+    def group_latest(self, g):  # :99-110
+        pp, tp = (g // self.t) & 0xFFFF, (g % self.t) & 0xFFFF
+        vals = [self.latest.get((dp, pp, tp), 0) for dp in range(self.d)]
+        return min(vals) if vals else 0
+
+    def worker_latest(self, role):  # :112-115
+        return self.latest.get(tuple(role), 0)
+
+    def rebase(self, it):  # :117-121
+        for dp in range(self.d):
+            for pp in range(self.p):
+                for tp in range(self.t):
+                    self.latest[(dp, pp, tp)] = it
 
 
 # ---- controller.cpp:144-209, restated (small cases only) ---------------------

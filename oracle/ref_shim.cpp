@@ -1,5 +1,6 @@
 // ref_shim.cpp -- extern "C" entry points onto the UNMODIFIED reference
-// library (proj/src/{hash,storage,ckpt,evolution,domain}.cpp), compiled by
+// library (proj/src/{hash,storage,ckpt,evolution,domain,dataloader,
+// controller + its network-stack deps}.cpp), compiled by
 // oracle/Makefile into oracle/_ref/libftsim_ref.so.
 //
 // TEST INFRASTRUCTURE ONLY: used by oracle/gen_golden.py to produce the golden
@@ -14,6 +15,8 @@
 #include <vector>
 
 #include "ftsim/ckpt.hpp"
+#include "ftsim/controller.hpp"
+#include "ftsim/transport.hpp"
 #include "ftsim/dataloader.hpp"
 #include "ftsim/evolution.hpp"
 #include "ftsim/hash.hpp"
@@ -213,4 +216,142 @@ int ref_ring_run(void* h, std::uint64_t iteration, double* secs) {
   return 0;
 }
 
+
+// ---- the controller's state machines (controller.cpp:16-121, :144-209) -----
+// Thin handles onto ctl::HeartbeatTable / ctl::IterationLedger / plan_recovery
+// for the parity tests of libffx's ffx_heartbeats / ffx_ledger / plan.
+
+void* ref_hb_create(std::uint32_t pods, std::int64_t interval_ns, std::uint32_t miss) {
+  ctl::ControllerConfig cfg;
+  cfg.heartbeat_interval = interval_ns;
+  cfg.miss_threshold = miss;
+  return new ctl::HeartbeatTable(pods, cfg);
+}
+void ref_hb_free(void* h) { delete static_cast<ctl::HeartbeatTable*>(h); }
+int ref_hb_enroll(void* h, std::uint32_t node, std::uint64_t it, std::int64_t now) {
+  try {
+    static_cast<ctl::HeartbeatTable*>(h)->enroll(node, it, now);
+    return 0;
+  } catch (const std::out_of_range&) {
+    return -1;
+  }
+}
+void ref_hb_observe(void* h, std::uint32_t node, std::uint64_t it, std::int64_t now) {
+  static_cast<ctl::HeartbeatTable*>(h)->observe(node, it, now);
+}
+std::uint32_t ref_hb_sweep(void* h, std::int64_t now, std::uint32_t* dead, std::uint32_t cap) {
+  const auto v = static_cast<ctl::HeartbeatTable*>(h)->sweep(now);
+  for (std::uint32_t i = 0; i < v.size() && i < cap; ++i) dead[i] = v[i];
+  return static_cast<std::uint32_t>(v.size());
+}
+int ref_hb_mark_failed(void* h, std::uint32_t node) {
+  try {
+    static_cast<ctl::HeartbeatTable*>(h)->mark_failed(node);
+    return 0;
+  } catch (const std::out_of_range&) {
+    return -1;
+  }
+}
+// out = {enrolled, failed, last_seen, last_iteration}; -1 where the last_*
+// accessors throw (enrolled/failed are still written).
+int ref_hb_query(void* h, std::uint32_t node, std::int64_t* out) {
+  auto* t = static_cast<ctl::HeartbeatTable*>(h);
+  out[0] = t->enrolled(node);
+  out[1] = t->failed(node);
+  try {
+    out[2] = t->last_seen(node);
+    out[3] = static_cast<std::int64_t>(t->last_iteration(node));
+    return 0;
+  } catch (const std::out_of_range&) {
+    return -1;
+  }
+}
+void ref_hb_counters(void* h, std::uint64_t* out) {
+  auto* t = static_cast<ctl::HeartbeatTable*>(h);
+  out[0] = t->unknown_reports();
+  out[1] = t->late_reports();
+  out[2] = t->regressions();
+}
+
+static ClusterSpec ref_spec(std::uint32_t nodes, std::uint32_t gpn, std::uint32_t d, std::uint32_t p,
+                            std::uint32_t t, int distributed, std::uint64_t phi) {
+  ClusterSpec s;
+  s.num_nodes = nodes;
+  s.gpus_per_node = gpn;
+  s.data_parallel = d;
+  s.pipeline_parallel = p;
+  s.tensor_parallel = t;
+  s.distributed_optimizer = distributed != 0;
+  s.params_per_device = phi;
+  return s;
+}
+
+void* ref_ledger_create(std::uint32_t nodes, std::uint32_t gpn, std::uint32_t d, std::uint32_t p, std::uint32_t t) {
+  return new ctl::IterationLedger(ref_spec(nodes, gpn, d, p, t, 1, 1));
+}
+void ref_ledger_free(void* g) { delete static_cast<ctl::IterationLedger*>(g); }
+int ref_ledger_record(void* g, std::uint16_t dp, std::uint16_t pp, std::uint16_t tp, std::uint64_t it) {
+  try {
+    static_cast<ctl::IterationLedger*>(g)->record(Role{dp, pp, tp}, it);
+    return 0;
+  } catch (const net::ProtocolError&) {
+    return -1;
+  }
+}
+std::uint64_t ref_ledger_global(void* g) { return static_cast<ctl::IterationLedger*>(g)->global_consistent(); }
+std::uint64_t ref_ledger_group(void* g, std::uint32_t group) {
+  return static_cast<ctl::IterationLedger*>(g)->group_latest(group);
+}
+std::uint64_t ref_ledger_worker(void* g, std::uint16_t dp, std::uint16_t pp, std::uint16_t tp) {
+  return static_cast<ctl::IterationLedger*>(g)->worker_latest(Role{dp, pp, tp});
+}
+void ref_ledger_rebase(void* g, std::uint64_t it) { static_cast<ctl::IterationLedger*>(g)->rebase(it); }
+
+// plan_recovery (controller.cpp:144-209) flattened into `out` (int64 words):
+// kind, resume, then each list as a count followed by its entries -- pods;
+// roles (dp,pp,tp); lazy (dp,pp,tp); forwards (dp,pp,tp,holder,dest);
+// redundant (target dp,pp,tp, source dp,pp,tp).  Returns the words written,
+// or -1 when the plan does not fit / the call throws.
+long ref_plan_recovery(std::uint32_t nodes, std::uint32_t gpn, std::uint32_t d, std::uint32_t p, std::uint32_t t,
+                       int distributed, std::uint64_t phi, const std::uint32_t* pods, std::uint32_t npods,
+                       const std::uint16_t* roles, std::uint32_t nroles, std::uint64_t global_consistent,
+                       std::uint64_t latest_fallback, std::int64_t* out, long cap) {
+  try {
+    std::vector<std::uint32_t> fp(pods, pods + npods);
+    std::vector<Role> fr;
+    for (std::uint32_t i = 0; i < nroles; ++i) fr.push_back(Role{roles[3 * i], roles[3 * i + 1], roles[3 * i + 2]});
+    const auto plan = ctl::plan_recovery(ref_spec(nodes, gpn, d, p, t, distributed, phi), fp, fr,
+                                         global_consistent, latest_fallback);
+    std::vector<std::int64_t> w;
+    w.push_back(plan.kind == ctl::RestoreKind::Fallback ? 1 : 0);
+    w.push_back(static_cast<std::int64_t>(plan.resume_iteration));
+    auto role = [&](const Role& r) {
+      w.push_back(r.dp);
+      w.push_back(r.pp);
+      w.push_back(r.tp);
+    };
+    w.push_back(static_cast<std::int64_t>(plan.failed_pods.size()));
+    for (auto x : plan.failed_pods) w.push_back(x);
+    w.push_back(static_cast<std::int64_t>(plan.failed_roles.size()));
+    for (auto& r : plan.failed_roles) role(r);
+    w.push_back(static_cast<std::int64_t>(plan.lazy_backup_targets.size()));
+    for (auto& r : plan.lazy_backup_targets) role(r);
+    w.push_back(static_cast<std::int64_t>(plan.forwards.size()));
+    for (auto& f : plan.forwards) {
+      role(f.origin);
+      w.push_back(f.holder_node);
+      w.push_back(f.dest_node);
+    }
+    w.push_back(static_cast<std::int64_t>(plan.redundant_from.size()));
+    for (auto& r : plan.redundant_from) {
+      role(r.target);
+      role(r.source);
+    }
+    if (static_cast<long>(w.size()) > cap) return -1;
+    std::memcpy(out, w.data(), w.size() * sizeof(std::int64_t));
+    return static_cast<long>(w.size());
+  } catch (const std::exception&) {
+    return -1;
+  }
+}
 }  // extern "C"

@@ -184,6 +184,11 @@ class RedundantSource(ctypes.Structure):
     _fields_ = [("target", Role), ("source", Role)]
 
 
+class HeartbeatSlot(ctypes.Structure):  # ffx_heartbeat_slot
+    _fields_ = [("enrolled", ctypes.c_uint32), ("failed", ctypes.c_uint32), ("last_seen_ns", ctypes.c_int64),
+                ("last_iteration", ctypes.c_uint64)]
+
+
 class RecoveryPlanC(ctypes.Structure):
     _fields_ = [("kind", ctypes.c_uint32), ("capacity", ctypes.c_uint32),
                 ("resume_iteration", ctypes.c_uint64),
@@ -289,6 +294,23 @@ SIGNATURES = {
     "ffx_ipc_close": (_I, [_P]),
     "ffx_inject": (_I, [_P, _I, _P, _U64]),
     "ffx_get_stats": (_I, [_P, ctypes.POINTER(Stats)]),
+    "ffx_now_ns": (ctypes.c_int64, []),
+    "ffx_heartbeats_create": (_I, [_U32, ctypes.c_int64, _U32, ctypes.POINTER(_P)]),
+    "ffx_heartbeats_destroy": (_I, [_P]),
+    "ffx_heartbeats_enroll": (_I, [_P, _U32, _U64, ctypes.c_int64]),
+    "ffx_heartbeats_observe": (_I, [_P, _U32, _U64, ctypes.c_int64]),
+    "ffx_heartbeats_sweep": (_I, [_P, ctypes.c_int64, ctypes.POINTER(_U32), _U32, ctypes.POINTER(_U32)]),
+    "ffx_heartbeats_mark_failed": (_I, [_P, _U32]),
+    "ffx_heartbeats_query": (_I, [_P, _U32, ctypes.POINTER(HeartbeatSlot)]),
+    "ffx_heartbeats_counters": (_I, [_P, ctypes.POINTER(_U64), ctypes.POINTER(_U64), ctypes.POINTER(_U64)]),
+    "ffx_ledger_create": (_I, [ctypes.POINTER(ClusterSpec), ctypes.POINTER(_P)]),
+    "ffx_ledger_destroy": (_I, [_P]),
+    "ffx_ledger_record": (_I, [_P, Role, _U64]),
+    "ffx_ledger_global_consistent": (_U64, [_P]),
+    "ffx_ledger_group_latest": (_U64, [_P, _U32]),
+    "ffx_ledger_worker_latest": (_U64, [_P, Role]),
+    "ffx_ledger_rebase": (_I, [_P, _U64]),
+    "ffx_ledger_record_replica": (_I, [_P, _P, ctypes.POINTER(_U64)]),
 }
 
 
@@ -439,6 +461,119 @@ def plan_recovery(spec, failed_pods: Sequence[int], failed_roles: Sequence, glob
                   for i in range(p.n_forwards)],
         redundant_from=[(cp(red[i].target), cp(red[i].source)) for i in range(p.n_redundant)],
     )
+
+
+# ---- controller state (controller.cpp:16-121; host-only, no GPU) -----------
+
+SECOND_NS = 1_000_000_000  # rt::kSecond
+
+
+def now_ns() -> int:
+    return lib.ffx_now_ns()
+
+
+class Heartbeats:
+    """ctl::HeartbeatTable (controller.hpp:56-101) over ffx_heartbeats_*.
+    Defaults = ControllerConfig (1 s interval, 3 misses)."""
+
+    def __init__(self, pods: int, interval_ns: int = SECOND_NS, miss_threshold: int = 3):
+        self.pods = pods
+        self._h = ctypes.c_void_p()
+        check(lib.ffx_heartbeats_create(pods, interval_ns, miss_threshold, ctypes.byref(self._h)),
+              "heartbeats_create")
+
+    def enroll(self, node: int, iteration: int, now: int):
+        check(lib.ffx_heartbeats_enroll(self._h, node, iteration, now), "heartbeats_enroll")
+
+    def observe(self, node: int, iteration: int, now: int):
+        check(lib.ffx_heartbeats_observe(self._h, node & 0xFFFFFFFF, iteration, now), "heartbeats_observe")
+
+    def sweep(self, now: int) -> list:
+        out = (_U32 * max(1, self.pods))()
+        n = _U32()
+        check(lib.ffx_heartbeats_sweep(self._h, now, out, self.pods, ctypes.byref(n)), "heartbeats_sweep")
+        return [out[i] for i in range(n.value)]
+
+    def mark_failed(self, node: int):
+        check(lib.ffx_heartbeats_mark_failed(self._h, node), "heartbeats_mark_failed")
+
+    def _slot(self, node):
+        s = HeartbeatSlot()
+        check(lib.ffx_heartbeats_query(self._h, node, ctypes.byref(s)), "heartbeats_query")
+        return s
+
+    def enrolled(self, node: int) -> bool:
+        return 0 <= node < self.pods and bool(self._slot(node).enrolled)
+
+    def failed(self, node: int) -> bool:
+        return 0 <= node < self.pods and bool(self._slot(node).failed)
+
+    def last_iteration(self, node: int) -> int:
+        return self._slot(node).last_iteration
+
+    def last_seen(self, node: int) -> int:
+        return self._slot(node).last_seen_ns
+
+    def counters(self):
+        u, l, r = _U64(), _U64(), _U64()
+        check(lib.ffx_heartbeats_counters(self._h, ctypes.byref(u), ctypes.byref(l), ctypes.byref(r)),
+              "heartbeats_counters")
+        return u.value, l.value, r.value
+
+    def unknown_reports(self) -> int:
+        return self.counters()[0]
+
+    def late_reports(self) -> int:
+        return self.counters()[1]
+
+    def regressions(self) -> int:
+        return self.counters()[2]
+
+    def destroy(self):
+        if self._h:
+            lib.ffx_heartbeats_destroy(self._h)
+            self._h = ctypes.c_void_p(0)
+
+    __del__ = destroy
+
+
+class Ledger:
+    """ctl::IterationLedger (controller.hpp:106-130) over ffx_ledger_*."""
+
+    def __init__(self, spec: ClusterSpec):
+        self._h = ctypes.c_void_p()
+        check(lib.ffx_ledger_create(ctypes.byref(spec), ctypes.byref(self._h)), "ledger_create")
+
+    def record(self, role, iteration: int):
+        r = role if isinstance(role, Role) else Role(*role)
+        check(lib.ffx_ledger_record(self._h, r, iteration), "ledger_record")
+
+    def record_replica(self, held: "Replica") -> int:
+        """CkptRecord after a completed replica (wire.hpp:85-90); returns the
+        iteration recorded (0: nothing committed yet)."""
+        it = _U64()
+        check(lib.ffx_ledger_record_replica(self._h, held.ptr, ctypes.byref(it)), "ledger_record_replica")
+        return it.value
+
+    def global_consistent(self) -> int:
+        return lib.ffx_ledger_global_consistent(self._h)
+
+    def group_latest(self, dp_group: int) -> int:
+        return lib.ffx_ledger_group_latest(self._h, dp_group)
+
+    def worker_latest(self, role) -> int:
+        r = role if isinstance(role, Role) else Role(*role)
+        return lib.ffx_ledger_worker_latest(self._h, r)
+
+    def rebase(self, iteration: int):
+        check(lib.ffx_ledger_rebase(self._h, iteration), "ledger_rebase")
+
+    def destroy(self):
+        if self._h:
+            lib.ffx_ledger_destroy(self._h)
+            self._h = ctypes.c_void_p(0)
+
+    __del__ = destroy
 
 
 # ---- device primitives ------------------------------------------------------

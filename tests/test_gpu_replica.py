@@ -429,3 +429,43 @@ def test_double_neighbour_dual_store(ffx, split):
     origin.inject(ffx.FAULT_POISON_STATE)
     origin.recover(v2, 7)
     assert host(state) == want
+
+
+def test_ledger_records_committed_replicas_only(ffx):
+    """CkptRecord after a completed replica (wire.hpp:85-90) read from the
+    replica's slot headers: the holder records its origin at the newest
+    COMMITTED iteration; a torn slot (origin died mid-snapshot) never counts,
+    and the ledger's global consistent iteration drives the recovery target
+    (controller.cpp:92-97, :144-209)."""
+    n = 3 * 4096 + 11
+    spec, holder, origin, rep, view = ring_pair(ffx, n)
+    spec.num_nodes, spec.gpus_per_node = 2, 1
+    led = ffx.Ledger(spec)
+    assert led.record_replica(rep) == 0  # nothing committed yet: no record
+    assert led.worker_latest((1, 0, 0)) == 0
+    state, want = blob_for(ffx, 1, n)
+    origin.register(ffx.REGION_BLOB, state)
+    for it in (4, 5, 6):
+        origin.snapshot(it)
+        torch.cuda.synchronize()
+        assert led.record_replica(rep) == it
+    assert led.worker_latest((1, 0, 0)) == 6
+    led.record((0, 0, 0), 6)
+    assert led.global_consistent() == 6
+    slot6 = rep.held()[6]
+    origin.inject(ffx.FAULT_TEAR_SLOT, view, slot6)  # dies while writing 6 again
+    assert led.record_replica(rep) == 5  # the older record is a no-op: still 6
+    assert led.worker_latest((1, 0, 0)) == 6
+    # the controller rewinds to what every worker can reproduce
+    led2 = ffx.Ledger(spec)
+    led2.record((0, 0, 0), 6)
+    assert led2.record_replica(rep) == 5
+    target = led2.global_consistent()
+    assert target == 5
+    plan = ffx.plan_recovery(spec, [1], [], target, 0)
+    assert plan.kind == "neighbor" and plan.forwards[0][1] == 0  # held by node 0
+    ffx.materialize(state, b"\xee" * 32)
+    origin.recover(view, target)
+    assert host(state) == want
+    led2.rebase(target)
+    assert led2.global_consistent() == 5
