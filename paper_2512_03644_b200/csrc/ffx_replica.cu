@@ -123,6 +123,11 @@ extern "C" int ffx_replica_open(ffx_ctx* c, const uint8_t handle[FFX_HANDLE_BYTE
   std::memcpy(&h, handle, sizeof h);
   if (h.magic != kHandleMagic || h.abi != FFX_ABI_VERSION)
     return fail(FFX_EINVAL, "replica_open: not an ffx replica handle");
+  // a damaged handle must not become out-of-bounds slot addressing
+  const SlotLayout want = make_layout(h.capacity, h.slice_bytes ? h.slice_bytes : 1);
+  if (h.versions < 1 || h.versions > 8 || !slice_ok(h.slice_bytes) || h.kind > 1 ||
+      std::memcmp(&want, &h.layout, sizeof want) != 0)
+    return fail(FFX_EINVAL, "replica_open: inconsistent replica handle");
   DeviceGuard g(c->device);
   auto* r = new ffx_replica;
   r->device = h.device;
@@ -144,7 +149,10 @@ extern "C" int ffx_replica_open(ffx_ctx* c, const uint8_t handle[FFX_HANDLE_BYTE
     r->base = reinterpret_cast<uint8_t*>(h.raw);
     if (h.device != c->device) {
       int can = 0;
-      FFX_CUDA(cudaDeviceCanAccessPeer(&can, c->device, h.device));
+      if (cudaDeviceCanAccessPeer(&can, c->device, h.device) != cudaSuccess) {
+        cudaGetLastError();
+        can = 0;
+      }
       if (!can) {
         delete r;
         return fail(FFX_ECONFIG, "device %d cannot access peer %d", c->device, h.device);

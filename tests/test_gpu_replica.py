@@ -469,3 +469,17 @@ def test_ledger_records_committed_replicas_only(ffx):
     assert host(state) == want
     led2.rebase(target)
     assert led2.global_consistent() == 5
+
+
+def test_damaged_handle_is_refused(ffx):
+    """A replica handle travels between processes as 256 opaque bytes; one
+    whose geometry does not add up is refused before any slot is addressed."""
+    import struct
+    spec, holder, origin, rep, view = ring_pair(ffx, 10_000)
+    good = bytearray(rep.export())
+    for off, fmt, val in ((40, "<I", 0), (40, "<I", 9), (32, "<Q", 100), (24, "<Q", 1 << 40), (0, "<I", 0)):
+        bad = bytearray(good)
+        struct.pack_into(fmt, bad, off, val)
+        with pytest.raises(ffx.InvalidArgument):
+            origin.open_replica(bytes(bad))
+    origin.open_replica(bytes(good)).destroy()
