@@ -319,3 +319,18 @@ def test_detection_to_plan_cycle():
     led.rebase(plan.resume_iteration)
     hb.enroll(2, 4, 12 * S)  # the substitute registers
     assert led.global_consistent() == 4 and not hb.failed(2)
+
+
+def test_facade_controller_cpp():
+    """The C++ facade's ftsim::ctl (HeartbeatTable, IterationLedger,
+    plan_recovery over libffx) against test_controller.cpp:37-276's
+    expectations, restated in tests/cpp/test_facade_controller.cpp."""
+    import os
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    binary = os.path.join(root, "paper_2512_03644_b200", "facade", "build", "test_facade_controller")
+    if not os.path.exists(binary):
+        pytest.fail("facade not built: run __graft_entry__.build()")
+    r = subprocess.run([binary], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "0 failed" in r.stdout
