@@ -131,12 +131,24 @@ def run(args, rank, world, local, fail):
             if fail and it == args.fail_at:
                 torch.cuda.synchronize()  # the snapshot of `it` has committed everywhere
                 dist.barrier()
-                plan = ffx.plan_recovery(spec, [], [ffx.Role(args.fail_rank, 0, 0)], it, 0)
+                # the controller state (controller.cpp:81-121): every holder reports
+                # the newest COMMITTED iteration of the replica it holds (the
+                # CkptRecord, wire.hpp:85-90); the restore target is the ledger's
+                # global consistent iteration
+                probe = ffx.Ledger(spec)
+                mine = (held[0].slot_info(held[0].held()[held[0].newest()]).role.tuple(),
+                        probe.record_replica(held[0]))
+                ledger = ffx.Ledger(spec)
+                for role, rec_it in all_gather(mine):
+                    ledger.record(role, rec_it)
+                target = ledger.global_consistent()
+                assert target == it, (target, it)
+                plan = ffx.plan_recovery(spec, [], [ffx.Role(args.fail_rank, 0, 0)], target, 0)
                 if rank == args.fail_rank:
                     _, holder, k = ring.recovery_sources(plan.forwards, world)[0]
                     ctx.inject(ffx.FAULT_POISON_STATE)  # the rank's optimizer shard is gone
                     src = ctx.open_replica(handles[holder][k])
-                    rpt = ctx.recover(src, it)
+                    rpt = ctx.recover(src, target)
                     recovered = {"iteration": it, "holder": holder, "bytes": rpt.bytes,
                                  "seconds": rpt.seconds, "bad_slices": rpt.bad_slices}
                     src.destroy()
