@@ -1,4 +1,4 @@
-// ffx_control.cu -- the C ABI, part 7: the controller state that drives the
+// ffx_control.cpp -- the C ABI, part 7: the controller state that drives the
 // hot path, host-only.
 //
 //   ffx_heartbeats  ctl::HeartbeatTable (controller.hpp:56-101,
@@ -20,11 +20,22 @@
 // reference runs everything on one SimLoop thread, runtime.hpp:5-10).
 // Timestamps are caller-supplied nanoseconds (rt::Nanos), so simulated and
 // wall clocks both work; ffx_now_ns gives CLOCK_MONOTONIC.
+// Plain host C++ (g++, no CUDA headers), so it also builds under
+// -fsanitize=thread for tests/cpp/test_control_threads.cpp.
 #include <time.h>
 
+#include <algorithm>
+#include <cstdint>
 #include <mutex>
+#include <new>
+#include <vector>
 
-#include "ffx_host.h"
+#include "ffx.h"
+
+namespace ffx::host {
+int fail(int status, const char* fmt, ...);  // ffx_api.cu: sets ffx_last_error()
+}
+using ffx::host::fail;
 
 struct ffx_heartbeats {
   struct Slot {

@@ -334,3 +334,24 @@ def test_facade_controller_cpp():
     r = subprocess.run([binary], capture_output=True, text=True, timeout=120)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "0 failed" in r.stdout
+
+
+def test_controller_state_is_race_free_under_tsan(tmp_path):
+    """ffx_control.cpp built with -fsanitize=thread and driven from 4
+    heartbeat reporters + a sweeper + a reader, then 8 ledger recorders + 2
+    readers (tests/cpp/test_control_threads.cpp); TSan aborts on any race."""
+    import os
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    exe = tmp_path / "test_control_threads"
+    cc = subprocess.run(["g++", "-std=c++17", "-O1", "-g", "-fsanitize=thread", "-I" + os.path.join(root, "include"),
+                         "-o", str(exe), os.path.join(root, "tests", "cpp", "test_control_threads.cpp"),
+                         os.path.join(root, "paper_2512_03644_b200", "csrc", "ffx_control.cpp"), "-lpthread"],
+                        capture_output=True, text=True)
+    if cc.returncode != 0 and "tsan" in cc.stderr.lower():
+        pytest.skip("no ThreadSanitizer runtime: " + cc.stderr[-200:])
+    assert cc.returncode == 0, cc.stderr
+    env = dict(os.environ, TSAN_OPTIONS="halt_on_error=1")
+    r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=300, env=env)
+    assert r.returncode == 0, r.stdout + r.stderr[-2000:]
+    assert "control threads ok" in r.stdout
