@@ -466,6 +466,55 @@ int ffx_sched_gap(ffx_sched* s, int gap_kind, void* train_stream);
 int ffx_sched_finish(ffx_sched* s, void* train_stream);
 int ffx_sched_destroy(ffx_sched* s);
 
+/* ---- the data loader's preload buffer -------------------
+ * data::PreloadBuffer (dataloader.hpp:45-73, dataloader.cpp:59-82) in HBM:
+ * byte-capped, ordered by iteration (this rank's TIDs), consumption evicts.
+ * Entries are stream-ordered allocations from the device memory pool. */
+typedef struct ffx_preload ffx_preload;
+typedef struct ffx_preload_state {
+  uint64_t capacity, bytes; /* PreloadBuffer::capacity() / bytes() */
+  uint64_t entries;         /* size() */
+  uint64_t oldest;          /* oldest() iteration, UINT64_MAX when empty */
+  uint64_t fetched, taken;
+} ffx_preload_state;
+int ffx_preload_create(ffx_ctx* ctx, uint64_t capacity_bytes, ffx_preload** out);
+int ffx_preload_destroy(ffx_preload* p);
+int ffx_preload_fits(ffx_preload* p, uint64_t bytes, int* fits);
+/* insert() with the bytes streamed in on `stream` after `gate_event` (either
+ * may be NULL): FFX_ECONFIG past the capacity, FFX_ESTATE for an iteration
+ * already held (the reference's std::logic_error cases).
+ *  _host:      `bytes` from host memory (H2D on the copy engines; pinned
+ *              memory must stay valid until the copy completes).
+ *  _synthetic: DataServerStub::fetch in synthetic mode, generated on the
+ *              device: `count` samples of `sample_bytes`, sample i =
+ *              expand(item_digests[i]) -- item_digests[i] =
+ *              data_item_digest(seed, window.first + i) (evolution.cpp:112-120),
+ *              32 bytes each, computed by the caller's SHA-256. */
+int ffx_preload_fetch_host(ffx_preload* p, uint64_t iteration, const void* host_src, uint64_t bytes, void* stream,
+                           void* gate_event);
+int ffx_preload_fetch_synthetic(ffx_preload* p, uint64_t iteration, const uint8_t* item_digests, uint32_t count,
+                                uint32_t sample_bytes, void* stream, void* gate_event);
+/* take(): the entry leaves the buffer; `consumer_stream` waits for its fetch
+ * and owns the device memory until ffx_preload_free (stream-ordered).
+ * FFX_ESTATE when the iteration is not held (take() -> nullopt). */
+int ffx_preload_take(ffx_preload* p, uint64_t iteration, void* consumer_stream, void** dev, uint64_t* bytes);
+int ffx_preload_free(ffx_preload* p, void* dev, void* consumer_stream);
+int ffx_preload_info(ffx_preload* p, ffx_preload_state* out);
+/* data::fold_of_blob (dataloader.cpp:150-164) on the device: FFX_EINVAL
+ * unless bytes is a whole number of samples. */
+int ffx_fold_of_blob(const void* dev, uint64_t bytes, uint32_t bytes_per_sample, uint64_t* host_out, void* stream);
+/* Preload through the slice scheduler (SPEC preload_loop: fetch only when
+ * the link is idle and the buffer has room): the fetch is queued and issued
+ * at the next FFX_GAP_LINK_IDLE report -- with or without a snapshot in
+ * flight -- on the scheduler's low-priority copy stream, gated on that gap;
+ * a fetch that does not fit stays queued (buffer full: no fetch issued).
+ * Host bytes must be pinned and stay valid until taken. */
+int ffx_sched_preload_host(ffx_sched* s, ffx_preload* p, uint64_t iteration, const void* host_src, uint64_t bytes);
+int ffx_sched_preload_synthetic(ffx_sched* s, ffx_preload* p, uint64_t iteration, const uint8_t* item_digests,
+                                uint32_t count, uint32_t sample_bytes);
+/* fetches still queued in the scheduler */
+int ffx_sched_preload_pending(ffx_sched* s, uint32_t* pending);
+
 /* Copy the checksum table written by this ctx's most recent snapshot into
  * host memory (async on `stream`; pinned memory for true overlap).
  * *n_out = entries copied (min(table, max_entries)). */

@@ -157,6 +157,34 @@ def sha256(data: bytes) -> bytes:
     return b.raw[:32]
 
 
+# ---- the data loader's synthetic samples (evolution.cpp:112-128, dataloader.cpp:104-164)
+
+def data_item_digest(seed: int, index: int) -> bytes:
+    """HashIn{}.str("D").u64(seed).u64(index).digest(): str = u64 length + bytes."""
+    import struct
+    return sha256(struct.pack("<Q", 1) + b"D" + struct.pack("<QQ", seed, index))
+
+
+def data_item(seed: int, index: int, nbytes: int) -> bytes:
+    return expand(data_item_digest(seed, index), nbytes)
+
+
+def fetch(seed: int, first: int, count: int, sample_bytes: int) -> bytes:
+    """DataServerStub::fetch in synthetic mode (dataloader.cpp:119-127)."""
+    return b"".join(data_item(seed, first + i, sample_bytes) for i in range(count))
+
+
+def fold_of_blob(blob: bytes, bytes_per_sample: int) -> int:
+    """dataloader.cpp:150-164."""
+    if bytes_per_sample == 0 or len(blob) % bytes_per_sample:
+        raise ValueError("blob is not a whole number of samples")
+    n = min(8, bytes_per_sample)
+    acc = 0
+    for off in range(0, len(blob), bytes_per_sample):
+        acc = (acc + int.from_bytes(blob[off:off + n], "little")) & (2**64 - 1)
+    return acc
+
+
 def ref_lib():
     """The reference library itself, or None when not built (GPU box w/o build)."""
     if not os.path.exists(REF_SO):
@@ -197,6 +225,8 @@ def ref_lib():
         r.ref_ledger_worker.restype = _u64
         r.ref_ledger_worker.argtypes = [_P, u16, u16, u16]
         r.ref_ledger_rebase.argtypes = [_P, _u64]
+        r.ref_fetch.argtypes = [_u64, _u64, u32, u32, _P]
+        r.ref_fold_of_blob.argtypes = [_P, _u64, u32, ctypes.POINTER(_u64)]
         r.ref_plan_recovery.restype = ctypes.c_long
         r.ref_plan_recovery.argtypes = [u32] * 5 + [ctypes.c_int, _u64, ctypes.POINTER(u32), u32,
                                                     ctypes.POINTER(u16), u32, _u64, _u64,

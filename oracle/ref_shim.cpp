@@ -354,4 +354,20 @@ long ref_plan_recovery(std::uint32_t nodes, std::uint32_t gpn, std::uint32_t d, 
     return -1;
   }
 }
+
+// ---- the data loader (dataloader.cpp:104-164) --------------------------------
+void ref_fetch(std::uint64_t seed, std::uint64_t first, std::uint32_t count, std::uint32_t bps, std::uint8_t* out) {
+  const data::DataServerStub server(seed);
+  const auto v = server.fetch(data::IndexWindow{first, count}, bps);
+  if (!v.empty()) std::memcpy(out, v.data(), v.size());
+}
+
+int ref_fold_of_blob(const std::uint8_t* p, std::uint64_t n, std::uint32_t bps, std::uint64_t* out) {
+  try {
+    *out = data::fold_of_blob(std::vector<std::uint8_t>(p, p + n), bps);
+    return 0;
+  } catch (const std::invalid_argument&) {
+    return -1;
+  }
+}
 }  // extern "C"

@@ -238,6 +238,10 @@ int find_slot(ffx_replica* r, uint64_t iteration, SlotMeta* meta);
 // Shareable (VMM) replicas: open an exported one / release (ffx_mcast.cu).
 int open_shared(ffx_ctx* c, const HandleBlob& h, ffx_replica* r);
 void release_shared(ffx_replica* r);
+// ffx_preload.cu: one fetch into the preload buffer (host bytes or synthetic
+// samples) on stream s after gate.
+int preload_fetch(ffx_preload* p, uint64_t iteration, const void* host_src, const uint8_t* digests, uint32_t count,
+                  uint32_t sample_bytes, uint64_t bytes, cudaStream_t s, cudaEvent_t gate);
 
 }  // namespace ffx::host
 

@@ -326,6 +326,46 @@ __global__ void fill_kernel(uint8_t* dst, uint64_t bytes, uint32_t pattern) {
 
 __global__ void xor_byte_kernel(uint8_t* dst, uint8_t mask) { *dst ^= mask; }
 
+// ---- data loader: synthetic samples and their fold ----------------------------
+
+// Word w of sample i is mix64(fold_i + (w+1) G) (expand, evolution.cpp:71-97);
+// samples are packed back to back, so a sample need not start 8-aligned:
+// aligned full words go out as one 8-byte store, the rest byte by byte.
+__global__ void items_kernel(uint8_t* dst, const uint64_t* folds, uint32_t count, uint32_t sample_bytes) {
+  const uint64_t wps = (sample_bytes + 7) / 8;  // words per sample
+  const uint64_t total = wps * count;
+  for (uint64_t g = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; g < total;
+       g += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t i = g / wps, w = g % wps;
+    const uint64_t v = mix64(folds[i] + (w + 1) * kGolden);
+    const uint64_t o = i * sample_bytes + 8 * w;
+    const uint32_t n = static_cast<uint32_t>(umin64(8, sample_bytes - 8 * w));
+    uint8_t* p = dst + o;
+    if (n == 8 && (reinterpret_cast<uintptr_t>(p) & 7u) == 0) {
+      *reinterpret_cast<uint64_t*>(p) = v;
+    } else {
+      for (uint32_t b = 0; b < n; ++b) p[b] = static_cast<uint8_t>(v >> (8 * b));
+    }
+  }
+}
+
+// fold_of_blob: the wrapped sum over samples of each sample's first
+// min(8, bytes_per_sample) bytes read little-endian.
+__global__ void fold_blob_kernel(const uint8_t* blob, uint64_t nsamples, uint32_t bps, unsigned long long* out) {
+  unsigned long long acc = 0;
+  const uint32_t n = bps < 8 ? bps : 8;
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < nsamples;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint8_t* p = blob + i * bps;
+    uint64_t v = 0;
+    for (uint32_t b = 0; b < n; ++b) v |= static_cast<uint64_t>(p[b]) << (8 * b);
+    acc += v;
+  }
+#pragma unroll
+  for (int d = 16; d; d >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, d);
+  if ((threadIdx.x & 31) == 0 && acc) atomicAdd(out, acc);
+}
+
 unsigned grid_for(uint64_t work_items, int threads) {
   const uint64_t want = (work_items + threads - 1) / threads;
   const uint64_t cap = static_cast<uint64_t>(sm_count()) * 8;
@@ -333,6 +373,22 @@ unsigned grid_for(uint64_t work_items, int threads) {
 }
 
 }  // namespace
+
+cudaError_t launch_items(uint8_t* dst, const uint64_t* folds, uint32_t count, uint32_t sample_bytes,
+                         cudaStream_t stream) {
+  const uint64_t words = (sample_bytes + 7) / 8 * uint64_t(count);
+  if (words == 0) return cudaSuccess;
+  items_kernel<<<grid_for(words, 256), 256, 0, stream>>>(dst, folds, count, sample_bytes);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fold_blob(const uint8_t* blob, uint64_t bytes, uint32_t bytes_per_sample,
+                             unsigned long long* out, cudaStream_t stream) {
+  const uint64_t ns = bytes_per_sample ? bytes / bytes_per_sample : 0;
+  if (ns == 0) return cudaSuccess;
+  fold_blob_kernel<<<grid_for(ns, 256), 256, 0, stream>>>(blob, ns, bytes_per_sample, out);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_expand(uint8_t* dst, uint64_t fold, uint64_t bytes, const uint8_t* prefix32,
                           cudaStream_t stream) {

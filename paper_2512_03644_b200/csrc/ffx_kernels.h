@@ -131,6 +131,15 @@ cudaError_t whole_fnv(const uint8_t* data, uint64_t len, uint64_t h0, uint64_t* 
 // Keep up to 256 MB cached in the current device's default memory pool.
 void retain_pool();
 
+// The data loader's device side (ffx_preload.cu): `count` synthetic samples
+// of `sample_bytes` each, sample i = expand(digest_i) given its fold64
+// (DataServerStub::fetch, dataloader.cpp:104-127, evolution.cpp:71-120), and
+// fold_of_blob (dataloader.cpp:150-164) accumulated into *out (wrapping).
+cudaError_t launch_items(uint8_t* dst, const uint64_t* folds, uint32_t count, uint32_t sample_bytes,
+                         cudaStream_t stream);
+cudaError_t launch_fold_blob(const uint8_t* blob, uint64_t bytes, uint32_t bytes_per_sample,
+                             unsigned long long* out, cudaStream_t stream);
+
 cudaError_t launch_fill(uint8_t* dst, uint64_t bytes, uint32_t pattern, cudaStream_t stream);
 cudaError_t launch_xor_byte(uint8_t* dst, uint8_t mask, cudaStream_t stream);
 

@@ -9,10 +9,21 @@
 // on that event, with a CTA cap bounding what a batch can hold while TRAIN
 // kernels arrive.  Copy batches go into link-idle gaps (after a collective),
 // checksum batches (split policies) into SM-idle gaps (before a collective).
+#include <deque>
+
 #include "ffx_host.h"
 
 struct ffx_sched {
+  struct Fetch {  // a queued preload (ffx_sched_preload_*)
+    ffx_preload* p;
+    uint64_t iteration;
+    const void* host_src;        // null: synthetic
+    std::vector<uint8_t> digests;
+    uint32_t count, sample_bytes;
+    uint64_t bytes;
+  };
   ffx_ctx* ctx = nullptr;
+  std::deque<Fetch> fetches;
   ffx_sched_opts opts{};
   std::vector<double> weights;        // link-gap durations (copy-batch sizes)
   cudaStream_t copy_stream = nullptr; // low priority
@@ -42,6 +53,23 @@ int issue(ffx_sched* s, int kind, cudaStream_t train) {
   if (kind == FFX_BATCH_COPY) s->copies_left = left;
   else s->hashes_left = left;
   if (s->copies_left == 0 && s->hashes_left == 0) FFX_CUDA(cudaEventRecord(s->done, st));  // carried the commit
+  return FFX_OK;
+}
+
+// Issue the queued preloads in iteration order on the copy stream after
+// `gate`, stopping at the first that does not fit (buffer full: no fetch).
+int issue_fetches(ffx_sched* s, cudaEvent_t gate) {
+  while (!s->fetches.empty()) {
+    auto& f = s->fetches.front();
+    int fits = 0;
+    int rc = ffx_preload_fits(f.p, f.bytes, &fits);
+    if (rc) return rc;
+    if (!fits) break;
+    rc = preload_fetch(f.p, f.iteration, f.host_src, f.digests.empty() ? nullptr : f.digests.data(), f.count,
+                       f.sample_bytes, f.bytes, s->copy_stream, gate);
+    if (rc) return rc;
+    s->fetches.pop_front();
+  }
   return FFX_OK;
 }
 
@@ -101,8 +129,17 @@ extern "C" int ffx_sched_begin(ffx_sched* s, uint64_t iteration) {
 
 extern "C" int ffx_sched_gap(ffx_sched* s, int kind, void* train_stream) {
   if (!s) return fail(FFX_EINVAL, "sched_gap: null argument");
-  if (!s->active) return FFX_OK;  // no snapshot this step
   DeviceGuard g(s->ctx->device);
+  if (kind == FFX_GAP_LINK_IDLE && !s->fetches.empty()) {  // the loader's preloads ride the same gaps
+    cudaEvent_t gate = nullptr;
+    if (train_stream) {
+      gate = s->gates[s->next_gate++ % s->gates.size()];
+      FFX_CUDA(cudaEventRecord(gate, as_stream(train_stream)));
+    }
+    const int rc = issue_fetches(s, gate);
+    if (rc) return rc;
+  }
+  if (!s->active) return FFX_OK;  // no snapshot this step
   if (kind == FFX_GAP_LINK_IDLE && s->copies_left) return issue(s, FFX_BATCH_COPY, as_stream(train_stream));
   if (kind == FFX_GAP_SM_IDLE && s->hashes_left) return issue(s, FFX_BATCH_HASH, as_stream(train_stream));
   if (kind != FFX_GAP_LINK_IDLE && kind != FFX_GAP_SM_IDLE) return fail(FFX_EINVAL, "sched_gap: kind %d", kind);
@@ -124,6 +161,28 @@ extern "C" int ffx_sched_finish(ffx_sched* s, void* train_stream) {
   s->active = false;
   // the optimizer may only mutate the snapshotted state after the commit
   FFX_CUDA(cudaStreamWaitEvent(as_stream(train_stream), s->done, 0));
+  return FFX_OK;
+}
+
+extern "C" int ffx_sched_preload_host(ffx_sched* s, ffx_preload* p, uint64_t iteration, const void* host_src,
+                                      uint64_t bytes) {
+  if (!s || !p || (bytes && !host_src)) return fail(FFX_EINVAL, "sched_preload_host: null argument");
+  s->fetches.push_back(ffx_sched::Fetch{p, iteration, host_src, {}, 0, 0, bytes});
+  return FFX_OK;
+}
+
+extern "C" int ffx_sched_preload_synthetic(ffx_sched* s, ffx_preload* p, uint64_t iteration,
+                                           const uint8_t* item_digests, uint32_t count, uint32_t sample_bytes) {
+  if (!s || !p || (count && !item_digests)) return fail(FFX_EINVAL, "sched_preload_synthetic: null argument");
+  ffx_sched::Fetch f{p, iteration, nullptr, std::vector<uint8_t>(item_digests, item_digests + 32 * size_t(count)),
+                     count, sample_bytes, uint64_t(count) * sample_bytes};
+  s->fetches.push_back(std::move(f));
+  return FFX_OK;
+}
+
+extern "C" int ffx_sched_preload_pending(ffx_sched* s, uint32_t* pending) {
+  if (!s || !pending) return fail(FFX_EINVAL, "sched_preload_pending: null argument");
+  *pending = static_cast<uint32_t>(s->fetches.size());
   return FFX_OK;
 }
 

@@ -189,6 +189,11 @@ class HeartbeatSlot(ctypes.Structure):  # ffx_heartbeat_slot
                 ("last_iteration", ctypes.c_uint64)]
 
 
+class PreloadState(ctypes.Structure):  # ffx_preload_state
+    _fields_ = [("capacity", ctypes.c_uint64), ("bytes", ctypes.c_uint64), ("entries", ctypes.c_uint64),
+                ("oldest", ctypes.c_uint64), ("fetched", ctypes.c_uint64), ("taken", ctypes.c_uint64)]
+
+
 class RecoveryPlanC(ctypes.Structure):
     _fields_ = [("kind", ctypes.c_uint32), ("capacity", ctypes.c_uint32),
                 ("resume_iteration", ctypes.c_uint64),
@@ -295,6 +300,18 @@ SIGNATURES = {
     "ffx_inject": (_I, [_P, _I, _P, _U64]),
     "ffx_get_stats": (_I, [_P, ctypes.POINTER(Stats)]),
     "ffx_now_ns": (ctypes.c_int64, []),
+    "ffx_preload_create": (_I, [_P, _U64, ctypes.POINTER(_P)]),
+    "ffx_preload_destroy": (_I, [_P]),
+    "ffx_preload_fits": (_I, [_P, _U64, ctypes.POINTER(_I)]),
+    "ffx_preload_fetch_host": (_I, [_P, _U64, _P, _U64, _P, _P]),
+    "ffx_preload_fetch_synthetic": (_I, [_P, _U64, _P, _U32, _U32, _P, _P]),
+    "ffx_preload_take": (_I, [_P, _U64, _P, ctypes.POINTER(_P), ctypes.POINTER(_U64)]),
+    "ffx_preload_free": (_I, [_P, _P, _P]),
+    "ffx_preload_info": (_I, [_P, ctypes.POINTER(PreloadState)]),
+    "ffx_fold_of_blob": (_I, [_P, _U64, _U32, ctypes.POINTER(_U64), _P]),
+    "ffx_sched_preload_host": (_I, [_P, _P, _U64, _P, _U64]),
+    "ffx_sched_preload_synthetic": (_I, [_P, _P, _U64, _P, _U32, _U32]),
+    "ffx_sched_preload_pending": (_I, [_P, ctypes.POINTER(_U32)]),
     "ffx_heartbeats_create": (_I, [_U32, ctypes.c_int64, _U32, ctypes.POINTER(_P)]),
     "ffx_heartbeats_destroy": (_I, [_P]),
     "ffx_heartbeats_enroll": (_I, [_P, _U32, _U64, ctypes.c_int64]),
@@ -784,9 +801,92 @@ class Sched:
     def finish(self, train_stream=None):
         check(lib.ffx_sched_finish(self._h, _stream_ptr(train_stream)), "sched_finish")
 
+    def preload_host(self, preload: "Preload", iteration: int, host_tensor):
+        """Queue a fetch of pinned host bytes for the next link-idle gap."""
+        preload._keep[iteration] = host_tensor  # must outlive the copy
+        check(lib.ffx_sched_preload_host(self._h, preload._h, iteration, host_tensor.data_ptr(),
+                                         host_tensor.numel() * host_tensor.element_size()), "sched_preload_host")
+
+    def preload_synthetic(self, preload: "Preload", iteration: int, item_digests: bytes, sample_bytes: int):
+        check(lib.ffx_sched_preload_synthetic(self._h, preload._h, iteration, item_digests, len(item_digests) // 32,
+                                              sample_bytes), "sched_preload_synthetic")
+
+    def preload_pending(self) -> int:
+        n = _U32()
+        check(lib.ffx_sched_preload_pending(self._h, ctypes.byref(n)), "sched_preload_pending")
+        return n.value
+
     def destroy(self):
         if self._h:
             check(lib.ffx_sched_destroy(self._h), "sched_destroy")
+            self._h = ctypes.c_void_p(0)
+
+
+def data_item_digests(seed: int, first: int, count: int) -> bytes:
+    """data_item_digest(seed, first + i) for a window (evolution.cpp:112-114):
+    SHA-256 of HashIn{}.str("D").u64(seed).u64(index) -- 32-byte keys on the
+    host, as the reference computes them (OpenSSL); the sample bytes are then
+    generated on the device (Preload.fetch_synthetic)."""
+    import hashlib
+    import struct
+    head = struct.pack("<Q", 1) + b"D" + struct.pack("<Q", seed)
+    return b"".join(hashlib.sha256(head + struct.pack("<Q", first + i)).digest() for i in range(count))
+
+
+def fold_of_blob(dev, bytes_per_sample: int, nbytes=None, stream=None) -> int:
+    """data::fold_of_blob (dataloader.cpp:150-164) on the device."""
+    out = _U64()
+    n = nbytes if nbytes is not None else dev.numel() * dev.element_size()
+    check(lib.ffx_fold_of_blob(_ptr(dev), n, bytes_per_sample, ctypes.byref(out), _stream_ptr(stream)),
+          "fold_of_blob")
+    return out.value
+
+
+class Preload:
+    """data::PreloadBuffer in HBM (dataloader.hpp:45-73) over ffx_preload_*."""
+
+    def __init__(self, ctx: "Context", capacity_bytes: int):
+        self._h = ctypes.c_void_p()
+        self._keep = {}
+        check(lib.ffx_preload_create(ctx.ptr, capacity_bytes, ctypes.byref(self._h)), "preload_create")
+
+    def fits(self, nbytes: int) -> bool:
+        v = _I()
+        check(lib.ffx_preload_fits(self._h, nbytes, ctypes.byref(v)), "preload_fits")
+        return bool(v.value)
+
+    def fetch_host(self, iteration: int, host_tensor, stream=None, gate_event=None):
+        self._keep[iteration] = host_tensor
+        check(lib.ffx_preload_fetch_host(self._h, iteration, host_tensor.data_ptr(),
+                                         host_tensor.numel() * host_tensor.element_size(), _stream_ptr(stream),
+                                         gate_event.cuda_event if gate_event is not None else None),
+              "preload_fetch_host")
+
+    def fetch_synthetic(self, iteration: int, item_digests: bytes, sample_bytes: int, stream=None, gate_event=None):
+        check(lib.ffx_preload_fetch_synthetic(self._h, iteration, item_digests, len(item_digests) // 32,
+                                              sample_bytes, _stream_ptr(stream),
+                                              gate_event.cuda_event if gate_event is not None else None),
+              "preload_fetch_synthetic")
+
+    def take(self, iteration: int, consumer_stream=None):
+        """-> (device pointer, bytes); the caller frees it with free()."""
+        p, n = ctypes.c_void_p(), _U64()
+        check(lib.ffx_preload_take(self._h, iteration, _stream_ptr(consumer_stream), ctypes.byref(p),
+                                   ctypes.byref(n)), "preload_take")
+        self._keep.pop(iteration, None)
+        return p.value, n.value
+
+    def free(self, dev_ptr: int, consumer_stream=None):
+        check(lib.ffx_preload_free(self._h, dev_ptr, _stream_ptr(consumer_stream)), "preload_free")
+
+    def info(self) -> PreloadState:
+        st = PreloadState()
+        check(lib.ffx_preload_info(self._h, ctypes.byref(st)), "preload_info")
+        return st
+
+    def destroy(self):
+        if self._h:
+            check(lib.ffx_preload_destroy(self._h), "preload_destroy")
             self._h = ctypes.c_void_p(0)
 
 
