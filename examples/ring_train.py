@@ -5,7 +5,10 @@ rank failure in the middle -- the FFTrainer path end to end on real state.
         examples/ring_train.py [--iters 12] [--fail-at 6] [--fail-rank 1] [--overlap]
 
 Every rank holds the full (bf16-free, fp32) MLP parameters, computes
-gradients on its own data, and owns one shard of the optimizer state
+gradients on its own data -- windows of the synthetic data server
+(DataServerStub, one IN-byte sample per row) preloaded into an HBM
+PreloadBuffer a few iterations ahead, the fetches issued in the step's
+link-idle gap through the slice scheduler -- and owns one shard of the optimizer state
 (ZeRO-1): the fp32 master shard, Adam m / v for that shard, and the data
 cursor.  Those four regions are registered with ffx and snapshotted into the
 ring successor's replica after every optimizer update (NVLink, one kernel).
@@ -27,6 +30,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2512_03644_b200 import ffx, ring  # noqa: E402
 
 IN, HID, OUT, BATCH = 512, 1024, 16, 256
+DATA_SEED = 11
 SHAPES = [(IN, HID), (HID,), (HID, OUT), (OUT,)]
 NPARAM = sum(torch.Size(s).numel() for s in SHAPES)
 
@@ -57,15 +61,57 @@ class Rank:
             o += n
         return out
 
+    # ---- the data loader: an HBM PreloadBuffer fed through the scheduler ----
+    DEPTH = 3  # iterations of data kept ahead (ClusterSpec.preload_depth)
+
+    def attach_loader(self, ctx):
+        self.preload = ffx.Preload(ctx, self.DEPTH * BATCH * IN)
+        self.loader_sched = ffx.Sched(ctx, ffx.SCHED_FUSED, link_gaps=1)
+        self.queued = set()
+
+    def lose_loader(self, ctx):
+        """The failed rank's buffered windows are gone with it; the
+        replacement refetches from its restored cursor."""
+        self.close_loader()
+        self.attach_loader(ctx)
+
+    def close_loader(self):
+        torch.cuda.synchronize()
+        self.loader_sched.destroy()
+        self.preload.destroy()
+
+    def window(self, pos):
+        # disjoint per (position, rank): the data_assignment geometry
+        first = (pos * self.world + self.rank) * BATCH
+        return ffx.data_item_digests(DATA_SEED, first, BATCH)
+
+    def batch(self, pos):
+        cur = torch.cuda.current_stream()
+        if pos not in self.queued:  # first step, or after a failure: fetch now
+            self.preload.fetch_synthetic(pos, self.window(pos), IN, stream=cur)
+            self.queued.add(pos)
+        for ahead in range(pos + 1, pos + self.DEPTH):
+            if ahead not in self.queued:
+                self.loader_sched.preload_synthetic(self.preload, ahead, self.window(ahead), IN)
+                self.queued.add(ahead)
+        dev, n = self.preload.take(pos, cur)  # the step's stream waits for the fetch
+        self.queued.discard(pos)
+        raw = torch.empty(BATCH, IN, dtype=torch.uint8, device="cuda")
+        ffx.check(ffx.lib.ffx_memcpy(raw.data_ptr(), dev, n, cur.cuda_stream, 0), "memcpy")
+        self.preload.free(dev, cur)
+        x = (raw.float() - 127.5) / 64.0
+        y = raw[:, 0].long() % OUT
+        return x, y
+
     def step(self, lr=1e-3, b1=0.9, b2=0.999, eps=1e-8, before_update=None):
         pos = int(self.cursor[1].item())
-        g = torch.Generator(device="cuda").manual_seed(10_000 * pos + self.rank)
-        x = torch.randn(BATCH, IN, device="cuda", generator=g)
-        y = torch.randint(0, OUT, (BATCH,), device="cuda", generator=g)
+        x, y = self.batch(pos)
         p = self.params.detach().requires_grad_(True)
         self.params = p
         w1, c1, w2, c2 = self.views()
         loss = torch.nn.functional.cross_entropy(torch.relu(x @ w1 + c1) @ w2 + c2, y)
+        # the link is idle while forward / backward compute: the preloads go now
+        self.loader_sched.gap(ffx.GAP_LINK_IDLE, torch.cuda.current_stream())
         loss.backward()
         with torch.no_grad():
             grad = p.grad
@@ -96,6 +142,7 @@ def run(args, rank, world, local, fail):
     ctx = ffx.Context(local, spec, ffx.Role(rank, 0, 0))
     for kind, t in me.regions():
         ctx.register(kind, t)
+    me.attach_loader(ctx)
     nbytes = sum(t.numel() * t.element_size() for _, t in me.regions())
 
     def all_gather(b):
@@ -147,6 +194,7 @@ def run(args, rank, world, local, fail):
                 if rank == args.fail_rank:
                     _, holder, k = ring.recovery_sources(plan.forwards, world)[0]
                     ctx.inject(ffx.FAULT_POISON_STATE)  # the rank's optimizer shard is gone
+                    me.lose_loader(ctx)                    # and its preloaded data
                     src = ctx.open_replica(handles[holder][k])
                     rpt = ctx.recover(src, target)
                     recovered = {"iteration": it, "holder": holder, "bytes": rpt.bytes,
@@ -158,6 +206,7 @@ def run(args, rank, world, local, fail):
         final = me.params.detach().clone()
     finally:
         torch.cuda.synchronize()
+        me.close_loader()
         for r in targets + held:
             r.destroy()
         ctx.close()
