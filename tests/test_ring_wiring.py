@@ -1,4 +1,4 @@
-"""Multi-process host logic of the DP ring on CPU (gloo, world_size 2 and 4).
+"""Multi-process host logic of the DP ring on CPU (gloo, world_size 2, 4 and 8 — the driver's 8-GPU scaling run).
 
 The replica handles are stand-in byte strings; what is checked is that every
 rank writes into exactly the replica its ring successor holds for it, and
@@ -55,7 +55,7 @@ def _worker(rank, world, port, replicas, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,replicas", [(2, 1), (4, 1), (4, 2)])
+@pytest.mark.parametrize("world,replicas", [(2, 1), (4, 1), (4, 2), (8, 1), (8, 2)])
 def test_ring_wiring_gloo(world, replicas):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
@@ -133,8 +133,8 @@ def _mcast_worker(rank, world, port, q):
         dist.destroy_process_group()
 
 
-def test_mcast_ring_wiring_gloo():
-    world = 4
+@pytest.mark.parametrize("world", [4, 8])
+def test_mcast_ring_wiring_gloo(world):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
