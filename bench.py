@@ -159,6 +159,17 @@ def cpu_ring(threads, bytes_per_thread, iters):
     return out
 
 
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
 def cpu_baseline_line(threads, bytes_per_thread, iters=4):
     """The reference's own CPU path on a bounded sample (threads x bytes per
     iteration, `iters` iterations: ~10-30 thread-seconds of work); medians."""
@@ -176,6 +187,7 @@ def cpu_baseline_line(threads, bytes_per_thread, iters=4):
                   % (threads, bytes_per_thread >> 20, iters),
         "stages_gbs": {"take": round(agg / take / 1e9, 3), "store": round(agg / store / 1e9, 3),
                        "restore": round(agg / restore / 1e9, 3)},
+        "nproc": os.cpu_count(), "cpu_model": cpu_model(),
     }
 
 
@@ -201,7 +213,8 @@ def run_reference(args):
                                "sample of the GPT-2 XL ZeRO-1 d=8 shard, one thread per ring rank",
                    "bytes_per_rank_sample": per, "ranks": threads},
         "cpu_baseline": {"value": round(value, 3), "unit": "GB/s", "cores": threads, "kind": "reference",
-                         "sample": "%d threads x 256 MiB per step" % threads},
+                         "sample": "%d threads x 256 MiB per step" % threads,
+                         "nproc": os.cpu_count(), "cpu_model": cpu_model()},
         "e2e": {"value": round(value, 3), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "restore_gbs": round(agg * len(res) / sum(r[2] for r in res) / 1e9, 3),
     }), flush=True)
