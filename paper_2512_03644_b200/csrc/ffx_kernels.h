@@ -67,7 +67,8 @@ struct SliceJob {
   uint32_t stagger_ns;            // start-up de-phasing: warp w sleeps (w % 8) * stagger_ns first
   uint32_t claim_order;           // 0: last task first, then backwards; 1: last task first, then forwards
   uint32_t store_hint;            // tensor stores with an L2 evict_first hint (experiment)
-  uint32_t pad3_;
+  uint32_t prefetch_next;         // tensor path: claim the next task S steps early and load its
+                                  // first S steps into the stages this task frees (no per-task drain)
   SlotCommit commit;
   SlotCommit commit2;             // second replica's slot (slot null = none)
 };

@@ -255,8 +255,8 @@ __global__ void __launch_bounds__(W * 32) slice_kernel(const __grid_constant__ S
   if (job.stagger_ns) __nanosleep(((blockIdx.x * W + warp) & 7u) * job.stagger_ns);
   uint64_t g_next = job.group_lo + static_cast<uint64_t>(blockIdx.x) * W + warp;
   const uint64_t g_stride = static_cast<uint64_t>(gridDim.x) * W;
-  for (;;) {
-    uint64_t g;
+  constexpr uint64_t kNone = ~0ull;
+  auto claim = [&]() -> uint64_t {
     if (job.sched != nullptr) {
       // Claims run from the LAST task down: each region's ragged tail (and
       // tiny register-path regions) starts first and overlaps the bulk
@@ -266,18 +266,33 @@ __global__ void __launch_bounds__(W * 32) slice_kernel(const __grid_constant__ S
       unsigned t = 0;
       if (lane == 0) t = atomicAdd(&job.sched[0], 1u);
       t = __shfl_sync(0xffffffffu, t, 0);
-      if (t >= job.group_hi - job.group_lo) break;
-      g = (job.claim_order == 0 || t == 0) ? job.group_hi - 1 - t : job.group_lo + t - 1;
-    } else {
-      g = g_next;
-      g_next += g_stride;
+      if (t >= job.group_hi - job.group_lo) return kNone;
+      return (job.claim_order == 0 || t == 0) ? job.group_hi - 1 - t : job.group_lo + t - 1;
     }
-    if (g >= job.group_hi) break;
-
-    SliceRegion R = job.reg[0];
+    const uint64_t gg = g_next;
+    g_next += g_stride;
+    return gg < job.group_hi ? gg : kNone;
+  };
+  auto region_of = [&](uint64_t gg) {
+    SliceRegion Q = job.reg[0];
 #pragma unroll
     for (int i = 1; i < static_cast<int>(kMaxRegions); ++i)
-      if (i < static_cast<int>(job.nregions) && g >= job.reg[i].group_base) R = job.reg[i];
+      if (i < static_cast<int>(job.nregions) && gg >= job.reg[i].group_base) Q = job.reg[i];
+    return Q;
+  };
+  // Cross-task prefetch (job.prefetch_next): the next task is claimed when
+  // this one's last S steps start, and its first S steps are loaded into the
+  // stages those steps free, so the stage ring runs on across task
+  // boundaries (stage of step k = (sbase + k) % S) instead of draining.
+  uint64_t g = claim();
+  bool prefetched = false;
+  uint32_t sbase = 0;
+  for (;;) {
+    if (g == kNone) break;
+    uint64_t g_pf = kNone;
+    bool claimed = false, pf_ok = false;
+
+    const SliceRegion R = region_of(g);
     const bool al = aligned16(R.src) && (!kCopy || aligned16(R.dst));
     const uint64_t s0 = (g - R.group_base) * K::ROWS;
 
@@ -293,7 +308,9 @@ __global__ void __launch_bounds__(W * 32) slice_kernel(const __grid_constant__ S
 
     // Stages are free once this lane's earlier bulk stores finished reading
     // them and every lane is past its previous hash.
-    if constexpr (kCopy) bulk_wait_read_all();
+    if constexpr (kCopy) {
+      if (!prefetched) bulk_wait_read_all();
+    }
     __syncwarp();
 
     if (R.tmap >= 0 && s0 + K::ROWS <= R.nfull) {
@@ -305,17 +322,18 @@ __global__ void __launch_bounds__(W * 32) slice_kernel(const __grid_constant__ S
       const int nsteps = static_cast<int>(Sl / (C * KC));
       const int y = static_cast<int>(s0);
       const int pro = nsteps < S ? nsteps : S;
-      if (lane == 0) {
+      if (lane == 0 && !prefetched) {
         fence_async_smem();  // rows written by the register path -> async proxy
         for (int k = 0; k < pro; ++k) {
-          mbar_expect_tx(bar0 + 8 * k, K::STAGE);
-          if constexpr (KC == 1) tensor_load(stage0 + k * K::STAGE, msrc, k * C, y, bar0 + 8 * k);
-          else tensor_load3(stage0 + k * K::STAGE, msrc, y, k * KC, bar0 + 8 * k);
+          const int s = static_cast<int>((sbase + k) % S);
+          mbar_expect_tx(bar0 + 8 * s, K::STAGE);
+          if constexpr (KC == 1) tensor_load(stage0 + s * K::STAGE, msrc, k * C, y, bar0 + 8 * s);
+          else tensor_load3(stage0 + s * K::STAGE, msrc, y, k * KC, bar0 + 8 * s);
         }
       }
       const int sw = lane & 7;  // (lane + 32 r) & 7 == lane & 7
       for (int k = 0; k < nsteps; ++k) {
-        const int s = k % S;
+        const int s = static_cast<int>((sbase + k) % S);
         mbar_wait(bar0 + 8 * s, (phase >> s) & 1u);
         phase ^= 1u << s;
         const uint32_t tile = stage0 + s * K::STAGE;
@@ -374,8 +392,32 @@ __global__ void __launch_bounds__(W * 32) slice_kernel(const __grid_constant__ S
             if constexpr (KC == 1) tensor_load(tile, msrc, (k + S) * C, y, bar0 + 8 * s);
             else tensor_load3(tile, msrc, y, (k + S) * KC, bar0 + 8 * s);
           }
+        } else if (job.prefetch_next) {
+          if (k + S == nsteps) {  // this task's refills are done: claim the next one now
+            claimed = true;
+            g_pf = claim();
+            if (g_pf != kNone) {
+              const SliceRegion P = region_of(g_pf);
+              pf_ok = P.tmap >= 0 && (g_pf - P.group_base) * K::ROWS + K::ROWS <= P.nfull;
+            }
+          }
+          if (pf_ok) {  // step j = k + S - nsteps of the next task, into the stage step k frees
+            __syncwarp();
+            if (lane == 0) {
+              const SliceRegion P = region_of(g_pf);
+              const CUtensorMap* psrc = &job.maps[3 * P.tmap];
+              const int py = static_cast<int>((g_pf - P.group_base) * K::ROWS);
+              const int j = k + S - nsteps;
+              if constexpr (kCopy) bulk_wait_read_all();
+              if (job.proxy_fence) fence_async_smem();
+              mbar_expect_tx(bar0 + 8 * s, K::STAGE);
+              if constexpr (KC == 1) tensor_load(tile, psrc, j * C, py, bar0 + 8 * s);
+              else tensor_load3(tile, psrc, py, j * KC, bar0 + 8 * s);
+            }
+          }
         }
       }
+      sbase = static_cast<uint32_t>((sbase + nsteps) % S);
     } else {
       // ---- register path: ragged tail or unaligned pointers, 32 slices at a time ----
       uint4* rows = reinterpret_cast<uint4*>(wbase);
@@ -433,6 +475,13 @@ __global__ void __launch_bounds__(W * 32) slice_kernel(const __grid_constant__ S
           atomicAdd(&job.result[1], 1ull);
         }
       }
+    }
+    if (claimed) {
+      g = g_pf;
+      prefetched = pf_ok;
+    } else {
+      g = claim();
+      prefetched = false;
     }
   }
 
@@ -679,6 +728,11 @@ cudaError_t launch_slices(const SliceJob& job_in, SliceMode mode, bool commit, u
   job.claim_order = order;
   static const uint32_t hint = std::getenv("FFX_STORE_HINT") != nullptr ? 1u : 0u;
   job.store_hint = hint;
+  static const uint32_t prefetch = [] {
+    const char* e = std::getenv("FFX_PREFETCH");
+    return e ? static_cast<uint32_t>(std::atoi(e)) : 0u;
+  }();
+  job.prefetch_next = prefetch;
   switch (mode) {
     case SliceMode::Hash:
       return commit ? launch_mode<SliceMode::Hash, true>(job, max_ctas, stream)
