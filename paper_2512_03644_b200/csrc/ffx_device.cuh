@@ -17,7 +17,9 @@ constexpr uint64_t kGolden = 0x9E3779B97F4A7C15ull;    // evolution.cpp:44, :76
 //   (h ^ b) * (2^40 + Q) mod 2^64  =  hi*Q*2^32 + x*2^40 + x*Q
 // so lo' = lo32(x*Q) and hi' = hi*Q + hi32(x*Q) + (x << 8): one wide
 // multiply, one multiply-add and one shift-add per byte.
-struct Fnv {
+// kAluShift selects how the (x << 8) add is issued -- see byte().
+template <bool kAluShift>
+struct FnvT {
   uint32_t lo, hi;
 
   __device__ __forceinline__ void init() {
@@ -32,14 +34,29 @@ struct Fnv {
     return (static_cast<uint64_t>(hi) << 32) | lo;
   }
   // Written as mul.lo/mul.hi/mad so ptxas folds hi32(x*Q) into the hi*Q
-  // multiply-add and splits the (x << 8) add between LEA (ALU pipe) and IMAD
-  // (FMA pipe): ~4.75 issue slots per byte, balanced across the two pipes.
+  // multiply-add (IMAD.WIDE + IMAD on the FMA-heavy pipe).  The (x << 8) add:
+  //  * kAluShift = false: `t + (x << 8)`, which ptxas issues as IMAD x*256 + t
+  //    for ~3/4 of the bytes (FMA-heavy) and LEA for the rest;
+  //  * kAluShift = true: a funnel shift + add, which ptxas fuses into one
+  //    LEA.HI on the ALU pipe, unloading the FMA-heavy pipe (66% busy in the
+  //    fused kernel, ncu).
+  // Same-box A/B (profiles/r1_fnv_alu_shift_ab_1gpu.txt): the ALU form makes
+  // checksum-only launches 3.4% faster (3543-3551 -> 3666-3671 GB/s) but the
+  // fused copy+hash kernel 0.7% slower (its ALU pipe also carries the TMA /
+  // barrier bookkeeping), so the kernels pick per mode.  With no memory in
+  // the way (tools/fnv_pipe_probe.cu) the ALU form is 5-25% faster.
   __device__ __forceinline__ void byte(uint32_t b) {
     const uint32_t x = lo ^ b;
     uint32_t plo, phi, t;
     asm("mul.lo.u32 %0, %2, 0x1b3;\n\tmul.hi.u32 %1, %2, 0x1b3;" : "=r"(plo), "=r"(phi) : "r"(x));
     asm("mad.lo.u32 %0, %1, 0x1b3, %2;" : "=r"(t) : "r"(hi), "r"(phi));
-    hi = t + (x << 8);
+    if constexpr (kAluShift) {
+      uint32_t s;
+      asm("shf.l.wrap.b32 %0, %1, %2, 8;" : "=r"(s) : "r"(0u), "r"(x));  // x << 8
+      asm("add.u32 %0, %1, %2;" : "=r"(hi) : "r"(t), "r"(s));
+    } else {
+      hi = t + (x << 8);
+    }
     lo = plo;
   }
   // Four bytes of a little-endian word, in memory order.
@@ -56,6 +73,8 @@ struct Fnv {
     word(v.w);
   }
 };
+using Fnv = FnvT<false>;     // copy + hash kernels
+using FnvAlu = FnvT<true>;   // checksum-only kernels
 
 // evo::mix64 including its leading golden-ratio add (evolution.cpp:43-48).
 __device__ __forceinline__ uint64_t mix64(uint64_t x) {

@@ -26,6 +26,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <type_traits>
 #include <cstdlib>
 
 #include <cudaTypedefs.h>
@@ -296,7 +297,7 @@ __global__ void __launch_bounds__(W * 32) slice_kernel(const __grid_constant__ S
     const bool al = aligned16(R.src) && (!kCopy || aligned16(R.dst));
     const uint64_t s0 = (g - R.group_base) * K::ROWS;
 
-    Fnv h[RPL];
+    std::conditional_t<kCopy, Fnv, FnvAlu> h[RPL];  // hash form per mode (ffx_device.cuh)
     uint64_t len[RPL];
 #pragma unroll
     for (int r = 0; r < RPL; ++r) {

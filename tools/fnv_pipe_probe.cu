@@ -35,6 +35,30 @@ struct FnvB {
   }
 };
 
+// D/E: the current mul.lo/mul.hi/mad, with (x << 8) moved off the FMA-heavy
+// pipe: D builds it with PRMT (byte permute), E with a funnel shift; both add
+// with IADD3 (ALU pipe) instead of the IMAD x*256 + t ptxas otherwise picks.
+template <int How>
+struct FnvD {
+  uint32_t lo, hi;
+  __device__ __forceinline__ void byte(uint32_t b) {
+    const uint32_t x = lo ^ b;
+    uint32_t plo, phi, t, s;
+    asm("mul.lo.u32 %0, %2, 0x1b3;\n\tmul.hi.u32 %1, %2, 0x1b3;" : "=r"(plo), "=r"(phi) : "r"(x));
+    asm("mad.lo.u32 %0, %1, 0x1b3, %2;" : "=r"(t) : "r"(hi), "r"(phi));
+    if constexpr (How == 0) s = __byte_perm(x, 0u, 0x2104);
+    else asm("shf.l.wrap.b32 %0, %1, %2, 8;" : "=r"(s) : "r"(0u), "r"(x));
+    asm("add.u32 %0, %1, %2;" : "=r"(hi) : "r"(t), "r"(s));
+    lo = plo;
+  }
+  __device__ __forceinline__ void word(uint32_t w) {
+    byte(w & 0xffu);
+    byte(__byte_perm(w, 0u, 0x4441));
+    byte(__byte_perm(w, 0u, 0x4442));
+    byte(w >> 24);
+  }
+};
+
 // C: plain 64-bit C++ (what nvcc makes of h = (h ^ b) * P)
 struct FnvC {
   uint64_t h;
@@ -67,6 +91,20 @@ __global__ void probe(const uint4* __restrict__ in, uint64_t* out, int reps) {
     for (int c = 0; c < CH; ++c) acc ^= h[c].value();
   } else if constexpr (V == 1) {
     FnvB h[CH];
+#pragma unroll
+    for (int c = 0; c < CH; ++c) { h[c].lo = 0x84222325u + c; h[c].hi = 0xcbf29ce4u; }
+    for (int r = 0; r < reps; ++r)
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int c = 0; c < CH; ++c) {
+          const uint4 w = v[(i + c) & 7];
+          h[c].word(w.x); h[c].word(w.y); h[c].word(w.z); h[c].word(w.w);
+        }
+#pragma unroll
+    for (int c = 0; c < CH; ++c) acc ^= (static_cast<uint64_t>(h[c].hi) << 32) | h[c].lo;
+  } else if constexpr (V == 3 || V == 4) {
+    FnvD<V - 3> h[CH];
 #pragma unroll
     for (int c = 0; c < CH; ++c) { h[c].lo = 0x84222325u + c; h[c].hi = 0xcbf29ce4u; }
     for (int r = 0; r < reps; ++r)
@@ -120,8 +158,12 @@ void run(const char* name, const uint4* in, uint64_t* out, int sms, int max_thre
     float ms = 0;
     cudaEventElapsedTime(&ms, a, b);
     const double bytes = static_cast<double>(blocks) * threads * CH * 128.0 * reps;
-    printf("{\"variant\": \"%s\", \"chains_per_lane\": %d, \"warps_per_sm\": %d, \"hash_gbs\": %.1f, \"err\": \"%s\"}\n",
-           name, CH, warps_per_sm, bytes / (ms * 1e-3) / 1e9, cudaGetErrorString(cudaGetLastError()));
+    uint64_t h0 = 0;
+    cudaMemcpy(&h0, out, 8, cudaMemcpyDeviceToHost);
+    printf("{\"variant\": \"%s\", \"chains_per_lane\": %d, \"warps_per_sm\": %d, \"hash_gbs\": %.1f, "
+           "\"lane0_hash\": \"%016llx\", \"err\": \"%s\"}\n",
+           name, CH, warps_per_sm, bytes / (ms * 1e-3) / 1e9, static_cast<unsigned long long>(h0),
+           cudaGetErrorString(cudaGetLastError()));
     cudaEventDestroy(a);
     cudaEventDestroy(b);
   }
@@ -138,10 +180,14 @@ int main() {
   cudaMalloc(&in, static_cast<size_t>(max_threads) * 128);
   cudaMalloc(&out, static_cast<size_t>(max_threads) * 8);
   cudaMemset(in, 0x5a, static_cast<size_t>(max_threads) * 128);
-  run<0, 1>("current(asm mul.lo/hi+mad)", in, out, sms, max_threads);
-  run<0, 2>("current(asm mul.lo/hi+mad)", in, out, sms, max_threads);
+  run<0, 1>("Fnv::byte (ffx_device.cuh)", in, out, sms, max_threads);
+  run<0, 2>("Fnv::byte (ffx_device.cuh)", in, out, sms, max_threads);
   run<1, 1>("wide-addend", in, out, sms, max_threads);
   run<1, 2>("wide-addend", in, out, sms, max_threads);
+  run<3, 1>("shift-by-prmt", in, out, sms, max_threads);
+  run<3, 2>("shift-by-prmt", in, out, sms, max_threads);
+  run<4, 1>("shift-by-shf", in, out, sms, max_threads);
+  run<4, 2>("shift-by-shf", in, out, sms, max_threads);
   run<2, 1>("plain-u64", in, out, sms, max_threads);
   run<2, 2>("plain-u64", in, out, sms, max_threads);
   return 0;
