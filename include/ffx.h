@@ -541,8 +541,15 @@ int ffx_snapshot_pull(ffx_ctx* ctx, ffx_remote* origin, ffx_replica* held, uint6
 int ffx_snapshot_begin_pull(ffx_ctx* ctx, ffx_remote* origin, ffx_replica* held, uint64_t iteration,
                             const ffx_snapshot_opts* opts, uint32_t* batches);
 /* Origin: make `stream` wait until the holder has committed `iteration`
- * (cuStreamWaitValue64 on the ack word; no kernel, no host round trip). */
+ * (cuStreamWaitValue64 on the ack word; no kernel, no host round trip).
+ * The ack is a one-shot token: the wait matches the committed iteration
+ * exactly and then consumes it, so call it once per pulled iteration. */
 int ffx_snapshot_wait_pulled(ffx_ctx* ctx, uint64_t iteration, void* stream);
+/* Origin: drop any un-consumed ack (stream-ordered).  Call on a rollback to
+ * the global consistent iteration (controller.cpp:315-318, ledger rebase):
+ * a replayed iteration must wait for its own re-pull.  ffx_recover* reset it
+ * implicitly. */
+int ffx_snapshot_ack_reset(ffx_ctx* ctx, void* stream);
 
 /* ---- recovery (assemble_restore, ckpt.cpp:111-167) ------------------------ */
 

@@ -485,6 +485,7 @@ extern "C" int ffx_open(int device, const ffx_cluster_spec* spec, ffx_role self,
   c->slice_bytes = slice_bytes;
   cudaError_t e = cudaMalloc(&c->done, 256);
   if (e == cudaSuccess) e = cudaMemset(c->done, 0, 256);
+  if (e == cudaSuccess) e = cudaMemset(c->done + kAckWord, 0xff, 8);  // kAckNone
   if (e == cudaSuccess) e = cudaMalloc(&c->result, 16);
   if (e == cudaSuccess) e = cudaMallocHost(&c->result_host, 16);
   if (e == cudaSuccess) e = cudaEventCreate(&c->ev0);

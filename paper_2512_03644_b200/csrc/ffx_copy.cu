@@ -161,6 +161,7 @@ __global__ void __launch_bounds__(32) copy_kernel(const __grid_constant__ CopyJo
   }
 }
 
+#ifdef FFX_DEV
 // SM copy (measurement reference for the probe, FFX_COPY_SM=1): grid-stride
 // 16-byte loads / stores, 4 in flight per thread.
 __global__ void __launch_bounds__(256) sm_copy_kernel(const __grid_constant__ CopyJob job) {
@@ -183,6 +184,7 @@ __global__ void __launch_bounds__(256) sm_copy_kernel(const __grid_constant__ Co
     if (blockIdx.x == 0 && threadIdx.x < R.bytes % 16) R.dst[nv * 16 + threadIdx.x] = R.src[nv * 16 + threadIdx.x];
   }
 }
+#endif  // FFX_DEV
 
 // Single thread: the final slot commit (meta, SNP1 header, then COMMITTED).
 __global__ void commit_kernel(const __grid_constant__ SlotCommit c) {
@@ -239,11 +241,13 @@ cudaError_t launch_copy(const CopyJob& job, uint32_t ctas, cudaStream_t stream) 
     if (e != cudaSuccess) return e;
     set_on |= bit;
   }
+#ifdef FFX_DEV
   static const bool sm = std::getenv("FFX_COPY_SM") != nullptr;
   if (sm && job.chunk_lo == 0 && job.chunk_hi == job.total_chunks && job.mark.slot == nullptr) {
     sm_copy_kernel<<<ctas ? ctas : 148 * 8, 256, 0, stream>>>(job);
     return cudaGetLastError();
   }
+#endif
   const uint64_t n = job.chunk_hi - job.chunk_lo;
   const uint64_t grid = std::max<uint64_t>(1, std::min<uint64_t>(n, ctas ? ctas : 16));
   copy_kernel<<<static_cast<unsigned>(grid), 32, kCopySmem, stream>>>(job);

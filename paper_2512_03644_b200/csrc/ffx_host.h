@@ -66,6 +66,9 @@ inline uint64_t rd(const uint8_t* p, int n) {
 // 16-17 split hash-batch task counter, 20-21 hybrid fused-share task
 // counter, 24-25 pull-mode ack (u64).
 constexpr uint32_t kAckWord = 24;
+// No pulled iteration pending (the ack word's value at open, after every
+// consumed wait and after a rollback / recovery).
+constexpr uint64_t kAckNone = ~0ull;
 
 inline bool valid_spec(const ffx_cluster_spec* s) {
   return s && s->data_parallel && s->pipeline_parallel && s->tensor_parallel && s->gpus_per_node;
@@ -161,7 +164,7 @@ struct PendingSnapshot {
   bool active = false;
   SliceJob job{};  // fused: copy + hash (+ commit); split: the hash-only job
   uint32_t batches = 1, next = 0, max_ctas = 0, slot = 0, slot2 = 0;
-  uint64_t iteration = 0, seq = 0, nslices = 0, logical = 0;
+  uint64_t iteration = 0, seq = 0, seq2 = 0, nslices = 0, logical = 0;
   bool verify = false;
   // split policy: copy batches and hash batches drain independently
   bool split = false, copy_engine = false;
@@ -243,6 +246,11 @@ void release_shared(ffx_replica* r);
 int preload_fetch(ffx_preload* p, uint64_t iteration, const void* host_src, const uint8_t* digests, uint32_t count,
                   uint32_t sample_bytes, uint64_t bytes, cudaStream_t s, cudaEvent_t gate);
 
+}  // namespace ffx::host
+
+namespace ffx::host {
+// Set ctx's pull-mode ack word to kAckNone on stream s (stream-ordered).
+int reset_ack(ffx_ctx* c, cudaStream_t s);
 }  // namespace ffx::host
 
 using namespace ffx::host;

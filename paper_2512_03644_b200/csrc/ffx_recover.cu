@@ -37,6 +37,11 @@ int check_source(ffx_ctx* c, ffx_replica* src, uint64_t target, SlotMeta* m, uin
 
 }  // namespace
 
+int ffx::host::reset_ack(ffx_ctx* c, cudaStream_t s) {
+  FFX_CUDA(cudaMemsetAsync(c->done + kAckWord, 0xff, 8, s));
+  return FFX_OK;
+}
+
 extern "C" int ffx_recover_from(ffx_ctx* c, ffx_replica* const* srcs, uint32_t nsrc, uint64_t target,
                                 void* stream, ffx_recover_report* rep) {
   if (!c || !srcs || nsrc == 0 || nsrc > 4) return fail(FFX_EINVAL, "recover: 1..4 sources");
@@ -80,6 +85,9 @@ extern "C" int ffx_recover_from(ffx_ctx* c, ffx_replica* const* srcs, uint32_t n
   job.result = c->result;
   job.sched = c->done + 12;
   finalize_job(job);
+  // restored state = a rollback: an ack left over from before the failure
+  // must not release a replayed iteration's optimizer update
+  if (int ast = reset_ack(c, s)) return ast;
   const unsigned long long init[2] = {~0ull, 0ull};
   FFX_CUDA(cudaMemcpyAsync(c->result, init, sizeof init, cudaMemcpyHostToDevice, s));
   FFX_CUDA(cudaEventRecord(c->ev0, s));
@@ -167,6 +175,9 @@ extern "C" int ffx_recover_full(ffx_ctx* c, ffx_replica* const* srcs, uint32_t n
   job.result = c->result;
   job.sched = c->done + 12;
   finalize_job(job);
+  // restored state = a rollback: an ack left over from before the failure
+  // must not release a replayed iteration's optimizer update
+  if (int ast = reset_ack(c, s)) return ast;
   const unsigned long long init[2] = {~0ull, 0ull};
   FFX_CUDA(cudaMemcpyAsync(c->result, init, sizeof init, cudaMemcpyHostToDevice, s));
   FFX_CUDA(cudaEventRecord(c->ev0, s));
@@ -212,6 +223,9 @@ extern "C" int ffx_recover_region(ffx_ctx* c, uint32_t idx, const void* peer_src
   job.sums_expected = peer_sums;
   job.result = c->result;
   job.sched = c->done + 12;
+  // restored state = a rollback: an ack left over from before the failure
+  // must not release a replayed iteration's optimizer update
+  if (int ast = reset_ack(c, s)) return ast;
   const unsigned long long init[2] = {~0ull, 0ull};
   FFX_CUDA(cudaMemcpyAsync(c->result, init, sizeof init, cudaMemcpyHostToDevice, s));
   FFX_CUDA(cudaEventRecord(c->ev0, s));

@@ -38,6 +38,16 @@ namespace ffx {
 
 namespace {
 
+// Tuning experiments (kernel variants, start-up stagger, claim order, store
+// hints, cross-task prefetch, per-step proxy fences) are compiled only into
+// development builds (make DEV=1 -> -DFFX_DEV); the product library carries
+// one configuration per mode and none of their branches.
+#ifdef FFX_DEV
+constexpr bool kDev = true;
+#else
+constexpr bool kDev = false;
+#endif
+
 __device__ __forceinline__ uint64_t umin64(uint64_t a, uint64_t b) { return a < b ? a : b; }
 
 __device__ __forceinline__ bool aligned16(const void* p) {
@@ -253,7 +263,7 @@ __global__ void __launch_bounds__(W * 32) slice_kernel(const __grid_constant__ S
   }
 
   const uint64_t Sl = job.slice_bytes;
-  if (job.stagger_ns) __nanosleep(((blockIdx.x * W + warp) & 7u) * job.stagger_ns);
+  if (kDev && job.stagger_ns) __nanosleep(((blockIdx.x * W + warp) & 7u) * job.stagger_ns);
   uint64_t g_next = job.group_lo + static_cast<uint64_t>(blockIdx.x) * W + warp;
   const uint64_t g_stride = static_cast<uint64_t>(gridDim.x) * W;
   constexpr uint64_t kNone = ~0ull;
@@ -268,7 +278,7 @@ __global__ void __launch_bounds__(W * 32) slice_kernel(const __grid_constant__ S
       if (lane == 0) t = atomicAdd(&job.sched[0], 1u);
       t = __shfl_sync(0xffffffffu, t, 0);
       if (t >= job.group_hi - job.group_lo) return kNone;
-      return (job.claim_order == 0 || t == 0) ? job.group_hi - 1 - t : job.group_lo + t - 1;
+      return (!kDev || job.claim_order == 0 || t == 0) ? job.group_hi - 1 - t : job.group_lo + t - 1;
     }
     const uint64_t gg = g_next;
     g_next += g_stride;
@@ -344,7 +354,7 @@ __global__ void __launch_bounds__(W * 32) slice_kernel(const __grid_constant__ S
               tensor_store(mdst, k * C, y, tile);
               if (dual) tensor_store(mdst2, k * C, y, tile);  // double neighbour: read once, write twice
             } else {
-              if (job.store_hint) {
+              if (kDev && job.store_hint) {
                 const uint64_t pol = evict_first_policy();
                 tensor_store3_hint(mdst, y, k * KC, tile, pol);
                 if (dual) tensor_store3_hint(mdst2, y, k * KC, tile, pol);
@@ -388,12 +398,12 @@ __global__ void __launch_bounds__(W * 32) slice_kernel(const __grid_constant__ S
           __syncwarp();
           if (lane == 0) {
             if constexpr (kCopy) bulk_wait_read_all();
-            if (job.proxy_fence) fence_async_smem();
+            if (kDev && job.proxy_fence) fence_async_smem();
             mbar_expect_tx(bar0 + 8 * s, K::STAGE);
             if constexpr (KC == 1) tensor_load(tile, msrc, (k + S) * C, y, bar0 + 8 * s);
             else tensor_load3(tile, msrc, y, (k + S) * KC, bar0 + 8 * s);
           }
-        } else if (job.prefetch_next) {
+        } else if (kDev && job.prefetch_next) {
           if (k + S == nsteps) {  // this task's refills are done: claim the next one now
             claimed = true;
             g_pf = claim();
@@ -410,7 +420,7 @@ __global__ void __launch_bounds__(W * 32) slice_kernel(const __grid_constant__ S
               const int py = static_cast<int>((g_pf - P.group_base) * K::ROWS);
               const int j = k + S - nsteps;
               if constexpr (kCopy) bulk_wait_read_all();
-              if (job.proxy_fence) fence_async_smem();
+              if (kDev && job.proxy_fence) fence_async_smem();
               mbar_expect_tx(bar0 + 8 * s, K::STAGE);
               if constexpr (KC == 1) tensor_load(tile, psrc, j * C, py, bar0 + 8 * s);
               else tensor_load3(tile, psrc, py, j * KC, bar0 + 8 * s);
@@ -537,7 +547,20 @@ cudaError_t launch_t(const SliceJob& job, uint32_t max_ctas, cudaStream_t stream
   return cudaGetLastError();
 }
 
-// Kernel variants for tuning: FFX_SLICE_VARIANT selects chunk/stages/warps.
+// Kernel configurations: stages / warps per CTA / slices per lane / SM
+// stores instead of TMA stores / 128 B chunks per TMA op.  The warp-task
+// size (32 * RPL slices) follows the configuration.
+struct Variant {
+  int S, W, RPL, stg, KC;
+};
+#ifdef FFX_DEV
+// Development builds: the round-1 sweep table (FFX_SLICE_VARIANT /
+// FFX_HASH_VARIANT; profiles/r1_variant_sweep_*.jsonl).
+constexpr Variant kVariants[] = {{3, 4, 1, 0, 2}, {2, 4, 2, 0, 1}, {3, 4, 2, 0, 1}, {6, 4, 1, 0, 1},
+                                 {3, 4, 1, 0, 1}, {2, 8, 2, 0, 1}, {4, 4, 1, 1, 1}, {3, 4, 2, 1, 1},
+                                 {6, 4, 1, 1, 1}, {2, 4, 1, 0, 2}, {4, 4, 1, 0, 1}, {2, 4, 1, 0, 4},
+                                 {2, 8, 1, 0, 2}, {2, 4, 1, 0, 1}};
+constexpr int kHashDefault = 9;
 int variant() {
   static const int v = [] {
     const char* e = std::getenv("FFX_SLICE_VARIANT");
@@ -545,29 +568,26 @@ int variant() {
   }();
   return v;
 }
-
-// Kernel variants for tuning (FFX_SLICE_VARIANT): stages / warps per CTA /
-// slices per lane.  The warp-task size (32 * RPL slices) follows the variant.
-struct Variant {
-  int S, W, RPL, stg, KC;
-};
-// 0 (default): 3 stages, 4 warps, 1 slice per lane, 2 chunks (256 B of
-// each slice) per TMA op -- the best of the round-1 sweep
-// (profiles/r1_variant_sweep_1gpu.jsonl); 10 was the previous default.
-constexpr Variant kVariants[] = {{3, 4, 1, 0, 2}, {2, 4, 2, 0, 1}, {3, 4, 2, 0, 1}, {6, 4, 1, 0, 1},
-                                 {3, 4, 1, 0, 1}, {2, 8, 2, 0, 1}, {4, 4, 1, 1, 1}, {3, 4, 2, 1, 1},
-                                 {6, 4, 1, 1, 1}, {2, 4, 1, 0, 2}, {4, 4, 1, 0, 1}, {2, 4, 1, 0, 4},
-                                 {2, 8, 1, 0, 2}, {2, 4, 1, 0, 1}};
+#else
+// Product: [0] copy modes -- 3 stages, 4 warps, 1 slice per lane, 2 chunks
+// (256 B of each slice) per TMA op, the best of the round-1 sweep
+// (profiles/r1_variant_sweep_1gpu.jsonl); [1] checksum-only modes -- the
+// same boxes with 2 stages (no store to wait for: 3.63 vs 3.29 TB/s
+// hash-only, profiles/r1_hash_variant_sweep.txt).
+constexpr Variant kVariants[] = {{3, 4, 1, 0, 2}, {2, 4, 1, 0, 2}};
+constexpr int kHashDefault = 1;
+int variant() { return 0; }
+#endif
 
 // Checksum-only launches (split-policy hash batches, HashVerify, the whole
-// FNV's sub-segment pass) may use another configuration than the fused
-// kernel (FFX_HASH_VARIANT): no store traffic, so fewer stages / planes and
-// more resident warps; the warp task must stay the same size (RPL).
+// FNV's sub-segment pass) use their own configuration: no store traffic, so
+// fewer stages; the warp task must stay the same size (RPL).
 int hash_variant();
 
 template <SliceMode M, bool kCommit>
 cudaError_t launch_mode(const SliceJob& job, uint32_t max_ctas, cudaStream_t stream) {
-  const bool hash_only = M == SliceMode::Hash || M == SliceMode::HashVerify;
+  constexpr bool hash_only = M == SliceMode::Hash || M == SliceMode::HashVerify;
+#ifdef FFX_DEV
   switch (hash_only ? hash_variant() : variant()) {
     case 1: return launch_t<2, 4, 2, false, M, kCommit>(job, max_ctas, stream);
     case 2: return launch_t<3, 4, 2, false, M, kCommit>(job, max_ctas, stream);
@@ -584,6 +604,10 @@ cudaError_t launch_mode(const SliceJob& job, uint32_t max_ctas, cudaStream_t str
     case 13: return launch_t<2, 4, 1, false, M, kCommit>(job, max_ctas, stream);
     default: return launch_t<3, 4, 1, false, M, kCommit, 2>(job, max_ctas, stream);
   }
+#else
+  if constexpr (hash_only) return launch_t<2, 4, 1, false, M, kCommit, 2>(job, max_ctas, stream);
+  else return launch_t<3, 4, 1, false, M, kCommit, 2>(job, max_ctas, stream);
+#endif
 }
 
 }  // namespace
@@ -609,17 +633,18 @@ int task_rows() { return 32 * active_variant().RPL; }
 
 namespace {
 int hash_variant() {
+#ifdef FFX_DEV
   static const int v = [] {
     const char* e = std::getenv("FFX_HASH_VARIANT");
-    // default: 2 stages instead of 3 -- the checksum-only pipeline has no
-    // store to wait for; +10% hash-only throughput (3.63 vs 3.29 TB/s,
-    // profiles/r1_hash_variant_sweep.txt)
-    const int h = e ? std::atoi(e) : (variant() == 0 ? 9 : variant());
+    const int h = e ? std::atoi(e) : (variant() == 0 ? kHashDefault : variant());
     const int n = static_cast<int>(sizeof kVariants / sizeof kVariants[0]);
     // same warp-task size as the fused kernel's jobs (finalize_job), else the fused variant
     return (h >= 0 && h < n && kVariants[h].RPL == active_variant().RPL) ? h : variant();
   }();
   return v;
+#else
+  return kHashDefault;
+#endif
 }
 }  // namespace
 
@@ -714,26 +739,25 @@ cudaError_t launch_slices(const SliceJob& job_in, SliceMode mode, bool commit, u
   attach_tensor_maps(job, !hash_only, kVariants[(vi >= 0 && vi < nv) ? vi : 0].KC);
   // The refill of a stage is a generic-read -> async-write (WAR) sequence,
   // ordered by the warp barrier; the proxy fence is only required for
-  // generic writes read by the async proxy (kept per task, optional per step).
-  static const bool fence = std::getenv("FFX_STEP_FENCE") != nullptr;
-  job.proxy_fence = fence ? 1u : 0u;
-  static const uint32_t stagger = [] {
-    const char* e = std::getenv("FFX_STAGGER_NS");
+  // generic writes read by the async proxy (kept per task).  The per-step
+  // fence and the other experiment knobs exist only in FFX_DEV builds.
+  job.proxy_fence = job.stagger_ns = job.claim_order = job.store_hint = job.prefetch_next = 0;
+#ifdef FFX_DEV
+  static const auto env_u32 = [](const char* name) {
+    const char* e = std::getenv(name);
     return e ? static_cast<uint32_t>(std::strtoul(e, nullptr, 10)) : 0u;
-  }();
-  job.stagger_ns = stagger;
-  static const uint32_t order = [] {
-    const char* e = std::getenv("FFX_CLAIM_ORDER");
-    return e ? static_cast<uint32_t>(std::atoi(e)) : 0u;
-  }();
-  job.claim_order = order;
+  };
+  static const uint32_t fence = std::getenv("FFX_STEP_FENCE") != nullptr ? 1u : 0u;
+  static const uint32_t stagger = env_u32("FFX_STAGGER_NS");
+  static const uint32_t order = env_u32("FFX_CLAIM_ORDER");
   static const uint32_t hint = std::getenv("FFX_STORE_HINT") != nullptr ? 1u : 0u;
+  static const uint32_t prefetch = env_u32("FFX_PREFETCH");
+  job.proxy_fence = fence;
+  job.stagger_ns = stagger;
+  job.claim_order = order;
   job.store_hint = hint;
-  static const uint32_t prefetch = [] {
-    const char* e = std::getenv("FFX_PREFETCH");
-    return e ? static_cast<uint32_t>(std::atoi(e)) : 0u;
-  }();
   job.prefetch_next = prefetch;
+#endif
   switch (mode) {
     case SliceMode::Hash:
       return commit ? launch_mode<SliceMode::Hash, true>(job, max_ctas, stream)

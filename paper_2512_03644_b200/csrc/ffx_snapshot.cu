@@ -89,11 +89,21 @@ int begin_impl(ffx_ctx* c, ffx_replica* t, ffx_replica* t2, const std::vector<Sr
   }
   const uint32_t slot = pick_slot(t, iteration);
   const uint32_t slot2 = t2 ? pick_slot(t2, iteration) : 0;
-  uint64_t seq = ++c->seq;
+  // Insertion order: a fresh iteration gets the next sequence number; a
+  // replace-in-place keeps its slot's (ckpt.cpp:46-50 swaps the bytes but
+  // leaves the entry where it is in the deque), so eviction and newest()
+  // still follow the first insertion.
+  uint64_t fresh = ++c->seq;
   for (ffx_replica* rr : {t, t2})
     if (rr)
-      for (const auto& sc : rr->cache) seq = std::max(seq, sc.seq + 1);
-  c->seq = seq;
+      for (const auto& sc : rr->cache) fresh = std::max(fresh, sc.seq + 1);
+  c->seq = fresh;
+  auto seq_for = [&](const ffx_replica* rr, uint32_t v) {
+    const SlotCache& sc = rr->cache[v];
+    return (sc.state != kSlotEmpty && sc.iteration == iteration && sc.seq) ? sc.seq : fresh;
+  };
+  const uint64_t seq = seq_for(t, slot);
+  const uint64_t seq2 = t2 ? seq_for(t2, slot2) : seq;
 
   PendingSnapshot& P = c->pending;
   P = PendingSnapshot{};
@@ -142,6 +152,8 @@ int begin_impl(ffx_ctx* c, ffx_replica* t, ffx_replica* t2, const std::vector<Sr
     job.sums_out2 = t2->wsums(slot2);
     job.commit2 = cm;
     job.commit2.slot = t2->wslot(slot2);
+    job.commit2.seq = seq2;
+    reinterpret_cast<SlotMeta*>(job.commit2.meta)->seq = seq2;
     job.commit2.done = c->done + 4;
     job.commit2.payload_off = t2->layout.payload_off;
     P.slot2 = slot2;
@@ -164,6 +176,7 @@ int begin_impl(ffx_ctx* c, ffx_replica* t, ffx_replica* t2, const std::vector<Sr
   P.slot = slot;
   P.iteration = iteration;
   P.seq = seq;
+  P.seq2 = seq2;
   P.nslices = nslices;
   P.logical = logical;
   P.verify = opts.verify_on_store != 0;
@@ -185,7 +198,7 @@ int begin_impl(ffx_ctx* c, ffx_replica* t, ffx_replica* t2, const std::vector<Sr
       cj.reg[i] = CopyRegion{job.reg[i].src, job.reg[i].dst, job.reg[i].bytes, 0, 0, job.reg[i].dst2};
     finalize_copy_job(cj);
     cj.mark = SlotMark{t->wslot(slot), iteration, seq};
-    if (t2) cj.mark2 = SlotMark{t2->wslot(slot2), iteration, seq};
+    if (t2) cj.mark2 = SlotMark{t2->wslot(slot2), iteration, seq2};
     if (opts.fused_permille) {
       if (!P.copy_engine) {
         P.active = false;
@@ -392,16 +405,33 @@ extern "C" int ffx_snapshot_pull(ffx_ctx* c, ffx_remote* origin, ffx_replica* he
   return FFX_OK;
 }
 
+// The ack word is a one-shot token: the holder's commit writes the pulled
+// iteration, the origin's wait matches it EXACTLY and then consumes it
+// (writes kAckNone back, stream-ordered).  A ">= iteration" test on a
+// monotone word would let a replayed iteration after a rollback pass on the
+// pre-failure maximum while the holder is still reading the live buffers.
 extern "C" int ffx_snapshot_wait_pulled(ffx_ctx* c, uint64_t iteration, void* stream) {
   if (!c) return fail(FFX_EINVAL, "wait_pulled: null ctx");
-  using Fn = CUresult (*)(CUstream, CUdeviceptr, cuuint64_t, unsigned int);
-  static Fn fn = driver_fn<Fn>("cuStreamWaitValue64");
-  if (!fn) return fail(FFX_ECUDA, "cuStreamWaitValue64 unavailable");
+  if (iteration == kAckNone) return fail(FFX_EINVAL, "wait_pulled: iteration %llu is reserved",
+                                         (unsigned long long)iteration);
+  using WaitFn = CUresult (*)(CUstream, CUdeviceptr, cuuint64_t, unsigned int);
+  using WriteFn = CUresult (*)(CUstream, CUdeviceptr, cuuint64_t, unsigned int);
+  static WaitFn wait = driver_fn<WaitFn>("cuStreamWaitValue64");
+  static WriteFn write = driver_fn<WriteFn>("cuStreamWriteValue64");
+  if (!wait || !write) return fail(FFX_ECUDA, "cuStreamWaitValue64 / cuStreamWriteValue64 unavailable");
   DeviceGuard g(c->device);
-  if (fn(static_cast<CUstream>(stream), reinterpret_cast<CUdeviceptr>(c->done + kAckWord), iteration,
-         CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS)
+  const CUdeviceptr ack = reinterpret_cast<CUdeviceptr>(c->done + kAckWord);
+  if (wait(static_cast<CUstream>(stream), ack, iteration, CU_STREAM_WAIT_VALUE_EQ) != CUDA_SUCCESS)
     return fail(FFX_ECUDA, "cuStreamWaitValue64 failed");
+  if (write(static_cast<CUstream>(stream), ack, kAckNone, 0) != CUDA_SUCCESS)
+    return fail(FFX_ECUDA, "cuStreamWriteValue64 failed");
   return FFX_OK;
+}
+
+extern "C" int ffx_snapshot_ack_reset(ffx_ctx* c, void* stream) {
+  if (!c) return fail(FFX_EINVAL, "ack_reset: null ctx");
+  DeviceGuard g(c->device);
+  return reset_ack(c, as_stream(stream));
 }
 
 extern "C" int ffx_snapshot_begin(ffx_ctx* c, uint64_t iteration, const ffx_snapshot_opts* o,
@@ -515,7 +545,7 @@ int finish_snapshot(ffx_ctx* c, PendingSnapshot& P, cudaStream_t s) {
   P.active = false;
   ffx_replica* t = P.tgt;
   t->cache[P.slot] = SlotCache{true, kSlotCommitted, P.iteration, P.seq};
-  if (P.tgt2) P.tgt2->cache[P.slot2] = SlotCache{true, kSlotCommitted, P.iteration, P.seq};
+  if (P.tgt2) P.tgt2->cache[P.slot2] = SlotCache{true, kSlotCommitted, P.iteration, P.seq2};
   c->last_target = t;
   c->last_slot = P.slot;
   c->last_nslices = P.nslices;

@@ -285,6 +285,7 @@ SIGNATURES = {
     "ffx_snapshot_pull": (_I, [_P, _P, _P, _U64, _P, ctypes.POINTER(SnapshotOpts)]),
     "ffx_snapshot_begin_pull": (_I, [_P, _P, _P, _U64, ctypes.POINTER(SnapshotOpts), ctypes.POINTER(_U32)]),
     "ffx_snapshot_wait_pulled": (_I, [_P, _U64, _P]),
+    "ffx_snapshot_ack_reset": (_I, [_P, _P]),
     "ffx_snapshot_begin": (_I, [_P, _U64, ctypes.POINTER(SnapshotOpts), ctypes.POINTER(_U32)]),
     "ffx_snapshot_next": (_I, [_P, _P, _P, ctypes.POINTER(_U32)]),
     "ffx_snapshot_next_kind": (_I, [_P, _I, _P, _P, ctypes.POINTER(_U32)]),
@@ -1005,6 +1006,10 @@ class Context:
 
     def wait_pulled(self, iteration: int, stream=None):
         check(lib.ffx_snapshot_wait_pulled(self._c, iteration, _stream_ptr(stream)), "snapshot_wait_pulled")
+
+    def ack_reset(self, stream=None):
+        """Drop an un-consumed pull ack (rollback): see ffx_snapshot_ack_reset."""
+        check(lib.ffx_snapshot_ack_reset(self._c, _stream_ptr(stream)), "snapshot_ack_reset")
 
     def set_target2(self, replica: Optional[Replica]):
         check(lib.ffx_snapshot_target2(self._c, replica.ptr if replica else None), "snapshot_target2")

@@ -90,6 +90,34 @@ int main() {
   }
   EXPECT(threw);
 
+  // re-taking the OLDER held iteration keeps insertion order (ckpt.cpp:46-52):
+  // take(1) take(2) take(1) take(3) holds {2, 3}; framed(2) must still exist
+  {
+    const std::uint64_t m = 4096 + 5;
+    ckpt::HostSnapshots hs2(me, m);
+    std::vector<std::uint8_t> a(m, 1), b(m, 2), a2(m, 11), c(m, 3);
+    hs2.take(1, a);
+    hs2.take(2, b);
+    hs2.take(1, a2);
+    EXPECT(hs2.newest().value() == 2);
+    EXPECT(hs2.previous().value() == 1);
+    EXPECT(hs2.framed(1) && *hs2.framed(1) == store::pack_blob(me, 1, store::BlobKind::Optimizer, a2));
+    hs2.take(3, c);
+    EXPECT(hs2.framed(1) == nullptr);
+    EXPECT(hs2.framed(2) && *hs2.framed(2) == store::pack_blob(me, 2, store::BlobKind::Optimizer, b));
+    EXPECT(hs2.framed(3) && *hs2.framed(3) == store::pack_blob(me, 3, store::BlobKind::Optimizer, c));
+    EXPECT(hs2.newest().value() == 3);
+    ckpt::NeighborBuffer nb2(me);
+    nb2.store(store::pack_blob(me, 1, store::BlobKind::Optimizer, a));
+    nb2.store(store::pack_blob(me, 2, store::BlobKind::Optimizer, b));
+    nb2.store(store::pack_blob(me, 1, store::BlobKind::Optimizer, a2));
+    EXPECT(nb2.newest().value() == 2);
+    nb2.store(store::pack_blob(me, 3, store::BlobKind::Optimizer, c));
+    EXPECT(nb2.framed_at(1) == nullptr);
+    EXPECT(nb2.framed_at(2) && *nb2.framed_at(2) == store::pack_blob(me, 2, store::BlobKind::Optimizer, b));
+    EXPECT(nb2.newest().value() == 3);
+  }
+
   ffx_device_free(0, dev);
   std::printf("[facade-device] %s (%d failures)\n", failures ? "FAILED" : "ok", failures);
   return failures ? 1 : 0;

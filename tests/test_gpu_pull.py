@@ -87,3 +87,82 @@ def test_pull_matches_push_bytes(ffx):
     torch.cuda.synchronize()
     assert pushed.export_frame(5) == pulled.export_frame(5)
     remote.close()
+
+
+def _released(ev, wait_s=0.05):
+    import time
+    time.sleep(wait_s)
+    return ev.query()
+
+
+def test_pull_ack_is_a_one_shot_token(ffx):
+    """The origin's wait matches the pulled iteration exactly and consumes
+    it: a fresh ctx does not release wait(0), a consumed ack does not
+    release the same iteration twice, and after a rollback (ack_reset, or a
+    recovery) a replayed iteration waits for its own re-pull instead of
+    passing on the pre-failure ack (GEQ on a monotone word)."""
+    spec = ffx.make_spec(d=2, phi=64, distributed=True)
+    origin = ffx.Context(0, spec, (1, 0, 0))
+    holder = ffx.Context(0, spec, (0, 0, 0))
+    n = 1 << 20
+    state = torch.zeros(n, dtype=torch.uint8, device="cuda")
+    origin.register(ffx.REGION_BLOB, state)
+    held = holder.create_replica((1, 0, 0), n, 2)
+    remote = holder.open_remote(origin.export_regions())
+    s, o = torch.cuda.Stream(), torch.cuda.Stream()
+    pending = []  # iterations an origin wait is still blocked on (released in finally)
+    try:
+        # fresh ctx: nothing pulled yet, wait(0) must block
+        origin.wait_pulled(0, stream=o)
+        pending.append(0)
+        ev = torch.cuda.Event()
+        ev.record(o)
+        assert not _released(ev)
+        holder.snapshot_pull(remote, held, 0, stream=s)
+        ev.synchronize()
+        pending.pop()
+        # pulled 1, consumed once; a second wait on 1 blocks until a re-pull
+        holder.snapshot_pull(remote, held, 1, stream=s)
+        origin.wait_pulled(1, stream=o)
+        ev1 = torch.cuda.Event()
+        ev1.record(o)
+        ev1.synchronize()
+        origin.wait_pulled(1, stream=o)
+        pending.append(1)
+        ev2 = torch.cuda.Event()
+        ev2.record(o)
+        assert not _released(ev2)
+        holder.snapshot_pull(remote, held, 1, stream=s)
+        ev2.synchronize()
+        pending.pop()
+        # pulled 2, never waited on (the origin failed); rollback to 1 and
+        # replay 2: the stale ack must not release the replay
+        holder.snapshot_pull(remote, held, 2, stream=s)
+        s.synchronize()
+        origin.ack_reset(stream=o)
+        origin.wait_pulled(2, stream=o)
+        pending.append(2)
+        ev3 = torch.cuda.Event()
+        ev3.record(o)
+        assert not _released(ev3)
+        holder.snapshot_pull(remote, held, 2, stream=s)
+        ev3.synchronize()
+        pending.pop()
+        # recovery resets it too
+        holder.snapshot_pull(remote, held, 3, stream=s)
+        s.synchronize()
+        view = origin.open_replica(held.export())
+        origin.recover(view, 3)
+        origin.wait_pulled(3, stream=o)
+        pending.append(3)
+        ev4 = torch.cuda.Event()
+        ev4.record(o)
+        assert not _released(ev4)
+        holder.snapshot_pull(remote, held, 3, stream=s)
+        ev4.synchronize()
+        pending.pop()
+    finally:
+        for it in pending:  # never leave a stream blocked on the device
+            holder.snapshot_pull(remote, held, it, stream=s)
+        torch.cuda.synchronize()
+        remote.close()

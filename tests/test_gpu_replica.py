@@ -95,6 +95,37 @@ def test_two_version_rule_and_replace_in_place(ffx):
     assert rep.export_frame(4)[32:] == payloads[4]
 
 
+@pytest.mark.parametrize("dual", [False, True])
+def test_replace_older_iteration_keeps_insertion_order(ffx, dual):
+    # ckpt.cpp:46-52 / :86-92: re-taking the OLDER held iteration swaps its
+    # bytes but leaves it first in the deque, so take(1) take(2) take(1)
+    # take(3) keeps {2, 3} and newest() stays 2 after the re-take.
+    n = 8192
+    spec, holder, origin, rep, view = ring_pair(ffx, n)
+    rep2 = view2 = None
+    if dual:
+        rep2 = holder.create_replica((1, 0, 0), n, 2)
+        view2 = origin.open_replica(rep2.export())
+        origin.set_target2(view2)
+    state = torch.zeros(n, dtype=torch.uint8, device="cuda")
+    origin.register(ffx.REGION_BLOB, state)
+    for it, fill in ((1, 1), (2, 2), (1, 11)):
+        state.fill_(fill)
+        origin.snapshot(it)
+    torch.cuda.synchronize()
+    for r in [rep] + ([rep2] if dual else []):
+        assert r.newest() == 2
+        assert sorted(r.held()) == [1, 2]
+        assert r.export_frame(1)[32:] == bytes([11]) * n
+    state.fill_(3)
+    origin.snapshot(3)
+    torch.cuda.synchronize()
+    for r in [rep] + ([rep2] if dual else []):
+        assert sorted(r.held()) == [2, 3]
+        assert r.newest() == 3
+        assert r.export_frame(2)[32:] == bytes([2]) * n
+
+
 def test_capacity_config_error(ffx):
     # proj/tests/test_ckpt.cpp:220-221
     spec, holder, origin, rep, view = ring_pair(ffx, 16)
