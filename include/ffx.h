@@ -304,6 +304,13 @@ typedef struct ffx_slot_info {
 } ffx_slot_info;
 int ffx_replica_slots(const ffx_replica* r, uint32_t* versions);
 int ffx_replica_slot_info(ffx_replica* r, uint32_t slot, ffx_slot_info* out);
+/* The state registry a committed slot was taken from: *n regions (at most
+ * FFX_MAX_REGIONS) with their ffx_region_kind and byte sizes, in payload
+ * order -- what a replacement process allocates and registers before
+ * ffx_recover (the reference's StateBundle shape, domain.hpp:105-110).
+ * kinds / bytes may be NULL.  FFX_ERESTORE if the slot is not committed. */
+#define FFX_MAX_REGIONS 16
+int ffx_replica_slot_regions(ffx_replica* r, uint32_t slot, uint32_t* n, int32_t* kinds, uint64_t* bytes);
 /* NeighborBuffer::newest() (ckpt.cpp:102-105): FFX_ERESTORE if nothing committed. */
 int ffx_replica_newest(ffx_replica* r, uint64_t* iteration);
 /* Device pointers into slot `slot` (payload, checksum table). */

@@ -39,7 +39,8 @@ struct SlotMeta {  // exactly 256 bytes
   uint32_t num_regions;
   uint32_t reserved0;
   uint64_t region_bytes[kMaxRegions];  // 128 bytes
-  uint64_t reserved[7];
+  uint8_t region_kinds[kMaxRegions];   // ffx_region_kind of each region (a replacement allocates from these)
+  uint64_t reserved[5];
 };
 static_assert(sizeof(SlotMeta) == kMetaBytes, "SlotMeta must be 256 bytes");
 

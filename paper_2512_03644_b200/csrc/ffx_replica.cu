@@ -200,6 +200,25 @@ extern "C" int ffx_replica_destroy(ffx_replica* r) {
   return FFX_OK;
 }
 
+extern "C" int ffx_replica_slot_regions(ffx_replica* r, uint32_t slot, uint32_t* n, int32_t* kinds,
+                                        uint64_t* bytes) {
+  if (!r || !n) return fail(FFX_EINVAL, "slot_regions: null argument");
+  if (slot >= r->versions) return fail(FFX_ERANGE, "slot_regions: slot %u of %u", slot, r->versions);
+  SlotMeta m;
+  int st = read_meta(r, slot, &m);
+  if (st) return st;
+  *n = 0;
+  if (m.magic != kSlotMagic || m.state != kSlotCommitted)
+    return fail(FFX_ERESTORE, "slot_regions: slot %u holds no committed snapshot", slot);
+  if (m.num_regions > kMaxRegions) return fail(FFX_ECORRUPT, "slot_regions: %u regions", m.num_regions);
+  *n = m.num_regions;
+  for (uint32_t i = 0; i < m.num_regions; ++i) {
+    if (kinds) kinds[i] = m.region_kinds[i];
+    if (bytes) bytes[i] = m.region_bytes[i];
+  }
+  return FFX_OK;
+}
+
 extern "C" int ffx_replica_slots(const ffx_replica* r, uint32_t* versions) {
   if (!r || !versions) return fail(FFX_EINVAL, "replica_slots: null argument");
   *versions = r->versions;

@@ -54,6 +54,7 @@ namespace {
 struct SrcRegion {
   const uint8_t* dev;  // local or peer-mapped
   uint64_t bytes;
+  int kind;            // ffx_region_kind (recorded in the slot meta)
 };
 
 // Shared by push (sources = this rank's registered regions, destination = the
@@ -131,7 +132,10 @@ int begin_impl(ffx_ctx* c, ffx_replica* t, ffx_replica* t2, const std::vector<Sr
   m.tp = role.tp;
   m.kind = opts.weights_kind ? 0 : 1;
   m.num_regions = job.nregions;
-  for (size_t i = 0; i < srcs.size(); ++i) m.region_bytes[i] = srcs[i].bytes;
+  for (size_t i = 0; i < srcs.size(); ++i) {
+    m.region_bytes[i] = srcs[i].bytes;
+    m.region_kinds[i] = static_cast<uint8_t>(srcs[i].kind);
+  }
   uint8_t hdr[32];
   ffx_pack_header(role, iteration, m.kind, logical > 0xffffffffull ? 0 : logical, 0, hdr);
 
@@ -259,6 +263,7 @@ struct RegionsBlob {
   struct Entry {
     cudaIpcMemHandle_t ipc;
     uint64_t off, raw, bytes;
+    int32_t kind, pad_;
   } r[kMaxRegions];
 };
 static_assert(sizeof(RegionsBlob) <= FFX_REGIONS_HANDLE_BYTES, "regions handle too large");
@@ -300,6 +305,7 @@ extern "C" int ffx_regions_export(ffx_ctx* c, uint8_t handle[FFX_REGIONS_HANDLE_
     if (!r.unique) continue;
     auto& e = b.r[b.nregions++];
     e.bytes = r.bytes;
+    e.kind = r.kind;
     e.raw = reinterpret_cast<uint64_t>(r.dev);
     if (r.bytes == 0) continue;
     st = alloc_base(r.dev, &base);
@@ -357,9 +363,9 @@ extern "C" int ffx_remote_open(ffx_ctx* c, const uint8_t handle[FFX_REGIONS_HAND
   for (uint32_t i = 0; i < b.nregions && !st; ++i) {
     const auto& e = b.r[i];
     if (local || e.bytes == 0) {
-      r->regs.push_back(SrcRegion{reinterpret_cast<const uint8_t*>(e.raw), e.bytes});
+      r->regs.push_back(SrcRegion{reinterpret_cast<const uint8_t*>(e.raw), e.bytes, e.kind});
     } else if (!(st = map(e.ipc, &base))) {
-      r->regs.push_back(SrcRegion{base + e.off, e.bytes});
+      r->regs.push_back(SrcRegion{base + e.off, e.bytes, e.kind});
     }
   }
   if (st) {
@@ -440,7 +446,7 @@ extern "C" int ffx_snapshot_begin(ffx_ctx* c, uint64_t iteration, const ffx_snap
   if (!c->target) return fail(FFX_ESTATE, "snapshot: no target replica (ffx_snapshot_target)");
   std::vector<SrcRegion> srcs;
   for (const auto& r : c->regions)
-    if (r.unique) srcs.push_back(SrcRegion{r.dev, r.bytes});
+    if (r.unique) srcs.push_back(SrcRegion{r.dev, r.bytes, r.kind});
   return begin_impl(c, c->target, c->target2, srcs, c->self, nullptr, iteration, o, batches_out);
 }
 

@@ -255,6 +255,7 @@ SIGNATURES = {
     "ffx_replica_open": (_I, [_P, _P, ctypes.POINTER(_P)]),
     "ffx_replica_destroy": (_I, [_P]),
     "ffx_replica_slots": (_I, [_P, ctypes.POINTER(_U32)]),
+    "ffx_replica_slot_regions": (_I, [_P, _U32, ctypes.POINTER(_U32), ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(_U64)]),
     "ffx_replica_slot_info": (_I, [_P, _U32, ctypes.POINTER(SlotInfo)]),
     "ffx_replica_newest": (_I, [_P, ctypes.POINTER(_U64)]),
     "ffx_replica_slot_ptrs": (_I, [_P, _U32, ctypes.POINTER(_P), ctypes.POINTER(_P)]),
@@ -686,6 +687,14 @@ class Replica:
         s = SlotInfo()
         check(lib.ffx_replica_slot_info(self._h, slot, ctypes.byref(s)), "slot_info")
         return s
+
+    def slot_regions(self, slot: int):
+        """[(region kind, bytes)] of the committed snapshot in `slot`."""
+        n = _U32()
+        kinds = (ctypes.c_int32 * 16)()
+        sizes = (_U64 * 16)()
+        check(lib.ffx_replica_slot_regions(self._h, slot, ctypes.byref(n), kinds, sizes), "slot_regions")
+        return [(int(kinds[i]), int(sizes[i])) for i in range(n.value)]
 
     def newest(self) -> Optional[int]:
         it = ctypes.c_uint64()
