@@ -324,8 +324,10 @@ int run_standby(const Args& a) {
   plan.forwards = fw.data();
   plan.redundant_from = red.data();
   // --target: the ledger's global consistent iteration (controller.cpp:93-98);
-  // without it the holder's newest committed slot is the resume point
-  ck(ffx_plan_recovery(&spec, nullptr, 0, &me, 1, a.target, 0, 1, &plan), "plan_recovery");
+  // without it the holder's newest committed slot is the resume point.  (A
+  // zero global iteration plans no forwards -- nothing recorded yet,
+  // controller.cpp:175-176 -- so plan with 1 to learn the holder.)
+  ck(ffx_plan_recovery(&spec, nullptr, 0, &me, 1, a.target ? a.target : 1, 0, 1, &plan), "plan_recovery");
   if (plan.kind != FFX_PLAN_NEIGHBOR || plan.n_forwards != 1) {
     std::fprintf(stderr, "ffx_standby: plan is not a neighbour restore\n");
     return 3;

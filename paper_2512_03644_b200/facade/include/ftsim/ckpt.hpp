@@ -72,6 +72,10 @@ class HostSnapshots {
   std::optional<std::uint64_t> previous() const;
   Role role() const { return role_; }
   std::uint64_t capacity() const { return capacity_; }
+  // B200 extension (not in the reference API): the per-slice FNV-1a-64
+  // table of the most recent take(), copied to host memory without framing
+  // the payload; returns the number of entries copied (<= max).
+  std::uint64_t last_slice_checksums(std::uint64_t* host, std::uint64_t max) const;
 
  private:
   Role role_;

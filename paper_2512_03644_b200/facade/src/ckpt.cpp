@@ -149,6 +149,13 @@ const std::vector<std::uint8_t>* HostSnapshots::framed(std::uint64_t iteration) 
   return slots_->frame(iteration);
 }
 
+std::uint64_t HostSnapshots::last_slice_checksums(std::uint64_t* host, std::uint64_t max) const {
+  std::uint64_t n = 0;
+  b200::check(ffx_snapshot_read_sums(slots_->ctx, host, max, &n, nullptr), "read_sums");
+  b200::check(ffx_stream_sync(nullptr), "sync");
+  return n;
+}
+
 std::optional<std::uint64_t> HostSnapshots::newest() const {
   if (slots_->kept.empty()) return std::nullopt;
   return slots_->kept.back();

@@ -211,3 +211,14 @@ def test_plain_c_host_compiles_against_the_abi(tmp_path):
                         "-Wl,-rpath," + os.path.join(root, "paper_2512_03644_b200"), "-o", str(out)],
                        capture_output=True, text=True)
     assert r.returncode == 0, r.stderr
+
+
+def test_facade_c_entry_points_exported():
+    """include/ftsim_capi.h: every declared ftsim_* symbol is exported by the
+    facade library (the C route to HostSnapshots for ctypes / cgo / JNI)."""
+    src = open(os.path.join(ROOT, "include", "ftsim_capi.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    syms = sorted(set(re.findall(r"^\s*(?:const\s+)?\w+\s*\*?\s*(ftsim_\w+)\s*\(", src, flags=re.M)))
+    assert len(syms) == 7
+    lib = ctypes.CDLL(os.path.join(ROOT, "paper_2512_03644_b200", "libftsim_b200.so"))
+    assert [s for s in syms if not hasattr(lib, s)] == []

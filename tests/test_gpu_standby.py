@@ -72,7 +72,8 @@ def failover(tmp_path, regs1, regs2, d, phi, role=1, warm=True, device=0):
                         "--regions2", ",".join(r.spec() for r in regs2)])
         assert _readline(origin, "SNAPSHOTTED") == "SNAPSHOTTED 2"
         samples = os.path.join(store, "samples.bin")
-        sb = ["standby", "--role", str(role), "--check", "--samples", samples]
+        # --target: the ledger's global consistent iteration after the failure
+        sb = ["standby", "--role", str(role), "--check", "--samples", samples, "--target", "2"]
         standby = None
         if warm:
             standby = spawn(sb + ["--warm"])
