@@ -317,6 +317,16 @@ int ffx_replica_newest(ffx_replica* r, uint64_t* iteration);
 int ffx_replica_slot_ptrs(ffx_replica* r, uint32_t slot, void** payload, uint64_t** sums);
 /* NeighborBuffer::clear() (ckpt.hpp:117). */
 int ffx_replica_clear(ffx_replica* r);
+/* Rollback to the global consistent iteration (the new epoch after
+ * orchestrate_recovery, controller.cpp:315-318): slots holding an iteration
+ * newer than `iteration` were committed before the failure and are dropped
+ * (marked empty), so a CkptRecord read from this replica
+ * (ffx_ledger_record_replica) cannot re-raise the rebased ledger before the
+ * replay re-commits them -- the reference ignores stale-epoch CkptRecords
+ * (Controller::on_ckpt_record).  *dropped = slots emptied (may be NULL).
+ * Writers into this replica re-arm it afterwards (ffx_snapshot_target re-reads
+ * the slot table), as every rank does when the new epoch starts. */
+int ffx_replica_rollback(ffx_replica* r, uint64_t iteration, uint32_t* dropped);
 /* SNP1 frame export (framed_at(), ckpt.cpp:95-100 + pack_blob layout): copies
  * header + payload (regions concatenated) to host memory; computes the
  * whole-payload FNV on the device if not yet known.  *framed_len = 32 + len.

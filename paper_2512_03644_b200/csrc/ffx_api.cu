@@ -492,6 +492,7 @@ extern "C" int ffx_open(int device, const ffx_cluster_spec* spec, ffx_role self,
   if (e == cudaSuccess) e = cudaEventCreate(&c->ev1);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->copy_done, cudaEventDisableTiming);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->hash_done, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->snap_done, cudaEventDisableTiming);
   if (e != cudaSuccess) {
     ffx_close(c);
     return cuda_fail(e, "open");
@@ -510,6 +511,7 @@ extern "C" int ffx_close(ffx_ctx* c) {
   if (c->ev1) cudaEventDestroy(c->ev1);
   if (c->copy_done) cudaEventDestroy(c->copy_done);
   if (c->hash_done) cudaEventDestroy(c->hash_done);
+  if (c->snap_done) cudaEventDestroy(c->snap_done);
   delete c;
   return FFX_OK;
 }

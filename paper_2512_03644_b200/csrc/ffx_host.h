@@ -196,6 +196,11 @@ struct ffx_ctx {
   unsigned long long* result_host = nullptr;  // pinned mirror
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   cudaEvent_t copy_done = nullptr, hash_done = nullptr;  // split-policy joins
+  // Recorded after each snapshot's last launch; the next snapshot's first
+  // launch of each kind waits on it, so two snapshots of one ctx never run
+  // concurrently (they share the task / commit counter words) even when the
+  // caller issues them on different streams.
+  cudaEvent_t snap_done = nullptr;
   uint64_t seq = 0;
   uint32_t last_slot = 0;
   ffx_replica* last_target = nullptr;

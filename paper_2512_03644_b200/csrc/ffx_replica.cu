@@ -219,6 +219,24 @@ extern "C" int ffx_replica_slot_regions(ffx_replica* r, uint32_t slot, uint32_t*
   return FFX_OK;
 }
 
+extern "C" int ffx_replica_rollback(ffx_replica* r, uint64_t iteration, uint32_t* dropped) {
+  if (!r) return fail(FFX_EINVAL, "replica_rollback: null argument");
+  DeviceGuard g(r->device);
+  uint32_t n = 0;
+  for (uint32_t v = 0; v < r->versions; ++v) {
+    SlotMeta m;
+    int st = read_meta(r, v, &m);
+    if (st) return st;
+    if (m.magic != kSlotMagic || m.state == kSlotEmpty || m.iteration <= iteration) continue;
+    const uint32_t empty = kSlotEmpty;
+    FFX_CUDA(cudaMemcpy(r->slot(v) + offsetof(SlotMeta, state), &empty, 4, cudaMemcpyHostToDevice));
+    if (v < r->cache.size()) r->cache[v] = SlotCache{true, kSlotEmpty, 0, 0};
+    ++n;
+  }
+  if (dropped) *dropped = n;
+  return FFX_OK;
+}
+
 extern "C" int ffx_replica_slots(const ffx_replica* r, uint32_t* versions) {
   if (!r || !versions) return fail(FFX_EINVAL, "replica_slots: null argument");
   *versions = r->versions;

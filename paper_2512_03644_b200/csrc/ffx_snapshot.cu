@@ -549,6 +549,7 @@ int issue_hash_batch(ffx_ctx* c, PendingSnapshot& P, uint32_t b, cudaStream_t s)
 
 int finish_snapshot(ffx_ctx* c, PendingSnapshot& P, cudaStream_t s) {
   P.active = false;
+  FFX_CUDA(cudaEventRecord(c->snap_done, s));
   ffx_replica* t = P.tgt;
   t->cache[P.slot] = SlotCache{true, kSlotCommitted, P.iteration, P.seq};
   if (P.tgt2) P.tgt2->cache[P.slot2] = SlotCache{true, kSlotCommitted, P.iteration, P.seq2};
@@ -575,6 +576,7 @@ extern "C" int ffx_snapshot_next_kind(ffx_ctx* c, int kind, void* stream, void* 
   const uint32_t total = kind == FFX_BATCH_COPY ? P.batches : P.hbatches;
   if (*next >= total) return fail(FFX_ESTATE, "snapshot_next: no %s batches left", kind ? "hash" : "copy");
   if (gate_event) FFX_CUDA(cudaStreamWaitEvent(s, static_cast<cudaEvent_t>(gate_event), 0));
+  if (*next == 0) FFX_CUDA(cudaStreamWaitEvent(s, c->snap_done, 0));  // the previous snapshot has drained
   const uint32_t b = (*next)++;
 
   if (!P.split) {

@@ -259,6 +259,7 @@ SIGNATURES = {
     "ffx_replica_slot_info": (_I, [_P, _U32, ctypes.POINTER(SlotInfo)]),
     "ffx_replica_newest": (_I, [_P, ctypes.POINTER(_U64)]),
     "ffx_replica_slot_ptrs": (_I, [_P, _U32, ctypes.POINTER(_P), ctypes.POINTER(_P)]),
+    "ffx_replica_rollback": (_I, [_P, _U64, ctypes.POINTER(_U32)]),
     "ffx_replica_clear": (_I, [_P]),
     "ffx_replica_export_frame": (_I, [_P, _U64, _P, _U64, ctypes.POINTER(_U64), _P]),
     "ffx_replica_export_frame_part": (_I, [_P, _U64, _U32, _P, _U64, ctypes.POINTER(_U64),
@@ -720,6 +721,13 @@ class Replica:
 
     def clear(self):
         check(lib.ffx_replica_clear(self._h), "replica_clear")
+
+    def rollback(self, iteration: int) -> int:
+        """Drop slots newer than `iteration` (ffx_replica_rollback); returns
+        how many.  Writers re-arm their target afterwards (set_target)."""
+        n = _U32()
+        check(lib.ffx_replica_rollback(self._h, iteration, ctypes.byref(n)), "replica_rollback")
+        return n.value
 
     def export_frame(self, iteration: int, stream=None) -> bytes:
         n = ctypes.c_uint64()

@@ -514,3 +514,57 @@ def test_damaged_handle_is_refused(ffx):
         with pytest.raises(ffx.InvalidArgument):
             origin.open_replica(bytes(bad))
     origin.open_replica(bytes(good)).destroy()
+
+
+def test_rollback_drops_pre_failure_slots_from_the_ledger(ffx):
+    """after ffx_ledger_rebase(N) a holder still has slots newer
+    than N committed before the failure; read back as a CkptRecord they would
+    re-raise the rebased ledger before the replay re-commits them (the
+    reference drops stale-epoch CkptRecords, Controller::on_ckpt_record).
+    ffx_replica_rollback(N) empties them; the replay then refills the slot."""
+    n = 2 * 4096 + 5
+    spec, holder, origin, rep, view = ring_pair(ffx, n)
+    spec.num_nodes, spec.gpus_per_node = 2, 1
+    led = ffx.Ledger(spec)
+    state = torch.zeros(n, dtype=torch.uint8, device="cuda")
+    origin.register(ffx.REGION_BLOB, state)
+    for it in (1, 2, 3):
+        state.fill_(it)
+        origin.snapshot(it)
+    torch.cuda.synchronize()
+    assert sorted(rep.held()) == [2, 3]
+    led.rebase(2)  # the new epoch resumes from global consistent iteration 2
+    assert rep.rollback(2) == 1
+    assert sorted(rep.held()) == [2]
+    assert led.record_replica(rep) == 2 and led.worker_latest((1, 0, 0)) == 2
+    origin.set_target(view)  # the writer re-arms its target in the new epoch
+    state.fill_(33)  # the replayed iteration 3 differs from the lost one
+    origin.snapshot(3)
+    torch.cuda.synchronize()
+    assert sorted(rep.held()) == [2, 3]
+    assert rep.export_frame(3)[32:] == bytes([33]) * n
+    assert rep.export_frame(2)[32:] == bytes([2]) * n
+    assert led.record_replica(rep) == 3
+
+
+def test_snapshots_on_two_streams_do_not_overlap(ffx):
+    """ADVICE r1: two snapshots of one ctx share its task / commit counters;
+    issued back to back on different streams, the second must wait for the
+    first (snap_done event) instead of racing it -- both frames stay exact."""
+    n = 64 * (1 << 20) + 3
+    spec, holder, origin, rep, view = ring_pair(ffx, n)
+    a = torch.empty(n, dtype=torch.uint8, device="cuda")
+    d1 = orc.optimizer_init(5, 1, 0, 0, True)
+    d2 = orc.optimizer_init(6, 1, 0, 0, True)
+    ffx.materialize(a, d1)
+    origin.register(ffx.REGION_BLOB, a)
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    origin.snapshot(1, stream=s1)
+    ev = torch.cuda.Event()
+    ev.record(s1)
+    origin.snapshot(2, stream=s2)  # same bytes, different stream, no caller-side ordering
+    torch.cuda.synchronize()
+    want = orc.materialize(d1, n)
+    assert rep.export_frame(1) == orc.pack_blob((1, 0, 0), 1, 1, want)
+    assert rep.export_frame(2) == orc.pack_blob((1, 0, 0), 2, 1, want)
+    del d2
