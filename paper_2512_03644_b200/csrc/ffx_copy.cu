@@ -70,11 +70,12 @@ __global__ void __launch_bounds__(32) copy_kernel(const __grid_constant__ CopyJo
   if (lane == 0) {  // WRITING before any payload byte
     for (const SlotMark* mk : {&job.mark, &job.mark2}) {
       if (mk->slot == nullptr) continue;
-      volatile SlotMeta* m = reinterpret_cast<volatile SlotMeta*>(mk->slot);
-      m->magic = kSlotMagic;
-      m->iteration = mk->iteration;
-      m->seq = mk->seq;
-      m->state = kSlotWriting;
+      SlotMeta* m = reinterpret_cast<SlotMeta*>(mk->slot);
+      const bool mc = mk->mcast != 0;
+      meta_st32(&m->magic, kSlotMagic, mc);
+      meta_st64(&m->iteration, mk->iteration, mc);
+      meta_st64(&m->seq, mk->seq, mc);
+      meta_st32(&m->state, kSlotWriting, mc);
     }
     __threadfence_system();
   }
@@ -189,24 +190,11 @@ __global__ void __launch_bounds__(256) sm_copy_kernel(const __grid_constant__ Co
 // Single thread: the final slot commit (meta, SNP1 header, then COMMITTED).
 __global__ void commit_kernel(const __grid_constant__ SlotCommit c) {
   __threadfence_system();
-  volatile uint4* m = reinterpret_cast<volatile uint4*>(c.slot);
-  for (int i = 1; i < static_cast<int>(kMetaBytes / 16); ++i) {
-    const uint4 v = c.meta[i];
-    m[i].x = v.x;
-    m[i].y = v.y;
-    m[i].z = v.z;
-    m[i].w = v.w;
-  }
-  volatile uint4* h = reinterpret_cast<volatile uint4*>(c.slot + c.payload_off - 32);
-  for (int i = 0; i < 2; ++i) {
-    const uint4 v = c.snp1[i];
-    h[i].x = v.x;
-    h[i].y = v.y;
-    h[i].z = v.z;
-    h[i].w = v.w;
-  }
+  const bool mc = c.mcast != 0;
+  for (int i = 1; i < static_cast<int>(kMetaBytes / 16); ++i) meta_st128(c.slot + 16 * i, c.meta[i], mc);
+  for (int i = 0; i < 2; ++i) meta_st128(c.slot + c.payload_off - 32 + 16 * i, c.snp1[i], mc);
   __threadfence_system();
-  reinterpret_cast<volatile SlotMeta*>(c.slot)->state = kSlotCommitted;
+  meta_st32(&reinterpret_cast<SlotMeta*>(c.slot)->state, kSlotCommitted, mc);
   __threadfence_system();
   if (c.ack != nullptr) {
     *reinterpret_cast<volatile uint64_t*>(c.ack) = c.ack_value;

@@ -84,6 +84,24 @@ __device__ __forceinline__ uint64_t mix64(uint64_t x) {
   return x ^ (x >> 31);
 }
 
+// Slot-metadata stores (SlotMeta words, SNP1 header, the COMMITTED flag).
+// Through an NVSwitch multicast range (the double-neighbour target) they are
+// multimem.st -- the only plain-store form the PTX ISA defines on a multimem
+// address -- so every bound holder receives them; elsewhere volatile stores.
+// Ordering is by the callers' system-scope fences, as before.
+__device__ __forceinline__ void meta_st32(void* p, uint32_t v, bool mc) {
+  if (mc) asm volatile("multimem.st.relaxed.sys.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+  else *reinterpret_cast<volatile uint32_t*>(p) = v;
+}
+__device__ __forceinline__ void meta_st64(void* p, uint64_t v, bool mc) {
+  if (mc) asm volatile("multimem.st.relaxed.sys.global.b64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+  else *reinterpret_cast<volatile uint64_t*>(p) = v;
+}
+__device__ __forceinline__ void meta_st128(void* p, const uint4& v, bool mc) {
+  meta_st64(p, (static_cast<uint64_t>(v.y) << 32) | v.x, mc);
+  meta_st64(static_cast<uint8_t*>(p) + 8, (static_cast<uint64_t>(v.w) << 32) | v.z, mc);
+}
+
 // Streaming global accesses: every payload byte is touched once per pass.
 __device__ __forceinline__ uint4 ld_stream(const void* p) {
   return __ldcs(reinterpret_cast<const uint4*>(p));

@@ -35,7 +35,7 @@ struct SlotCommit {
   uint8_t* slot;             // slot base (peer-mapped or local); null = no commit
   unsigned int* done;        // local completion counter (zero between launches)
   uint32_t finalize;         // this launch is the last batch of the snapshot
-  uint32_t pad_;
+  uint32_t mcast;            // slot is written through a multicast range (multimem.st metadata)
   uint64_t payload_off;      // SNP1 header lives at slot + payload_off - 32
   uint64_t iteration, seq;
   uint4 meta[kMetaBytes / 16];  // final SlotMeta image (state field = COMMITTED)
@@ -89,6 +89,8 @@ struct CopyRegion {
 struct SlotMark {  // every copy CTA marks the slot WRITING first
   uint8_t* slot;   // null = no mark
   uint64_t iteration, seq;
+  uint32_t mcast;  // through a multicast range (multimem.st)
+  uint32_t pad_;
 };
 
 struct CopyJob {

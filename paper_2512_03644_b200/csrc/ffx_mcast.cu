@@ -410,14 +410,18 @@ extern "C" int ffx_snapshot_target_mcast(ffx_ctx* c, ffx_mcast* m, ffx_replica* 
   if (!m->va) {
     // Every member of a team must back the range: the origin binds one small
     // sink repeatedly (aliased) instead of a replica-sized buffer -- without
-    // any binding here the stores crawl at ~50 GB/s (measured).
-    m->sink_bytes = std::min<uint64_t>(m->bytes, kSinkMax);
-    m->sink_bytes = align_up(m->sink_bytes, m->gran);
-    while (m->bytes % m->sink_bytes) m->sink_bytes -= m->gran;
-    CUmemAllocationProp ap = share_prop(c->device);
-    FFX_DRV(drv().memCreate(&m->sink, m->sink_bytes, &ap, 0));
-    for (uint64_t o = 0; o < m->bytes; o += m->sink_bytes)
-      FFX_DRV(drv().mcBindMem(m->handle, o, m->sink, 0, m->sink_bytes, 0));
+    // any binding here the stores crawl at ~50 GB/s (measured).  When the
+    // origin's own device already backs it with a holder's replica (a holder
+    // on the writer's GPU, e.g. a one-GPU team), that binding is the backing.
+    if (!m->bound) {
+      m->sink_bytes = std::min<uint64_t>(m->bytes, kSinkMax);
+      m->sink_bytes = align_up(m->sink_bytes, m->gran);
+      while (m->bytes % m->sink_bytes) m->sink_bytes -= m->gran;
+      CUmemAllocationProp ap = share_prop(c->device);
+      FFX_DRV(drv().memCreate(&m->sink, m->sink_bytes, &ap, 0));
+      for (uint64_t o = 0; o < m->bytes; o += m->sink_bytes)
+        FFX_DRV(drv().mcBindMem(m->handle, o, m->sink, 0, m->sink_bytes, 0));
+    }
     int st = map_range(m->handle, m->bytes, m->gran, c->device, &m->va);
     if (st) return st;
   }

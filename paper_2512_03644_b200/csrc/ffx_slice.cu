@@ -176,11 +176,12 @@ __device__ __forceinline__ void fence_async_global() {
 
 __device__ __forceinline__ void commit_begin(const SlotCommit& c) {
   if (threadIdx.x == 0) {
-    volatile SlotMeta* m = reinterpret_cast<volatile SlotMeta*>(c.slot);
-    m->magic = kSlotMagic;
-    m->iteration = c.iteration;
-    m->seq = c.seq;
-    m->state = kSlotWriting;
+    SlotMeta* m = reinterpret_cast<SlotMeta*>(c.slot);
+    const bool mc = c.mcast != 0;
+    meta_st32(&m->magic, kSlotMagic, mc);
+    meta_st64(&m->iteration, c.iteration, mc);
+    meta_st64(&m->seq, c.seq, mc);
+    meta_st32(&m->state, kSlotWriting, mc);
     __threadfence_system();
   }
   __syncthreads();
@@ -193,24 +194,11 @@ __device__ __forceinline__ void commit_end(const SlotCommit& c) {
   const unsigned prev = atomicAdd(c.done, 1u);
   if (prev != gridDim.x - 1) return;
   __threadfence_system();
-  volatile uint4* m = reinterpret_cast<volatile uint4*>(c.slot);
-  for (int i = 1; i < static_cast<int>(kMetaBytes / 16); ++i) {
-    const uint4 v = c.meta[i];
-    m[i].x = v.x;
-    m[i].y = v.y;
-    m[i].z = v.z;
-    m[i].w = v.w;
-  }
-  volatile uint4* h = reinterpret_cast<volatile uint4*>(c.slot + c.payload_off - 32);
-  for (int i = 0; i < 2; ++i) {
-    const uint4 v = c.snp1[i];
-    h[i].x = v.x;
-    h[i].y = v.y;
-    h[i].z = v.z;
-    h[i].w = v.w;
-  }
+  const bool mc = c.mcast != 0;
+  for (int i = 1; i < static_cast<int>(kMetaBytes / 16); ++i) meta_st128(c.slot + 16 * i, c.meta[i], mc);
+  for (int i = 0; i < 2; ++i) meta_st128(c.slot + c.payload_off - 32 + 16 * i, c.snp1[i], mc);
   __threadfence_system();
-  reinterpret_cast<volatile SlotMeta*>(c.slot)->state = kSlotCommitted;
+  meta_st32(&reinterpret_cast<SlotMeta*>(c.slot)->state, kSlotCommitted, mc);
   __threadfence_system();
   if (c.ack != nullptr) {  // pull mode: release the origin's optimizer update
     *reinterpret_cast<volatile uint64_t*>(c.ack) = c.ack_value;

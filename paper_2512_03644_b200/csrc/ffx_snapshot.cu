@@ -149,6 +149,7 @@ int begin_impl(ffx_ctx* c, ffx_replica* t, ffx_replica* t2, const std::vector<Sr
   std::memcpy(cm.snp1, hdr, 32);
   cm.ack = ack;
   cm.ack_value = iteration;
+  cm.mcast = t->wbase != nullptr ? 1u : 0u;
   if (t2) {
     // Double-neighbour replication: the same tiles stored twice, one table
     // per replica, each slot committed by its own counter.
@@ -160,6 +161,7 @@ int begin_impl(ffx_ctx* c, ffx_replica* t, ffx_replica* t2, const std::vector<Sr
     reinterpret_cast<SlotMeta*>(job.commit2.meta)->seq = seq2;
     job.commit2.done = c->done + 4;
     job.commit2.payload_off = t2->layout.payload_off;
+    job.commit2.mcast = t2->wbase != nullptr ? 1u : 0u;
     P.slot2 = slot2;
   }
 
@@ -201,8 +203,8 @@ int begin_impl(ffx_ctx* c, ffx_replica* t, ffx_replica* t2, const std::vector<Sr
     for (uint32_t i = 0; i < job.nregions; ++i)
       cj.reg[i] = CopyRegion{job.reg[i].src, job.reg[i].dst, job.reg[i].bytes, 0, 0, job.reg[i].dst2};
     finalize_copy_job(cj);
-    cj.mark = SlotMark{t->wslot(slot), iteration, seq};
-    if (t2) cj.mark2 = SlotMark{t2->wslot(slot2), iteration, seq2};
+    cj.mark = SlotMark{t->wslot(slot), iteration, seq, t->wbase != nullptr ? 1u : 0u, 0};
+    if (t2) cj.mark2 = SlotMark{t2->wslot(slot2), iteration, seq2, t2->wbase != nullptr ? 1u : 0u, 0};
     if (opts.fused_permille) {
       if (!P.copy_engine) {
         P.active = false;

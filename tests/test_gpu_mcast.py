@@ -138,3 +138,60 @@ def test_multicast_layout_mismatch_is_refused(ffx):
         held.destroy()
         origin.close()
         holder.close()
+
+
+@pytest.fixture(scope="module")
+def ffx1():
+    """Any GPU with multicast support: the one-device team below."""
+    from paper_2512_03644_b200 import ffx as m
+    if not m.mcast_supported(0):
+        pytest.skip("no multicast support on device 0")
+    return m
+
+
+def test_one_gpu_team_multicast_target_commits_and_restores(ffx1):
+    """The multicast write path on a single GPU (runs on the driver's 1-GPU
+    box): a one-member team whose range the holder's shareable replica backs
+    on the writer's own device.  The fused kernel's tiles, the slot metadata
+    (multimem.st) and the COMMITTED flag all go through the multicast VA; the
+    slot must then read back (unicast) as the reference frame and restore
+    bit-exactly, verify-on-store included; a flipped byte is still caught."""
+    ffx = ffx1
+    spec = ffx.make_spec(d=2, phi=(1 << 20), distributed=True)
+    origin = ffx.Context(0, spec, (1, 0, 0))
+    holder = ffx.Context(0, spec, (0, 0, 0))
+    n = 3 * (1 << 20) + 12345
+    held = holder.create_shared_replica((1, 0, 0), n, 2)
+    mc = origin.create_mcast(n, 2, members=1)
+    view = None
+    try:
+        mc.join()
+        mc.bind(held)  # the holder's memory backs the range on this device
+        view = origin.open_replica(held.export())
+        origin.set_target_mcast(mc, view)
+        d0 = orc.optimizer_init(42, 1, 0, 0, True)
+        state = torch.empty(n, dtype=torch.uint8, device="cuda:0")
+        ffx.materialize(state, d0)
+        origin.register(ffx.REGION_BLOB, state)
+        origin.snapshot(5)
+        d1 = orc.optimizer_init(43, 1, 0, 0, True)
+        ffx.materialize(state, d1)
+        origin.snapshot(6, verify_on_store=True)
+        torch.cuda.synchronize()
+        assert sorted(held.held()) == [5, 6]
+        assert held.export_frame(5) == orc.pack_blob((1, 0, 0), 5, 1, orc.materialize(d0, n))
+        assert held.export_frame(6) == orc.pack_blob((1, 0, 0), 6, 1, orc.materialize(d1, n))
+        state.fill_(0)
+        assert origin.recover(view, 5).bad_slices == 0
+        assert host(state) == orc.materialize(d0, n)
+        origin.inject(ffx.FAULT_CORRUPT_REPLICA, view, (held.held()[6] << 48) | 4097)
+        with pytest.raises(ffx.RestoreError, match="checksum mismatch"):
+            origin.recover(view, 6)
+    finally:
+        torch.cuda.synchronize()
+        if view is not None:
+            view.destroy()
+        mc.destroy()
+        held.destroy()
+        origin.close()
+        holder.close()

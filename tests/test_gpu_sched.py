@@ -113,3 +113,78 @@ def test_sched_zero_weight_gaps_and_idle_calls(ffx):
         rep.destroy()
         origin.close()
         holder.close()
+
+
+def _train_ms(train, a, b, reps=3):
+    """Device time of a full-GPU TRAIN kernel (bf16 GEMM) on the train stream."""
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(train):
+        e0.record(train)
+        for _ in range(reps):
+            torch.matmul(a, b)
+        e1.record(train)
+    return e0, e1
+
+
+@pytest.mark.parametrize("cap", [32, 0])
+def test_train_waits_at_most_one_state_batch(ffx, cap):
+    """TRAIN > STATE with bounded inversion (sim_net.cpp:401-454; the pin is
+    test_transport.cpp:173-197: a TRAIN chunk queued while a STATE chunk is
+    on the wire starts at the next chunk boundary).  Here a STATE batch (one
+    fused snapshot batch, CTA-capped, low-priority stream) is resident when a
+    full-GPU TRAIN GEMM arrives on the high-priority stream: the GEMM's extra
+    time is at most one batch's duration."""
+    spec = ffx.make_spec(d=2, phi=64, distributed=True)
+    holder = ffx.Context(0, spec, (0, 0, 0))
+    origin = ffx.Context(0, spec, (1, 0, 0))
+    n = 1 << 30
+    rep = holder.create_replica((1, 0, 0), n, 2)
+    view = origin.open_replica(rep.export())
+    origin.set_target(view)
+    state = torch.empty(n, dtype=torch.uint8, device="cuda")
+    ffx.materialize(state, orc.optimizer_init(3, 1, 0, 0, True))
+    origin.register(ffx.REGION_BLOB, state)
+    train = torch.cuda.Stream(priority=-1)
+    low = torch.cuda.Stream(priority=0)
+    a = torch.randn(8192, 8192, dtype=torch.bfloat16, device="cuda")
+    b = torch.randn(8192, 8192, dtype=torch.bfloat16, device="cuda")
+    try:
+        batches = 4
+        # one STATE batch alone
+        it = 1
+        origin.snapshot_begin(it, batches=batches, max_ctas=cap)
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record(low)
+        origin.snapshot_next(stream=low)
+        f1.record(low)
+        while origin.snapshot_next(stream=low):
+            pass
+        torch.cuda.synchronize()
+        batch_ms = f0.elapsed_time(f1)
+        # TRAIN alone
+        for _ in range(2):
+            e0, e1 = _train_ms(train, a, b)
+        torch.cuda.synchronize()
+        alone = e0.elapsed_time(e1)
+        # TRAIN arriving while a STATE batch is resident
+        worst = 0.0
+        for it in (2, 3, 4):
+            origin.snapshot_begin(it, batches=batches, max_ctas=cap)
+            origin.snapshot_next(stream=low)
+            with torch.cuda.stream(low):
+                torch.cuda._sleep(1000)  # keep the low stream busy behind the batch
+            e0, e1 = _train_ms(train, a, b)
+            while origin.snapshot_next(stream=low):
+                pass
+            torch.cuda.synchronize()
+            worst = max(worst, e0.elapsed_time(e1) - alone)
+        assert rep.newest() == 4
+        print("inversion cap=%d: batch %.3f ms, train alone %.3f ms, worst extra %.3f ms"
+              % (cap, batch_ms, alone, worst))
+        assert worst <= batch_ms * 1.1 + 0.05, (worst, batch_ms, alone)
+    finally:
+        torch.cuda.synchronize()
+        view.destroy()
+        rep.destroy()
+        origin.close()
+        holder.close()
