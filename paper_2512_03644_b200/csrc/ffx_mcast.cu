@@ -292,7 +292,7 @@ static_assert(sizeof(McastBlob) <= FFX_MCAST_HANDLE_BYTES, "mcast handle too lar
 extern "C" int ffx_mcast_create(ffx_ctx* c, uint64_t capacity, uint32_t versions, uint32_t members,
                                 ffx_mcast** out) {
   if (!c || !out) return fail(FFX_EINVAL, "mcast_create: null argument");
-  if (members < 2 || members > 8) return fail(FFX_EINVAL, "mcast_create: 2..8 members");
+  if (members < 1 || members > 8) return fail(FFX_EINVAL, "mcast_create: 1..8 members");
   if (versions < 1 || versions > 8) return fail(FFX_EINVAL, "mcast_create: 1..8 versions");
   DeviceGuard g(c->device);
   uint64_t gran = 0;

@@ -115,7 +115,7 @@ def test_sched_zero_weight_gaps_and_idle_calls(ffx):
         holder.close()
 
 
-def _train_ms(train, a, b, reps=3):
+def _train_ms(train, a, b, reps=1):
     """Device time of a full-GPU TRAIN kernel (bf16 GEMM) on the train stream."""
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with torch.cuda.stream(train):
@@ -131,9 +131,10 @@ def test_train_waits_at_most_one_state_batch(ffx, cap):
     """TRAIN > STATE with bounded inversion (sim_net.cpp:401-454; the pin is
     test_transport.cpp:173-197: a TRAIN chunk queued while a STATE chunk is
     on the wire starts at the next chunk boundary).  Here a STATE batch (one
-    fused snapshot batch, CTA-capped, low-priority stream) is resident when a
-    full-GPU TRAIN GEMM arrives on the high-priority stream: the GEMM's extra
-    time is at most one batch's duration."""
+    fused snapshot batch, low-priority stream, optionally CTA-capped) is
+    resident when one full-GPU TRAIN GEMM arrives on the high-priority
+    stream: the GEMM's extra time is at most one batch's duration (the batch
+    is never cut; nothing of STATE starts ahead of the queued TRAIN kernel)."""
     spec = ffx.make_spec(d=2, phi=64, distributed=True)
     holder = ffx.Context(0, spec, (0, 0, 0))
     origin = ffx.Context(0, spec, (1, 0, 0))
@@ -146,13 +147,12 @@ def test_train_waits_at_most_one_state_batch(ffx, cap):
     origin.register(ffx.REGION_BLOB, state)
     train = torch.cuda.Stream(priority=-1)
     low = torch.cuda.Stream(priority=0)
-    a = torch.randn(8192, 8192, dtype=torch.bfloat16, device="cuda")
+    a = torch.randn(16384, 8192, dtype=torch.bfloat16, device="cuda")
     b = torch.randn(8192, 8192, dtype=torch.bfloat16, device="cuda")
     try:
         batches = 4
         # one STATE batch alone
-        it = 1
-        origin.snapshot_begin(it, batches=batches, max_ctas=cap)
+        origin.snapshot_begin(1, batches=batches, max_ctas=cap)
         f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         f0.record(low)
         origin.snapshot_next(stream=low)
@@ -162,22 +162,22 @@ def test_train_waits_at_most_one_state_batch(ffx, cap):
         torch.cuda.synchronize()
         batch_ms = f0.elapsed_time(f1)
         # TRAIN alone
-        for _ in range(2):
+        for _ in range(3):
             e0, e1 = _train_ms(train, a, b)
-        torch.cuda.synchronize()
+            torch.cuda.synchronize()
         alone = e0.elapsed_time(e1)
-        # TRAIN arriving while a STATE batch is resident
+        # TRAIN arriving while the first STATE batch is resident; the other
+        # batches are issued only after TRAIN finished
         worst = 0.0
         for it in (2, 3, 4):
             origin.snapshot_begin(it, batches=batches, max_ctas=cap)
             origin.snapshot_next(stream=low)
-            with torch.cuda.stream(low):
-                torch.cuda._sleep(1000)  # keep the low stream busy behind the batch
             e0, e1 = _train_ms(train, a, b)
+            train.synchronize()
+            worst = max(worst, e0.elapsed_time(e1) - alone)
             while origin.snapshot_next(stream=low):
                 pass
             torch.cuda.synchronize()
-            worst = max(worst, e0.elapsed_time(e1) - alone)
         assert rep.newest() == 4
         print("inversion cap=%d: batch %.3f ms, train alone %.3f ms, worst extra %.3f ms"
               % (cap, batch_ms, alone, worst))
