@@ -676,6 +676,11 @@ def e2e_leg(args, ffx, torch, R, world, rank, local, n, stream, barrier, max_ove
     return out
 
 
+def torch_count():
+    import torch
+    return torch.cuda.device_count()
+
+
 def standby_leg(args, world, local):
     """Time to restore a REPLACED rank (north star: < 1 s for a Llama-3 8B
     ZeRO-3 shard): holder, origin and replacement are separate processes of
@@ -704,9 +709,12 @@ def standby_leg(args, world, local):
             common = ["--d", str(d), "--phi", str(PHI_LLAMA3_8B), "--store", store]
             procs = []
 
-            def spawn(a, dev):
+            def spawn(a, dev, visible=None):
+                env = dict(os.environ)
+                if visible is not None:  # a replacement sees only the GPUs it needs
+                    env["CUDA_VISIBLE_DEVICES"] = ",".join(str(x) for x in visible)
                 p = subprocess.Popen([exe] + a + common + ["--device", str(dev)], stdin=subprocess.PIPE,
-                                     stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True)
+                                     stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True, env=env)
                 procs.append(p)
                 return p
 
@@ -726,9 +734,14 @@ def standby_leg(args, world, local):
                            "--regions2", ",".join(r.spec() for r in regs2)], local)
                 line(o, "SNAPSHOTTED")
                 sb = ["standby", "--role", str(role), "--check", "--target", "2"]
+                # a replacement sees only its own GPU and the holder's (CUDA
+                # context creation scales with the visible GPUs): device 0 is its own
+                parent = os.environ.get("CUDA_VISIBLE_DEVICES")
+                phys = parent.split(",") if parent else [str(i) for i in range(torch_count())]
+                vis = [phys[local]] + ([phys[hdev]] if hdev != local else [])
                 s = None
-                if warm:
-                    s = spawn(sb + ["--warm"], local)
+                if warm:  # a provisioned spare: context, peers and the state arena up before the failure
+                    s = spawn(sb + ["--warm", "--prealloc", str(nbytes + 8 * 256)], 0, vis)
                     line(s, "ARMED")
                 os.kill(o.pid, signal.SIGKILL)
                 o.wait()
@@ -737,7 +750,7 @@ def standby_leg(args, world, local):
                     s.stdin.write("FAIL %d\n" % t0)
                     s.stdin.flush()
                 else:
-                    s = spawn(sb + ["--t0", str(t0)], local)
+                    s = spawn(sb + ["--t0", str(t0)], 0, vis)
                 so, se = s.communicate(timeout=600)
                 if s.returncode != 0:
                     return {"error": se[-300:]}

@@ -231,6 +231,10 @@ int ffx_blob_check(const void* dev, uint64_t bytes, uint64_t* host_first_bad, vo
  * C++ facade over the reference API) ---------------------------------------- */
 
 int ffx_device_alloc(int device, uint64_t bytes, void** dev);
+/* Enable peer access from `device` to every peer it can reach over NVLink
+ * (a warm spare does this before any failure, so mapping a holder's replica
+ * later skips the lazy enable).  *enabled = peers now accessible. */
+int ffx_prepare_peers(int device, uint32_t* enabled);
 int ffx_device_free(int device, void* dev);
 /* cudaMemcpyAsync(kind = default) on `stream`; blocks when sync != 0. */
 int ffx_memcpy(void* dst, const void* src, uint64_t bytes, void* stream, int sync);

@@ -432,6 +432,26 @@ extern "C" int ffx_device_alloc(int device, uint64_t bytes, void** dev) {
   return FFX_OK;
 }
 
+extern "C" int ffx_prepare_peers(int device, uint32_t* enabled) {
+  DeviceGuard g(device);
+  int n = 0;
+  FFX_CUDA(cudaGetDeviceCount(&n));
+  uint32_t k = 0;
+  for (int p = 0; p < n; ++p) {
+    if (p == device) continue;
+    int can = 0;
+    if (cudaDeviceCanAccessPeer(&can, device, p) != cudaSuccess || !can) {
+      cudaGetLastError();
+      continue;
+    }
+    const cudaError_t e = cudaDeviceEnablePeerAccess(p, 0);
+    if (e == cudaSuccess || e == cudaErrorPeerAccessAlreadyEnabled) ++k;
+    cudaGetLastError();
+  }
+  if (enabled) *enabled = k;
+  return FFX_OK;
+}
+
 extern "C" int ffx_device_free(int device, void* dev) {
   if (!dev) return FFX_OK;
   DeviceGuard g(device);

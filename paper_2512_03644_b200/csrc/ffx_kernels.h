@@ -52,7 +52,7 @@ struct SliceJob {
   CUtensorMap maps[3 * kTmaRegions];
   SliceRegion reg[kMaxRegions];
   uint32_t nregions;
-  uint32_t pad_;
+  uint32_t rows;                  // slices per warp task (32 or 64; set by finalize_job)
   uint64_t total_groups;
   uint64_t group_lo, group_hi;  // warp tasks this launch covers (a scheduler batch)
   uint64_t slice_bytes;
@@ -109,12 +109,17 @@ cudaError_t launch_copy(const CopyJob& job, uint32_t ctas, cudaStream_t stream);
 // One-thread kernel writing the final meta + SNP1 header, then COMMITTED.
 cudaError_t launch_commit(const SlotCommit& c, cudaStream_t stream);
 
-// Slices per warp task of the active kernel variant (32 x slices per lane).
-int task_rows();
+// Slices per warp task.  Two kernel configurations ship (ffx_slice.cu):
+// kBulkRows (32 slices, one chain per lane: the full-GPU, HBM/NVLink-bound
+// launches) and kCappedRows (64 slices, two chains per lane, 8 warps per
+// CTA: CTA-capped scheduler batches, where SM time per byte is the cost).
+constexpr uint32_t kBulkRows = 32, kCappedRows = 64;
+// Default rows for a launch with at most max_ctas CTAs (0 = whole GPU).
+uint32_t rows_for_cap(uint32_t max_ctas);
 
 // Fill job.reg[*].group_base / slice_base, job.total_groups and the group
-// range [0, total_groups).
-void finalize_job(SliceJob& job);
+// range [0, total_groups) for `rows` slices per task (0 = kBulkRows).
+void finalize_job(SliceJob& job, uint32_t rows = 0);
 // Launch with at most max_ctas CTAs (0 = occupancy-sized full grid).
 cudaError_t launch_slices(const SliceJob& job, SliceMode mode, bool commit, uint32_t max_ctas,
                           cudaStream_t stream);

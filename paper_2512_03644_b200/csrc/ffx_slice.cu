@@ -558,11 +558,15 @@ int variant() {
 }
 #else
 // Product: [0] copy modes -- 3 stages, 4 warps, 1 slice per lane, 2 chunks
-// (256 B of each slice) per TMA op, the best of the round-1 sweep
-// (profiles/r1_variant_sweep_1gpu.jsonl); [1] checksum-only modes -- the
-// same boxes with 2 stages (no store to wait for: 3.63 vs 3.29 TB/s
-// hash-only, profiles/r1_hash_variant_sweep.txt).
-constexpr Variant kVariants[] = {{3, 4, 1, 0, 2}, {2, 4, 1, 0, 2}};
+// (256 B of each slice) per TMA op, the best full-GPU configuration of the
+// round-1 sweep (profiles/r1_variant_sweep_1gpu.jsonl); [1] checksum-only
+// modes -- the same boxes with 2 stages (no store to wait for: 3.63 vs 3.29
+// TB/s hash-only, profiles/r1_hash_variant_sweep.txt); [2] CTA-capped
+// batches (the slice scheduler inside a training step) -- 8 warps, 2 chains
+// per lane, 2 stages of 128 B x 64 slices: 25.9 GB/s per CTA vs 14.0 for [0]
+// at 8-64 CTAs (profiles/r2_cap_sweep_1gpu.jsonl), i.e. 1.85x less SM time
+// per snapshotted byte where the SMs are borrowed from the step.
+constexpr Variant kVariants[] = {{3, 4, 1, 0, 2}, {2, 4, 1, 0, 2}, {2, 8, 2, 0, 1}};
 constexpr int kHashDefault = 1;
 int variant() { return 0; }
 #endif
@@ -593,6 +597,7 @@ cudaError_t launch_mode(const SliceJob& job, uint32_t max_ctas, cudaStream_t str
     default: return launch_t<3, 4, 1, false, M, kCommit, 2>(job, max_ctas, stream);
   }
 #else
+  if (job.rows == kCappedRows) return launch_t<2, 8, 2, false, M, kCommit, 1>(job, max_ctas, stream);
   if constexpr (hash_only) return launch_t<2, 4, 1, false, M, kCommit, 2>(job, max_ctas, stream);
   else return launch_t<3, 4, 1, false, M, kCommit, 2>(job, max_ctas, stream);
 #endif
@@ -617,7 +622,15 @@ const Variant& active_variant() {
 }
 }  // namespace
 
-int task_rows() { return 32 * active_variant().RPL; }
+uint32_t rows_for_cap(uint32_t max_ctas) {
+#ifdef FFX_DEV
+  (void)max_ctas;
+  return 32u * static_cast<uint32_t>(active_variant().RPL);  // the variant under test decides
+#else
+  // capped launches (fewer CTAs than SMs) are SM-time bound: 2 chains per lane
+  return (max_ctas > 0 && max_ctas < static_cast<uint32_t>(sm_count())) ? kCappedRows : kBulkRows;
+#endif
+}
 
 namespace {
 int hash_variant() {
@@ -626,7 +639,7 @@ int hash_variant() {
     const char* e = std::getenv("FFX_HASH_VARIANT");
     const int h = e ? std::atoi(e) : (variant() == 0 ? kHashDefault : variant());
     const int n = static_cast<int>(sizeof kVariants / sizeof kVariants[0]);
-    // same warp-task size as the fused kernel's jobs (finalize_job), else the fused variant
+    // same warp-task size as the jobs (rows_for_cap), else the fused variant
     return (h >= 0 && h < n && kVariants[h].RPL == active_variant().RPL) ? h : variant();
   }();
   return v;
@@ -636,8 +649,9 @@ int hash_variant() {
 }
 }  // namespace
 
-void finalize_job(SliceJob& job) {
-  const uint64_t rows = static_cast<uint64_t>(task_rows());
+void finalize_job(SliceJob& job, uint32_t rows_in) {
+  job.rows = rows_in ? rows_in : rows_for_cap(0);
+  const uint64_t rows = job.rows;
   uint64_t groups = 0, slices = 0;
   for (uint32_t r = 0; r < job.nregions; ++r) {
     const uint64_t ns = (job.reg[r].bytes + job.slice_bytes - 1) / job.slice_bytes;
@@ -703,7 +717,7 @@ void attach_tensor_maps(SliceJob& job, bool copy, int kc_planes) {
     R.nfull = R.bytes / job.slice_bytes;
     const bool al = (reinterpret_cast<uintptr_t>(R.src) % 16 == 0) &&
                     (!copy || reinterpret_cast<uintptr_t>(R.dst) % 16 == 0);
-    const uint32_t rows = static_cast<uint32_t>(task_rows());
+    const uint32_t rows = job.rows;
     if (!al || R.nfull < rows || R.nfull > (1ull << 31)) continue;
     if (R.dst2 != nullptr && reinterpret_cast<uintptr_t>(R.dst2) % 16 != 0) continue;
     const uint32_t kc = static_cast<uint32_t>(kc_planes);
@@ -722,9 +736,15 @@ cudaError_t launch_slices(const SliceJob& job_in, SliceMode mode, bool commit, u
   SliceJob job = job_in;
   const bool hash_only = mode == SliceMode::Hash || mode == SliceMode::HashVerify;
   // the tensor maps' box depth follows the configuration this launch uses
+#ifdef FFX_DEV
   const int vi = hash_only ? hash_variant() : variant();
   const int nv = static_cast<int>(sizeof kVariants / sizeof kVariants[0]);
-  attach_tensor_maps(job, !hash_only, kVariants[(vi >= 0 && vi < nv) ? vi : 0].KC);
+  const Variant& V = kVariants[(vi >= 0 && vi < nv) ? vi : 0];
+  if (job.rows != 32u * static_cast<uint32_t>(V.RPL)) return cudaErrorInvalidValue;  // job cut for another variant
+#else
+  const Variant& V = job.rows == kCappedRows ? kVariants[2] : kVariants[hash_only ? 1 : 0];
+#endif
+  attach_tensor_maps(job, !hash_only, V.KC);
   // The refill of a stage is a generic-read -> async-write (WAR) sequence,
   // ordered by the warp barrier; the proxy fence is only required for
   // generic writes read by the async proxy (kept per task).  The per-step

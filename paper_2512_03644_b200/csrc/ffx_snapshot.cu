@@ -117,7 +117,9 @@ int begin_impl(ffx_ctx* c, ffx_replica* t, ffx_replica* t2, const std::vector<Sr
   job.slice_bytes = c->slice_bytes;
   job.sums_out = t->wsums(slot);
   job.sched = c->done + 8;  // dynamic task counter (words 8-9 of the ctx scratch)
-  finalize_job(job);
+  // CTA-capped snapshots (scheduler batches inside a step) use the SM-lean
+  // configuration (two chains per lane); split hash batches follow hash_ctas
+  finalize_job(job, rows_for_cap(opts.split ? opts.hash_ctas : opts.max_ctas));
 
   SlotMeta m{};
   m.magic = kSlotMagic;
@@ -214,7 +216,7 @@ int begin_impl(ffx_ctx* c, ffx_replica* t, ffx_replica* t2, const std::vector<Sr
       // range starts where its fused slices end.
       const uint64_t G = job.total_groups;
       P.gcut = G * std::min<uint32_t>(opts.fused_permille, 1000) / 1000;
-      const uint64_t rows = static_cast<uint64_t>(task_rows());
+      const uint64_t rows = job.rows;
       for (uint32_t i = 0; i < job.nregions; ++i) {
         const SliceRegion& R = job.reg[i];
         const uint64_t ns = slices_of(R.bytes, job.slice_bytes);

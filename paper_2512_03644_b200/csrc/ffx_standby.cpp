@@ -17,9 +17,11 @@
 //       iteration 1 (and 2 from --regions2) into holder H's replica, prints
 //       "SNAPSHOTTED <it>", waits (the harness SIGKILLs it).
 //   ffx_standby standby --device D --d N --phi P --role DP --store DIR
-//                       (--warm | --t0 NS) [--target IT] [--samples FILE] [--check]
-//       --warm: open a CUDA context + ffx ctx first, print "ARMED", then read
-//       "FAIL <t0 ns>" on stdin.  --t0: a cold start after the failure.
+//                       (--warm [--prealloc B] | --t0 NS) [--target IT] [--samples FILE] [--check]
+//       --warm: a provisioned spare -- CUDA context + ffx ctx, peer access to
+//       every NVLink peer, and (--prealloc) the job's state arena allocated
+//       before the failure; prints "ARMED", then reads "FAIL <t0 ns>" on
+//       stdin.  --t0: a cold start after the failure.
 //       Then: plan_recovery -> open the planned holder's replica handle ->
 //       allocate + register the regions the committed slot records ->
 //       ffx_recover (gather + per-slice FNV verify) -> one JSON line with the
@@ -65,7 +67,7 @@ struct Args {
   std::string mode, store, regions, regions2, samples;
   int device = 0, origin = -1, role = -1, holder = -1;
   uint32_t d = 2, versions = 2;
-  uint64_t phi = 0, capacity = 0, t0 = 0, slice = 4096, target = 0;
+  uint64_t phi = 0, capacity = 0, t0 = 0, slice = 4096, target = 0, prealloc = 0;
   bool warm = false, check = false;
 };
 
@@ -98,6 +100,7 @@ Args parse(int argc, char** argv) {
     else if (k == "--regions") a.regions = val();
     else if (k == "--regions2") a.regions2 = val();
     else if (k == "--samples") a.samples = val();
+    else if (k == "--prealloc") a.prealloc = std::strtoull(val().c_str(), nullptr, 10);
     else if (k == "--target") a.target = std::strtoull(val().c_str(), nullptr, 10);
     else if (k == "--t0") a.t0 = std::strtoull(val().c_str(), nullptr, 10);
     else if (k == "--warm") a.warm = true;
@@ -288,11 +291,14 @@ int run_standby(const Args& a) {
   const ffx_cluster_spec spec = spec_of(a);
   const ffx_role me = dp_role(a.role);
   ffx_ctx* ctx = nullptr;
+  void* arena = nullptr;  // --prealloc: regions are carved from it
   uint64_t t0 = a.t0, t_ctx_start = 0, t_ctx = 0;
   if (a.warm) {
     // a spare that starts before the failure: CUDA context + ffx ctx ready
     t_ctx_start = now_ns();
     ck(ffx_open(a.device, &spec, me, a.slice, &ctx), "open");
+    ck(ffx_prepare_peers(a.device, nullptr), "prepare_peers");
+    if (a.prealloc) ck(ffx_device_alloc(a.device, a.prealloc, &arena), "prealloc");
     t_ctx = now_ns();
     std::printf("ARMED\n");
     std::fflush(stdout);
@@ -364,9 +370,15 @@ int run_standby(const Args& a) {
   uint64_t sizes[FFX_MAX_REGIONS];
   ck(ffx_replica_slot_regions(src, slot, &n, kinds, sizes), "slot_regions");
   std::vector<void*> dev(n, nullptr);
-  uint64_t total = 0;
+  uint64_t total = 0, carved = 0;
   for (uint32_t i = 0; i < n; ++i) {
-    ck(ffx_device_alloc(a.device, sizes[i], &dev[i]), "device_alloc");
+    const uint64_t need = (sizes[i] + 255) / 256 * 256;
+    if (arena && carved + need <= a.prealloc) {
+      dev[i] = static_cast<uint8_t*>(arena) + carved;
+      carved += need;
+    } else {
+      ck(ffx_device_alloc(a.device, sizes[i], &dev[i]), "device_alloc");
+    }
     ck(ffx_register_region(ctx, kinds[i], dev[i], sizes[i], 1), "register_region");
     total += sizes[i];
   }
@@ -416,7 +428,9 @@ int run_standby(const Args& a) {
       rpt.seconds * 1e3, a.warm ? ms(t_ctx_start, t_ctx) : 0.0, (unsigned long long)rpt.bad_slices,
       rpt.bad_slices == 0 ? "true" : "false", sound, rpt.seconds > 0 ? total / rpt.seconds / 1e9 : 0.0);
   std::fflush(stdout);
-  for (void* p : dev) ffx_device_free(a.device, p);
+  for (void* p : dev)
+    if (!arena || p < arena || p >= static_cast<uint8_t*>(arena) + a.prealloc) ffx_device_free(a.device, p);
+  if (arena) ffx_device_free(a.device, arena);
   ffx_replica_destroy(src);
   ffx_close(ctx);
   return 0;

@@ -240,6 +240,7 @@ SIGNATURES = {
     "ffx_expand": (_I, [_P, _P, _U64, _P]),
     "ffx_materialize": (_I, [_P, _P, _U64, _P]),
     "ffx_blob_check": (_I, [_P, _U64, ctypes.POINTER(_U64), _P]),
+    "ffx_prepare_peers": (_I, [_I, ctypes.POINTER(_U32)]),
     "ffx_device_alloc": (_I, [_I, _U64, ctypes.POINTER(_P)]),
     "ffx_device_free": (_I, [_I, _P]),
     "ffx_memcpy": (_I, [_P, _P, _U64, _P, _I]),
