@@ -68,7 +68,7 @@ struct Args {
   int device = 0, origin = -1, role = -1, holder = -1;
   uint32_t d = 2, versions = 2;
   uint64_t phi = 0, capacity = 0, t0 = 0, slice = 4096, target = 0, prealloc = 0;
-  bool warm = false, check = false;
+  bool warm = false, check = false, shared = false;
 };
 
 Args parse(int argc, char** argv) {
@@ -105,6 +105,7 @@ Args parse(int argc, char** argv) {
     else if (k == "--t0") a.t0 = std::strtoull(val().c_str(), nullptr, 10);
     else if (k == "--warm") a.warm = true;
     else if (k == "--check") a.check = true;
+    else if (k == "--shared") a.shared = true;
     else {
       std::fprintf(stderr, "ffx_standby: unknown option %s\n", k.c_str());
       std::exit(2);
@@ -235,7 +236,10 @@ int run_holder(const Args& a) {
   ck(ffx_dp_neighbor(&spec, dp_role(a.origin), &self), "dp_neighbor");
   ck(ffx_open(a.device, &spec, self, a.slice, &ctx), "open");
   ffx_replica* rep = nullptr;
-  ck(ffx_replica_create(ctx, dp_role(a.origin), a.capacity, a.versions, &rep), "replica_create");
+  // --shared: a VMM (cuMemCreate) allocation exported by fd, mapped with 2 MiB
+  // pages in the importer; default: cudaMalloc + CUDA IPC
+  if (a.shared) ck(ffx_replica_create_shared(ctx, dp_role(a.origin), a.capacity, a.versions, &rep), "create_shared");
+  else ck(ffx_replica_create(ctx, dp_role(a.origin), a.capacity, a.versions, &rep), "replica_create");
   uint8_t h[FFX_HANDLE_BYTES];
   ck(ffx_replica_export(rep, h), "replica_export");
   publish(handle_path(a.store, a.origin, self.dp), h, sizeof h);
@@ -348,6 +352,7 @@ int run_standby(const Args& a) {
   }
   ffx_replica* src = nullptr;
   ck(ffx_replica_open(ctx, h, &src), "replica_open");
+  const uint64_t t_open = now_ns();
   uint64_t target = a.target;
   if (!target) ck(ffx_replica_newest(src, &target), "replica_newest");
   uint32_t versions = 0, slot = 0;
@@ -419,12 +424,13 @@ int run_standby(const Args& a) {
   std::printf(
       "{\"mode\": \"%s\", \"target_iteration\": %llu, \"holder_dp\": %d, \"bytes\": %llu, \"regions\": %u, "
       "\"time_to_restore_s\": %.6f, \"breakdown_ms\": {\"notice_to_main\": %.3f, \"context\": %.3f, "
-      "\"plan\": %.3f, \"ipc_map\": %.3f, \"alloc_register\": %.3f, \"gather_verify\": %.3f, "
+      "\"plan\": %.3f, \"ipc_map\": %.3f, \"ipc_open\": %.3f, \"alloc_register\": %.3f, \"gather_verify\": %.3f, "
       "\"gather_verify_kernel\": %.3f}, \"warm_context_ms\": %.3f, \"bad_slices\": %llu, \"verified\": %s, "
       "\"blob_is_sound\": %d, \"gbs_kernel\": %.1f}\n",
       a.warm ? "warm" : "cold", (unsigned long long)target, holder, (unsigned long long)total, n,
       (t_done - t0) * 1e-9, a.warm ? ms(t0, t_notice) : ms(t0, t_main), a.warm ? 0.0 : ms(t_ctx_start, t_ctx),
-      ms(a.warm ? t_notice : t_ctx, t_plan), ms(t_plan, t_map), ms(t_map, t_alloc), ms(t_alloc, t_done),
+      ms(a.warm ? t_notice : t_ctx, t_plan), ms(t_plan, t_map), ms(t_plan, t_open), ms(t_map, t_alloc),
+      ms(t_alloc, t_done),
       rpt.seconds * 1e3, a.warm ? ms(t_ctx_start, t_ctx) : 0.0, (unsigned long long)rpt.bad_slices,
       rpt.bad_slices == 0 ? "true" : "false", sound, rpt.seconds > 0 ? total / rpt.seconds / 1e9 : 0.0);
   std::fflush(stdout);
