@@ -150,13 +150,13 @@ def cpu_ring(threads, bytes_per_thread, iters):
     if ref is None:
         return None
     h = ref.ref_ring_setup(threads, bytes_per_thread)
-    secs = (ctypes.c_double * 4)()
+    secs = (ctypes.c_double * 5)()
     out = []
     try:
         for i in range(iters):
             if ref.ref_ring_run(h, i + 1, secs) != 0:
                 raise RuntimeError("reference ring iteration failed")
-            out.append(tuple(secs[k] for k in range(4)))
+            out.append(tuple(secs[k] for k in range(5)))
     finally:
         ref.ref_ring_free(h)
     return out
@@ -182,12 +182,16 @@ def cpu_baseline_line(threads, bytes_per_thread, iters=4):
     take = statistics.median(r[0] for r in res)
     store = statistics.median(r[1] for r in res)
     restore = statistics.median(r[2] for r in res)
+    snap = statistics.median(r[4] for r in res)  # slowest thread's own take + store
     agg = threads * bytes_per_thread
     return {
-        "value": round(agg / (take + store) / 1e9, 3), "unit": "GB/s", "cores": threads, "kind": "reference",
-        "sample": "%d threads x %d MiB per rank x %d iterations (median): HostSnapshots::take + "
-                  "NeighborBuffer::store (the snapshot); reference proj/src compiled -O3 into oracle/_ref"
-                  % (threads, bytes_per_thread >> 20, iters),
+        "value": round(agg / snap / 1e9, 3), "unit": "GB/s", "cores": threads, "kind": "reference",
+        "sample": "%d threads x %d MiB per rank x %d iterations (median of the slowest thread's take + store): "
+                  "HostSnapshots::take + NeighborBuffer::store (the snapshot); reference proj/src compiled -O3 "
+                  "into oracle/_ref" % (threads, bytes_per_thread >> 20, iters),
+        "same_config": False,
+        "sample_vs_config": "a 256 MiB per-thread sample of the %d-byte shard (the metric is GB/s)" %
+                            ((12 * PHI_GPT2_XL + D_REF - 1) // D_REF),
         "stages_gbs": {"take": round(agg / take / 1e9, 3), "store": round(agg / store / 1e9, 3),
                        "restore": round(agg / restore / 1e9, 3)},
         "nproc": os.cpu_count(), "cpu_model": cpu_model(),
@@ -208,7 +212,7 @@ def run_reference(args):
         return
     res = res[max(1, args.warmup):]
     agg = threads * per
-    t = sum(r[0] + r[1] for r in res)
+    t = sum(r[4] for r in res)  # per step: the slowest thread's own take + store
     value = agg * len(res) / t / 1e9
     print(json.dumps({
         "impl": "reference", "metric": "snapshot GB/s (per-iteration neighbour backup, all ranks)",
@@ -217,7 +221,9 @@ def run_reference(args):
         "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic (evo::materialize, seed 42)",
         "config": {"workload": "reference CPU path (HostSnapshots::take + NeighborBuffer::store) on a bounded "
                                "sample of the GPT-2 XL ZeRO-1 d=8 shard, one thread per ring rank",
-                   "bytes_per_rank_sample": per, "ranks": threads},
+                   "bytes_per_rank_sample": per, "ranks": threads, "same_config": False,
+                   "sample_vs_config": "256 MiB per thread vs the %d-byte shard (GB/s metric)"
+                                       % ((12 * PHI_GPT2_XL + D_REF - 1) // D_REF)},
         "cpu_baseline": {"value": round(value, 3), "unit": "GB/s", "cores": threads, "kind": "reference",
                          "sample": "%d threads x 256 MiB per step" % threads,
                          "nproc": os.cpu_count(), "cpu_model": cpu_model()},

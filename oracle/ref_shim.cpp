@@ -165,7 +165,9 @@ void* ref_ring_setup(int threads, std::uint64_t bytes) {
 void ref_ring_free(void* h) { delete static_cast<RefRing*>(h); }
 
 // Per-stage seconds (max over threads) into secs[0..2] (take, store,
-// restore) and the wall time of the whole parallel iteration into secs[3].
+// restore), the wall time of the whole parallel iteration into secs[3], and
+// the snapshot time of the slowest thread -- max over threads of that
+// thread's own take + store -- into secs[4].
 // Returns 0, or -1 if any stage threw or restored the wrong size.
 int ref_ring_run(void* h, std::uint64_t iteration, double* secs) {
   auto* r = static_cast<RefRing*>(h);
@@ -210,6 +212,11 @@ int ref_ring_run(void* h, std::uint64_t iteration, double* secs) {
   for (int k = 0; k < 3; ++k) {
     secs[k] = 0;
     for (int t = 0; t < threads; ++t) secs[k] = st[3 * t + k] > secs[k] ? st[3 * t + k] : secs[k];
+  }
+  secs[4] = 0;
+  for (int t = 0; t < threads; ++t) {
+    const double snap = st[3 * t + 0] + st[3 * t + 1];
+    secs[4] = snap > secs[4] ? snap : secs[4];
   }
   for (int t = 0; t < threads; ++t)
     if (!ok[t]) return -1;
