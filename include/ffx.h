@@ -384,6 +384,15 @@ int ffx_mcast_supported(int device, int* supported);
 /* A replica whose memory can be bound to a multicast range (a shareable VMM
  * allocation instead of cudaMalloc); otherwise identical to
  * ffx_replica_create, exported/opened with the same calls. */
+/* Tiered replica (SURVEY 7.2 hard part 3: a Llama-3 70B replica does not fit
+ * next to its holder's own state in 180 GB): one slot range whose first
+ * hbm_bytes are device memory and the rest pinned host memory on the
+ * holder's NUMA node -- the reference keeps its replicas in host memory
+ * (ckpt.cpp:52, :92).  Exported / opened / snapshotted / recovered like any
+ * replica; the host tier moves over PCIe.  ffx_replica_tiers reports the split. */
+int ffx_replica_create_tiered(ffx_ctx* ctx, ffx_role origin, uint64_t capacity, uint32_t versions,
+                              uint64_t hbm_bytes, ffx_replica** out);
+int ffx_replica_tiers(const ffx_replica* r, uint64_t* hbm_bytes, uint64_t* host_bytes);
 int ffx_replica_create_shared(ffx_ctx* ctx, ffx_role origin, uint64_t capacity, uint32_t versions,
                               ffx_replica** out);
 /* Origin: a multicast object sized for replicas of (capacity, versions,

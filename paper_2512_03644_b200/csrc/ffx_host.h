@@ -146,6 +146,13 @@ struct ffx_replica {
   unsigned long long vmm_handle = 0;
   uint64_t vmm_bytes = 0;
   int vmm_fd = -1;
+  // Tiered replicas (a replica larger than the holder's free HBM, configs[4]):
+  // one VA range whose first tier_hbm bytes are device memory and the rest
+  // pinned host memory on the device's NUMA node (vmm_handle2 / vmm_fd2).
+  // Kernels address it as one buffer; the host tier moves over PCIe.
+  uint64_t tier_hbm = 0;
+  unsigned long long vmm_handle2 = 0;
+  int vmm_fd2 = -1;
   // Multicast target: kernels WRITE through wbase (the multicast range every
   // holder's replica is bound to) and the host READS slot metadata through
   // base (one holder's unicast mapping).  Null = write through base.
@@ -221,9 +228,12 @@ struct HandleBlob {  // FFX_HANDLE_BYTES on the wire
   uint16_t dp, pp, tp, pad_;
   SlotLayout layout;
   cudaIpcMemHandle_t ipc;
-  uint32_t kind;         // 0 = cudaMalloc + CUDA IPC, 1 = shareable VMM allocation
-  int32_t fd;            // kind 1: the exporter's fd (fetched through its fd server)
-  uint64_t alloc_bytes;  // kind 1: allocation size
+  uint32_t kind;         // 0 = cudaMalloc + CUDA IPC, 1 = shareable VMM allocation, 2 = tiered VMM
+  int32_t fd;            // kind 1/2: the exporter's fd (fetched through its fd server)
+  uint64_t alloc_bytes;  // kind 1/2: size of the whole range
+  int32_t fd2;           // kind 2: the host-memory tier's fd
+  uint32_t pad2_;
+  uint64_t tier_hbm;     // kind 2: bytes of the range backed by device memory (the rest: host memory)
 };
 static_assert(sizeof(HandleBlob) <= FFX_HANDLE_BYTES, "handle too large");
 constexpr uint32_t kHandleMagic = 0x48584646u;

@@ -125,6 +125,51 @@ int map_range(CUmemGenericAllocationHandle h, uint64_t bytes, uint64_t align, in
   return FFX_OK;
 }
 
+// A pinned host-memory allocation on the NUMA node closest to `device`
+// (the tier below HBM of a tiered replica), shareable by fd like the rest.
+CUmemAllocationProp host_prop(int device) {
+  CUmemAllocationProp ap{};
+  ap.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+  ap.location.type = CU_MEM_LOCATION_TYPE_HOST_NUMA;
+  int numa = -1;
+  CUdevice d;
+  if (drv().deviceGet(&d, device) == CUDA_SUCCESS) drv().deviceAttr(&numa, CU_DEVICE_ATTRIBUTE_HOST_NUMA_ID, d);
+  ap.location.id = numa < 0 ? 0 : numa;
+  ap.requestedHandleTypes = kShareType;
+  return ap;
+}
+
+// One VA range [0, dev_bytes + host_bytes): device memory first, host memory
+// after; `device` gets read/write access to all of it.
+int map_tiered(CUmemGenericAllocationHandle hd, uint64_t dev_bytes, CUmemGenericAllocationHandle hh,
+               uint64_t host_bytes, uint64_t align, int device, uint8_t** va) {
+  const uint64_t total = dev_bytes + host_bytes;
+  CUdeviceptr p = 0;
+  FFX_DRV(drv().addressReserve(&p, total, align, 0, 0));
+  CUresult r = CUDA_SUCCESS;
+  if (dev_bytes) r = drv().memMap(p, dev_bytes, 0, hd, 0);
+  if (r == CUDA_SUCCESS && host_bytes) {
+    r = drv().memMap(p + dev_bytes, host_bytes, 0, hh, 0);
+    if (r != CUDA_SUCCESS && dev_bytes) drv().memUnmap(p, dev_bytes);
+  }
+  if (r != CUDA_SUCCESS) {
+    drv().addressFree(p, total);
+    return drv_fail(r, "cuMemMap (tiered)");
+  }
+  CUmemAccessDesc acc{};
+  acc.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+  acc.location.id = device;
+  acc.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+  r = drv().setAccess(p, total, &acc, 1);
+  if (r != CUDA_SUCCESS) {
+    drv().memUnmap(p, total);
+    drv().addressFree(p, total);
+    return drv_fail(r, "cuMemSetAccess (tiered)");
+  }
+  *va = reinterpret_cast<uint8_t*>(p);
+  return FFX_OK;
+}
+
 int grant_access(uint8_t* va, uint64_t bytes, int owner_dev, int other_dev) {
   CUmemAccessDesc acc[2] = {};
   for (int i = 0; i < 2; ++i) {
@@ -155,21 +200,31 @@ int open_shared(ffx_ctx* c, const HandleBlob& h, ffx_replica* r) {
     if (h.device != c->device) return grant_access(r->base, h.alloc_bytes, h.device, c->device);
     return FFX_OK;
   }
-  int fd = -1;
-  int st = fetch_or_fail(h.pid, h.fd, &fd);
-  if (st) return st;
-  CUmemGenericAllocationHandle mh = 0;
-  CUresult cr = drv().importHandle(&mh, reinterpret_cast<void*>(static_cast<uintptr_t>(fd)), kShareType);
-  close(fd);
-  if (cr != CUDA_SUCCESS) return drv_fail(cr, "cuMemImportFromShareableHandle");
+  auto import_fd = [&](int remote_fd, CUmemGenericAllocationHandle* out) -> int {
+    int fd = -1;
+    int st = fetch_or_fail(h.pid, remote_fd, &fd);
+    if (st) return st;
+    CUresult cr = drv().importHandle(out, reinterpret_cast<void*>(static_cast<uintptr_t>(fd)), kShareType);
+    close(fd);
+    return cr != CUDA_SUCCESS ? drv_fail(cr, "cuMemImportFromShareableHandle") : FFX_OK;
+  };
+  CUmemGenericAllocationHandle mh = 0, mh2 = 0;
+  const bool tiered = h.kind == 2;
+  const uint64_t dev_bytes = tiered ? h.tier_hbm : h.alloc_bytes;
+  int st = dev_bytes ? import_fd(h.fd, &mh) : FFX_OK;
+  if (!st && tiered && h.alloc_bytes > dev_bytes) st = import_fd(h.fd2, &mh2);
   uint64_t gran = 0;
-  st = share_gran(c->device, &gran);
-  if (!st) st = map_range(mh, h.alloc_bytes, gran, c->device, &r->base);
+  if (!st) st = share_gran(c->device, &gran);
+  if (!st) st = tiered ? map_tiered(mh, dev_bytes, mh2, h.alloc_bytes - dev_bytes, gran, c->device, &r->base)
+                       : map_range(mh, h.alloc_bytes, gran, c->device, &r->base);
   if (st) {
-    drv().memRelease(mh);
+    if (mh) drv().memRelease(mh);
+    if (mh2) drv().memRelease(mh2);
     return st;
   }
   r->vmm_handle = mh;
+  r->vmm_handle2 = mh2;
+  r->tier_hbm = tiered ? dev_bytes : 0;
   r->vmm_mapped = true;
   return FFX_OK;
 }
@@ -178,11 +233,14 @@ void release_shared(ffx_replica* r) {
   if ((r->owned || r->vmm_mapped) && r->base) {
     drv().memUnmap(reinterpret_cast<CUdeviceptr>(r->base), r->vmm_bytes);
     drv().addressFree(reinterpret_cast<CUdeviceptr>(r->base), r->vmm_bytes);
-    drv().memRelease(r->vmm_handle);
+    if (r->vmm_handle) drv().memRelease(r->vmm_handle);
+    if (r->vmm_handle2) drv().memRelease(r->vmm_handle2);
   }
-  if (r->owned && r->vmm_fd >= 0) {
-    unshare_fd(r->vmm_fd);
-    close(r->vmm_fd);
+  for (int fd : {r->vmm_fd, r->vmm_fd2}) {
+    if (r->owned && fd >= 0) {
+      unshare_fd(fd);
+      close(fd);
+    }
   }
 }
 
@@ -257,6 +315,94 @@ extern "C" int ffx_replica_create_shared(ffx_ctx* c, ffx_role origin, uint64_t c
     return cuda_fail(ce, "replica_create_shared");
   }
   *out = r;
+  return FFX_OK;
+}
+
+extern "C" int ffx_replica_create_tiered(ffx_ctx* c, ffx_role origin, uint64_t capacity, uint32_t versions,
+                                         uint64_t hbm_bytes, ffx_replica** out) {
+  if (!c || !out) return fail(FFX_EINVAL, "replica_create_tiered: null argument");
+  if (versions < 1 || versions > 8) return fail(FFX_EINVAL, "replica_create_tiered: 1..8 versions");
+  DeviceGuard g(c->device);
+  uint64_t gran = 0;
+  int st = share_gran(c->device, &gran);
+  if (st) return st;
+  CUmemAllocationProp hp = host_prop(c->device);
+  size_t hg = 0;
+  FFX_DRV(drv().allocGran(&hg, &hp, CU_MEM_ALLOC_GRANULARITY_MINIMUM));
+  gran = std::max<uint64_t>(gran, hg);
+  const SlotLayout L = make_layout(capacity, c->slice_bytes);
+  const uint64_t total = align_up(L.slot_stride * versions, gran);
+  const uint64_t dev_bytes = std::min(total, align_up(hbm_bytes, gran));
+  const uint64_t host_bytes = total - dev_bytes;
+  CUmemAllocationProp dp = share_prop(c->device);
+  CUmemGenericAllocationHandle hd = 0, hh = 0;
+  if (dev_bytes) FFX_DRV(drv().memCreate(&hd, dev_bytes, &dp, 0));
+  if (host_bytes) {
+    CUresult cr = drv().memCreate(&hh, host_bytes, &hp, 0);
+    if (cr != CUDA_SUCCESS) {
+      if (hd) drv().memRelease(hd);
+      return drv_fail(cr, "cuMemCreate (host tier)");
+    }
+  }
+  auto* r = new ffx_replica;
+  r->device = c->device;
+  r->owner_pid = getpid();
+  r->owned = true;
+  r->vmm = true;
+  r->vmm_handle = hd;
+  r->vmm_handle2 = hh;
+  r->vmm_bytes = total;
+  r->tier_hbm = dev_bytes;
+  r->origin = origin;
+  r->capacity = capacity;
+  r->slice_bytes = c->slice_bytes;
+  r->versions = versions;
+  r->layout = L;
+  r->cache.assign(versions, SlotCache{});
+  r->ctx = c;
+  st = map_tiered(hd, dev_bytes, hh, host_bytes, gran, c->device, &r->base);
+  if (st) {
+    if (hd) drv().memRelease(hd);
+    if (hh) drv().memRelease(hh);
+    delete r;
+    return st;
+  }
+  auto export_fd = [&](CUmemGenericAllocationHandle h, int* fd_out) -> int {
+    if (!h) return FFX_OK;
+    int fd = -1;
+    CUresult cr = drv().exportHandle(&fd, h, kShareType, 0);
+    const int e = cr == CUDA_SUCCESS ? share_fd(fd) : 0;
+    if (cr != CUDA_SUCCESS || e) {
+      if (fd >= 0) close(fd);
+      return cr != CUDA_SUCCESS ? drv_fail(cr, "cuMemExportToShareableHandle (tiered)")
+                                : fail(FFX_ECUDA, "fd server: %s", std::strerror(e));
+    }
+    *fd_out = fd;
+    return FFX_OK;
+  };
+  st = export_fd(hd, &r->vmm_fd);
+  if (!st) st = export_fd(hh, &r->vmm_fd2);
+  cudaError_t ce = cudaSuccess;
+  for (uint32_t v = 0; !st && v < versions && ce == cudaSuccess; ++v) {
+    ce = cudaMemset(r->slot(v), 0, kMetaBytes);
+    r->cache[v].known = true;
+  }
+  if (!st && ce == cudaSuccess) ce = cudaDeviceSynchronize();
+  if (st || ce != cudaSuccess) {
+    release_shared(r);
+    delete r;
+    return st ? st : cuda_fail(ce, "replica_create_tiered");
+  }
+  *out = r;
+  return FFX_OK;
+}
+
+extern "C" int ffx_replica_tiers(const ffx_replica* r, uint64_t* hbm_bytes, uint64_t* host_bytes) {
+  if (!r) return fail(FFX_EINVAL, "replica_tiers: null argument");
+  const uint64_t total = r->vmm ? r->vmm_bytes : r->layout.slot_stride * r->versions;
+  const uint64_t dev = (r->vmm_handle2 || r->tier_hbm) ? r->tier_hbm : total;
+  if (hbm_bytes) *hbm_bytes = dev;
+  if (host_bytes) *host_bytes = total - dev;
   return FFX_OK;
 }
 

@@ -103,8 +103,10 @@ extern "C" int ffx_replica_export(const ffx_replica* r, uint8_t handle[FFX_HANDL
   h.tp = r->origin.tp;
   h.layout = r->layout;
   if (r->vmm) {
-    h.kind = 1;
+    h.kind = r->vmm_handle2 || r->vmm_fd2 >= 0 ? 2 : 1;
     h.fd = r->vmm_fd;
+    h.fd2 = r->vmm_fd2;
+    h.tier_hbm = r->tier_hbm;
     h.alloc_bytes = r->vmm_bytes;
     if (r->vmm_fd < 0) return fail(FFX_EINVAL, "replica_export: an imported shared replica cannot be re-exported");
   } else if (r->owned) {
@@ -125,7 +127,7 @@ extern "C" int ffx_replica_open(ffx_ctx* c, const uint8_t handle[FFX_HANDLE_BYTE
     return fail(FFX_EINVAL, "replica_open: not an ffx replica handle");
   // a damaged handle must not become out-of-bounds slot addressing
   const SlotLayout want = make_layout(h.capacity, h.slice_bytes ? h.slice_bytes : 1);
-  if (h.versions < 1 || h.versions > 8 || !slice_ok(h.slice_bytes) || h.kind > 1 ||
+  if (h.versions < 1 || h.versions > 8 || !slice_ok(h.slice_bytes) || h.kind > 2 ||
       std::memcmp(&want, &h.layout, sizeof want) != 0)
     return fail(FFX_EINVAL, "replica_open: inconsistent replica handle");
   DeviceGuard g(c->device);
@@ -139,7 +141,7 @@ extern "C" int ffx_replica_open(ffx_ctx* c, const uint8_t handle[FFX_HANDLE_BYTE
   r->layout = h.layout;
   r->cache.assign(h.versions, SlotCache{});
   r->ctx = c;
-  if (h.kind == 1) {
+  if (h.kind == 1 || h.kind == 2) {
     int st = open_shared(c, h, r);
     if (st) {
       delete r;

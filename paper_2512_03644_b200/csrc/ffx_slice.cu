@@ -216,8 +216,9 @@ struct Cfg {
   static constexpr int STAGE = PLANE * KC;           // one TMA box: KC planes
   static constexpr int PADROW = C + 16;              // register-path row, padded for banks
   static constexpr int WARPB = S * STAGE > 32 * PADROW ? S * STAGE : 32 * PADROW;
-  static constexpr int BARB = ((W * S * 8 + 1023) / 1024) * 1024;
-  static constexpr int SMEM = BARB + W * WARPB + 1024;  // + slack to 1 KB-align the base
+  // [tiles: W x WARPB, 1 KB-aligned (128 B swizzle atoms)][mbarriers: W x S x 8 B]
+  static constexpr int TILES = W * WARPB;
+  static constexpr int SMEM = TILES + W * S * 8 + 1024;  // + slack to 1 KB-align the base
 };
 
 // One warp task = ROWS consecutive slices of one region; lane l owns slices
@@ -234,8 +235,8 @@ __global__ void __launch_bounds__(W * 32) slice_kernel(const __grid_constant__ S
   uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
-  uint8_t* wbase = smem + K::BARB + warp * K::WARPB;
-  const uint32_t bar0 = smem_u32(smem) + warp * S * 8;
+  uint8_t* wbase = smem + warp * K::WARPB;
+  const uint32_t bar0 = smem_u32(smem) + K::TILES + warp * S * 8;
   const uint32_t stage0 = smem_u32(wbase);
 
   if (lane == 0) {
@@ -547,7 +548,10 @@ struct Variant {
 constexpr Variant kVariants[] = {{3, 4, 1, 0, 2}, {2, 4, 2, 0, 1}, {3, 4, 2, 0, 1}, {6, 4, 1, 0, 1},
                                  {3, 4, 1, 0, 1}, {2, 8, 2, 0, 1}, {4, 4, 1, 1, 1}, {3, 4, 2, 1, 1},
                                  {6, 4, 1, 1, 1}, {2, 4, 1, 0, 2}, {4, 4, 1, 0, 1}, {2, 4, 1, 0, 4},
-                                 {2, 8, 1, 0, 2}, {2, 4, 1, 0, 1}};
+                                 {2, 8, 1, 0, 2}, {2, 4, 1, 0, 1},
+                                 // 14-16: small enough (< 18 KB smem, 64 threads) to sit beside a
+                                 // 213 KB / 256-thread cuBLAS GEMM CTA on the same SM
+                                 {2, 2, 1, 0, 1}, {3, 1, 1, 0, 1}, {2, 1, 1, 0, 2}};
 constexpr int kHashDefault = 9;
 int variant() {
   static const int v = [] {
@@ -594,6 +598,9 @@ cudaError_t launch_mode(const SliceJob& job, uint32_t max_ctas, cudaStream_t str
     case 11: return launch_t<2, 4, 1, false, M, kCommit, 4>(job, max_ctas, stream);
     case 12: return launch_t<2, 8, 1, false, M, kCommit, 2>(job, max_ctas, stream);
     case 13: return launch_t<2, 4, 1, false, M, kCommit>(job, max_ctas, stream);
+    case 14: return launch_t<2, 2, 1, false, M, kCommit>(job, max_ctas, stream);
+    case 15: return launch_t<3, 1, 1, false, M, kCommit>(job, max_ctas, stream);
+    case 16: return launch_t<2, 1, 1, false, M, kCommit, 2>(job, max_ctas, stream);
     default: return launch_t<3, 4, 1, false, M, kCommit, 2>(job, max_ctas, stream);
   }
 #else

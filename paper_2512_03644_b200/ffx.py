@@ -274,6 +274,8 @@ SIGNATURES = {
     "ffx_sched_gap": (_I, [_P, _I, _P]),
     "ffx_sched_finish": (_I, [_P, _P]),
     "ffx_sched_destroy": (_I, [_P]),
+    "ffx_replica_create_tiered": (_I, [_P, Role, _U64, _U32, _U64, ctypes.POINTER(_P)]),
+    "ffx_replica_tiers": (_I, [_P, ctypes.POINTER(_U64), ctypes.POINTER(_U64)]),
     "ffx_replica_create_shared": (_I, [_P, Role, _U64, _U32, ctypes.POINTER(_P)]),
     "ffx_mcast_create": (_I, [_P, _U64, _U32, _U32, ctypes.POINTER(_P)]),
     "ffx_mcast_export": (_I, [_P, _P]),
@@ -723,6 +725,12 @@ class Replica:
     def clear(self):
         check(lib.ffx_replica_clear(self._h), "replica_clear")
 
+    def tiers(self):
+        """(bytes in HBM, bytes in host memory) of this replica's range."""
+        a, b = _U64(), _U64()
+        check(lib.ffx_replica_tiers(self._h, ctypes.byref(a), ctypes.byref(b)), "replica_tiers")
+        return a.value, b.value
+
     def rollback(self, iteration: int) -> int:
         """Drop slots newer than `iteration` (ffx_replica_rollback); returns
         how many.  Writers re-arm their target afterwards (set_target)."""
@@ -977,6 +985,15 @@ class Context:
         h = ctypes.c_void_p()
         check(lib.ffx_replica_create_shared(self._c, origin, capacity, versions, ctypes.byref(h)),
               "replica_create_shared")
+        return Replica(h.value, self)
+
+    def create_tiered_replica(self, origin, capacity: int, versions: int, hbm_bytes: int) -> Replica:
+        """A replica whose first hbm_bytes live in HBM and the rest in pinned
+        host memory (ffx_replica_create_tiered)."""
+        origin = origin if isinstance(origin, Role) else Role(*origin)
+        h = ctypes.c_void_p()
+        check(lib.ffx_replica_create_tiered(self._c, origin, capacity, versions, hbm_bytes, ctypes.byref(h)),
+              "replica_create_tiered")
         return Replica(h.value, self)
 
     def create_mcast(self, capacity: int, versions: int = 2, members: int = 3) -> Mcast:
