@@ -565,6 +565,15 @@ def main():
         except Exception as ex:
             seventy = {"error": repr(ex)}
 
+    # ---- Llama-3 70B ZeRO-3 (configs[4]): one full replica on a tiered slot ------
+    tiered = None
+    if world == 1 and not args.no_70b:
+        try:
+            tiered = seventy_tiered_leg(args, ffx, torch, local, peaks)
+        except Exception as ex:  # reported, never fatal
+            tiered = {"error": repr(ex)}
+        torch.cuda.empty_cache()
+
     # ---- time to restore a replaced rank (configs[3]): a new process ----------
     ttr = None
     if not args.no_llama and not args.no_standby:
@@ -600,6 +609,7 @@ def main():
             "llama3_8b": llama,
             "llama3_8b_failure_at_d": dfail,
             "llama3_70b_double_neighbour": seventy,
+            "llama3_70b_tiered_replica": tiered,
             "time_to_restore": ttr,
             "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": int(launches), "clocks": ck, "commit_ok": bool(commit_ok),
@@ -607,6 +617,65 @@ def main():
 
     dist.barrier()
     dist.destroy_process_group()
+
+
+def seventy_tiered_leg(args, ffx, torch, local, peaks):
+    """configs[4] at full size on one B200: a Llama-3 70B ZeRO-3 d=8 rank's
+    six regions (123.5 GB: ceil(12phi/8) fp32 master + Adam m/v, 2phi/8 bf16
+    params, cursor, RNG) and ONE complete replica of them.  Own state plus a
+    replica is 247 GB -- more than the 180 GB of HBM -- so the replica is
+    tiered (ffx_replica_create_tiered): what still fits in HBM, the rest in
+    pinned host memory on the GPU's NUMA node (the reference keeps replicas in
+    host memory, ckpt.cpp:52, :92).  Snapshot and recovery run the same
+    kernels over the one VA range; the host tier is PCIe-bound."""
+    from paper_2512_03644_b200 import state
+    regs = state.zero3_shard(PHI_LLAMA3_70B, D_REF, 1)
+    nbytes = state.shard_bytes(regs)
+    spec = ffx.make_spec(d=D_REF, phi=PHI_LLAMA3_70B, distributed=True)
+    holder = ffx.Context(local, spec, ffx.Role(2, 0, 0), args.slice_bytes)
+    origin = ffx.Context(local, spec, ffx.Role(1, 0, 0), args.slice_bytes)
+    out = {"bytes_per_rank": nbytes, "regions": len(regs), "replica_versions": 1}
+    ts, rep, view = [], None, None
+    try:
+        ts = state.allocate(ffx, torch, origin, regs)
+        torch.cuda.synchronize()
+        free, total = torch.cuda.mem_get_info()
+        hbm = max(0, free - (12 << 30))  # leave headroom for the context and the kernels
+        rep = holder.create_tiered_replica(ffx.Role(1, 0, 0), nbytes, 1, hbm)
+        view = origin.open_replica(rep.export())
+        origin.set_target(view)
+        dev, host = rep.tiers()
+        out.update(hbm_tier_bytes=dev, host_tier_bytes=host, hbm_total_bytes=total)
+        s = torch.cuda.Stream()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(s)
+        origin.snapshot(1, stream=s)
+        e1.record(s)
+        s.synchronize()
+        t = e0.elapsed_time(e1) / 1e3
+        out["snapshot_s"] = round(t, 4)
+        out["snapshot_gbs"] = round(nbytes / t / 1e9, 2)
+        origin.inject(ffx.FAULT_POISON_STATE)
+        rpt = origin.recover(view, 1, stream=s)
+        ok = rpt.bad_slices == 0
+        for r, tt in zip(regs, ts):
+            ok = ok and (bytes(tt.cpu().numpy().tobytes()) == r.literal if r.literal is not None
+                         else ffx.blob_is_sound(tt))
+        out["recovery_s"] = round(rpt.seconds, 4)
+        out["recovery_gbs"] = round(nbytes / rpt.seconds / 1e9, 2)
+        out["verified_bit_exact"] = bool(ok)
+        out["note"] = ("host tier over PCIe (one GPU's link); HBM tier at HBM rate -- the time is the PCIe "
+                       "share: host_tier_bytes / (PCIe GB/s)")
+    finally:
+        torch.cuda.synchronize()
+        if view is not None:
+            view.destroy()
+        if rep is not None:
+            rep.destroy()
+        del ts
+        origin.close()
+        holder.close()
+    return out
 
 
 def e2e_leg(args, ffx, torch, R, world, rank, local, n, stream, barrier, max_over_ranks, it):

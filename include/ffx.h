@@ -33,7 +33,7 @@
 extern "C" {
 #endif
 
-#define FFX_ABI_VERSION 1
+#define FFX_ABI_VERSION 2
 #define FFX_MAX_REGIONS 16
 #define FFX_HANDLE_BYTES 256
 
@@ -437,6 +437,14 @@ typedef struct ffx_snapshot_opts {
    * in a calibration step).  NULL = equal batches.  Hash batches of the
    * split policy stay equal. */
   const double* batch_weights;
+  /* Nonzero: fused batches launch one CTA per task group and no persistent
+   * claim loop, so under stream priorities the block scheduler hands SMs to
+   * pending TRAIN CTAs at every task boundary (one 32-slice task, ~0.1 ms) and
+   * STATE CTAs only fill what TRAIN leaves idle (wave tails, kernel
+   * boundaries) -- the reference's chunk-boundary preemption
+   * (sim_net.cpp:401-454) at task granularity; max_ctas is then ignored. */
+  uint32_t task_ctas;
+  uint32_t pad_;
 } ffx_snapshot_opts;
 
 enum ffx_batch_kind { FFX_BATCH_COPY = 0, FFX_BATCH_HASH = 1 };
@@ -486,7 +494,7 @@ typedef struct ffx_sched_opts {
   uint32_t sm_gaps;        /* FFX_GAP_SM_IDLE reports per step (checksum batches; split) */
   uint32_t copy_ctas;      /* CTA cap of fused / TMA copy batches (0 = 32 / 8) */
   uint32_t hash_ctas;      /* CTA cap of checksum batches (0 = 96) */
-  uint32_t pad_;
+  uint32_t task_ctas;      /* fused policy: task-granular batches (ffx_snapshot_opts.task_ctas) */
   const double* gap_ms;    /* measured link-idle gap durations, link_gaps entries (NULL = equal) */
 } ffx_sched_opts;
 typedef struct ffx_sched ffx_sched;

@@ -242,6 +242,15 @@ cudaError_t launch_copy(const CopyJob& job, uint32_t ctas, cudaStream_t stream) 
   return cudaGetLastError();
 }
 
+cudaError_t launch_mark(const SlotCommit& c, const SlotCommit* c2, cudaStream_t stream) {
+  CopyJob mark{};
+  mark.mark = SlotMark{c.slot, c.iteration, c.seq, c.mcast, 0};
+  if (c2) mark.mark2 = SlotMark{c2->slot, c2->iteration, c2->seq, c2->mcast, 0};
+  finalize_copy_job(mark);
+  mark.chunk_lo = mark.chunk_hi = 0;
+  return launch_copy(mark, 1, stream);
+}
+
 cudaError_t launch_commit(const SlotCommit& c, cudaStream_t stream) {
   commit_kernel<<<1, 1, 0, stream>>>(c);
   return cudaGetLastError();

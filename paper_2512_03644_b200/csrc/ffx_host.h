@@ -173,6 +173,7 @@ struct PendingSnapshot {
   uint32_t batches = 1, next = 0, max_ctas = 0, slot = 0, slot2 = 0;
   uint64_t iteration = 0, seq = 0, seq2 = 0, nslices = 0, logical = 0;
   bool verify = false;
+  bool one_shot = false;  // task-granular fused batches (opts.task_ctas)
   // split policy: copy batches and hash batches drain independently
   bool split = false, copy_engine = false;
   CopyJob copy{};

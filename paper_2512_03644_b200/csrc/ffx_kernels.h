@@ -69,6 +69,8 @@ struct SliceJob {
   uint32_t store_hint;            // tensor stores with an L2 evict_first hint (experiment)
   uint32_t prefetch_next;         // tensor path: claim the next task S steps early and load its
                                   // first S steps into the stages this task frees (no per-task drain)
+  uint32_t one_shot;              // one task per warp, no claim loop (task-granular batches)
+  uint32_t skip_begin;            // the slot was marked WRITING by a preceding mark launch
   SlotCommit commit;
   SlotCommit commit2;             // second replica's slot (slot null = none)
 };
@@ -108,6 +110,8 @@ void finalize_copy_job(CopyJob& job);
 cudaError_t launch_copy(const CopyJob& job, uint32_t ctas, cudaStream_t stream);
 // One-thread kernel writing the final meta + SNP1 header, then COMMITTED.
 cudaError_t launch_commit(const SlotCommit& c, cudaStream_t stream);
+// One-warp kernel marking the slot(s) of c (and c2) WRITING.
+cudaError_t launch_mark(const SlotCommit& c, const SlotCommit* c2, cudaStream_t stream);
 
 // Slices per warp task.  Two kernel configurations ship (ffx_slice.cu):
 // kBulkRows (32 slices, one chain per lane: the full-GPU, HBM/NVLink-bound

@@ -108,7 +108,7 @@ extern "C" int ffx_replica_export(const ffx_replica* r, uint8_t handle[FFX_HANDL
     h.fd2 = r->vmm_fd2;
     h.tier_hbm = r->tier_hbm;
     h.alloc_bytes = r->vmm_bytes;
-    if (r->vmm_fd < 0) return fail(FFX_EINVAL, "replica_export: an imported shared replica cannot be re-exported");
+    if (!r->owned) return fail(FFX_EINVAL, "replica_export: an imported shared replica cannot be re-exported");
   } else if (r->owned) {
     DeviceGuard g(r->device);
     FFX_CUDA(cudaIpcGetMemHandle(&h.ipc, r->base));

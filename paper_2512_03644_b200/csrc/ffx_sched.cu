@@ -110,6 +110,7 @@ extern "C" int ffx_sched_begin(ffx_sched* s, uint64_t iteration) {
   ffx_snapshot_opts o{};
   o.batches = s->opts.link_gaps;
   o.max_ctas = s->opts.copy_ctas;
+  o.task_ctas = s->opts.policy == FFX_SCHED_FUSED ? s->opts.task_ctas : 0;
   o.batch_weights = s->weights.empty() ? nullptr : s->weights.data();
   if (split_policy(s)) {
     o.split = 1;

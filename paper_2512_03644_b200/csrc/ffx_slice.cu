@@ -247,8 +247,10 @@ __global__ void __launch_bounds__(W * 32) slice_kernel(const __grid_constant__ S
   uint32_t phase = 0;  // bit s: parity of the next completion of stage s
 
   if constexpr (kCommit) {
-    if (job.commit2.slot != nullptr) commit_begin(job.commit2);
-    commit_begin(job.commit);
+    if (!job.skip_begin) {
+      if (job.commit2.slot != nullptr) commit_begin(job.commit2);
+      commit_begin(job.commit);
+    }
   }
 
   const uint64_t Sl = job.slice_bytes;
@@ -256,7 +258,15 @@ __global__ void __launch_bounds__(W * 32) slice_kernel(const __grid_constant__ S
   uint64_t g_next = job.group_lo + static_cast<uint64_t>(blockIdx.x) * W + warp;
   const uint64_t g_stride = static_cast<uint64_t>(gridDim.x) * W;
   constexpr uint64_t kNone = ~0ull;
+  bool once = false;
   auto claim = [&]() -> uint64_t {
+    if (job.one_shot) {
+      // task-granular batch: warp i of the grid owns task i (last first), once
+      if (once) return kNone;
+      once = true;
+      const uint64_t i = static_cast<uint64_t>(blockIdx.x) * W + warp;
+      return i < job.group_hi - job.group_lo ? job.group_hi - 1 - i : kNone;
+    }
     if (job.sched != nullptr) {
       // Claims run from the LAST task down: each region's ragged tail (and
       // tiny register-path regions) starts first and overlaps the bulk
@@ -531,6 +541,7 @@ cudaError_t launch_t(const SliceJob& job, uint32_t max_ctas, cudaStream_t stream
   const uint64_t want = (job.group_hi - job.group_lo + W - 1) / W;
   uint64_t cap = static_cast<uint64_t>(occ) * sm_count();
   if (max_ctas) cap = std::min<uint64_t>(cap, max_ctas);
+  if (job.one_shot) cap = ~0ull;  // one CTA per W tasks: the block scheduler interleaves
   const uint64_t grid = std::max<uint64_t>(1, std::min(want, cap));
   kern<<<static_cast<unsigned>(grid), W * 32, smem, stream>>>(job);
   return cudaGetLastError();

@@ -188,6 +188,7 @@ int begin_impl(ffx_ctx* c, ffx_replica* t, ffx_replica* t2, const std::vector<Sr
   P.nslices = nslices;
   P.logical = logical;
   P.verify = opts.verify_on_store != 0;
+  P.one_shot = opts.task_ctas != 0 && !opts.split;
   P.split = opts.split != 0;
   if (P.split && ack) {
     P.active = false;
@@ -591,6 +592,16 @@ extern "C" int ffx_snapshot_next_kind(ffx_ctx* c, int kind, void* stream, void* 
     bj.group_hi = P.cut(G, b + 1);
     bj.commit.finalize = (b + 1 == P.batches);
     bj.commit2.finalize = bj.commit.finalize;
+    if (P.one_shot) {
+      // thousands of short CTAs: mark the slot WRITING once, stream-ordered
+      // ahead of every payload store, instead of in each CTA
+      if (b == 0) {
+        FFX_CUDA(launch_mark(P.job.commit, P.job.commit2.slot ? &P.job.commit2 : nullptr, s));
+        c->stats.kernel_launches++;
+      }
+      bj.one_shot = 1;
+      bj.skip_begin = 1;
+    }
     if (bj.group_lo != bj.group_hi || bj.commit.finalize) {
       FFX_CUDA(launch_slices(bj, SliceMode::Copy, true, P.max_ctas, s));
       c->stats.kernel_launches++;

@@ -19,7 +19,7 @@ from typing import Optional, Sequence
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libffx.so")
-ABI_VERSION = 1
+ABI_VERSION = 2
 HANDLE_BYTES = 256
 REGIONS_HANDLE_BYTES = 2048
 MCAST_HANDLE_BYTES = 64
@@ -145,12 +145,13 @@ class SnapshotOpts(ctypes.Structure):
                 ("weights_kind", ctypes.c_uint32), ("split", ctypes.c_uint32),
                 ("hash_batches", ctypes.c_uint32), ("hash_ctas", ctypes.c_uint32),
                 ("copy_engine", ctypes.c_uint32), ("fused_permille", ctypes.c_uint32),
-                ("batch_weights", ctypes.POINTER(ctypes.c_double))]
+                ("batch_weights", ctypes.POINTER(ctypes.c_double)),
+                ("task_ctas", ctypes.c_uint32), ("pad_", ctypes.c_uint32)]
 
 
 class SchedOpts(ctypes.Structure):
     _fields_ = [("policy", ctypes.c_uint32), ("link_gaps", ctypes.c_uint32), ("sm_gaps", ctypes.c_uint32),
-                ("copy_ctas", ctypes.c_uint32), ("hash_ctas", ctypes.c_uint32), ("pad_", ctypes.c_uint32),
+                ("copy_ctas", ctypes.c_uint32), ("hash_ctas", ctypes.c_uint32), ("task_ctas", ctypes.c_uint32),
                 ("gap_ms", ctypes.POINTER(ctypes.c_double))]
 
 
@@ -808,10 +809,11 @@ class Sched:
     the training step reports."""
 
     def __init__(self, ctx: "Context", policy: int, link_gaps: int, sm_gaps: int = 0, copy_ctas: int = 0,
-                 hash_ctas: int = 0, gap_ms=None):
+                 hash_ctas: int = 0, gap_ms=None, task_ctas: bool = False):
         o = SchedOpts()
         o.policy, o.link_gaps, o.sm_gaps = policy, link_gaps, sm_gaps
         o.copy_ctas, o.hash_ctas = copy_ctas, hash_ctas
+        o.task_ctas = int(task_ctas)
         if gap_ms is not None:
             self._gaps = (ctypes.c_double * len(gap_ms))(*gap_ms)
             o.gap_ms = self._gaps
@@ -1052,8 +1054,9 @@ class Context:
     def snapshot(self, iteration: int, stream=None, max_ctas: int = 0, batches: int = 1,
                  gate_events=None, verify_on_store: bool = False, weights_kind: bool = False,
                  split: bool = False, hash_batches: int = 0, hash_ctas: int = 0, copy_engine: bool = False,
-                 fused_permille: int = 0):
+                 fused_permille: int = 0, task_ctas: bool = False):
         o = SnapshotOpts()
+        o.task_ctas = int(task_ctas)
         o.split = int(split)
         o.fused_permille = fused_permille
         o.hash_batches = hash_batches
@@ -1073,8 +1076,9 @@ class Context:
     def snapshot_begin(self, iteration: int, batches: int = 1, max_ctas: int = 0,
                        verify_on_store: bool = False, split: bool = False, hash_batches: int = 0,
                        hash_ctas: int = 0, copy_engine: bool = False, batch_weights=None,
-                       fused_permille: int = 0) -> int:
+                       fused_permille: int = 0, task_ctas: bool = False) -> int:
         o = SnapshotOpts()
+        o.task_ctas = int(task_ctas)
         o.fused_permille = fused_permille
         if batch_weights is not None:
             self._weights = (ctypes.c_double * len(batch_weights))(*batch_weights)  # kept alive

@@ -88,7 +88,8 @@ class SliceScheduler:
     """Drives one ffx snapshot per step through the gaps of a SyntheticStep."""
 
     def __init__(self, ctx, step: SyntheticStep, policy: str = "split", copy_ctas: int = 8,
-                 hash_ctas: int = 96, copy_engine: bool = False, front: float = 1.0, rs_gaps: bool = False):
+                 hash_ctas: int = 96, copy_engine: bool = False, front: float = 1.0, rs_gaps: bool = False,
+                 task_ctas: bool = False):
         from paper_2512_03644_b200 import ffx
         self.ffx = ffx
         self.ctx = ctx
@@ -103,6 +104,9 @@ class SliceScheduler:
         # the commit).
         self.front = front
         self.rs_gaps = rs_gaps  # checksum batches also before each reduce-scatter
+        # fused policy: task-granular batches (one CTA per task group, no
+        # persistent loop) -- STATE yields SMs to TRAIN at every task boundary
+        self.task_ctas = task_ctas
         self.native = None  # ffx.Sched, built on first use / after calibrate()
 
     weights = None  # measured idle-link window per copy gap (calibrate())
@@ -148,7 +152,7 @@ class SliceScheduler:
         ks = max(1, min(S, int(round(S * self.front))))
         self.native = ffx.Sched(self.ctx, pol, link_gaps=G, sm_gaps=0 if pol == ffx.SCHED_FUSED else ks,
                                 copy_ctas=self.copy_ctas or (1 << 20), hash_ctas=self.hash_ctas or (1 << 20),
-                                gap_ms=gaps)
+                                gap_ms=gaps, task_ctas=self.task_ctas)
 
     def begin(self, iteration: int):
         if self.native is None:
@@ -202,7 +206,8 @@ def measure_overhead(step: SyntheticStep, sched: SliceScheduler, steps: int = 8,
         it += 1
     b = statistics.median(base)
     w = statistics.median(with_snap)
-    return {"policy": sched.policy + ("+ce" if sched.copy_engine else ""), "copy_ctas": sched.copy_ctas,
+    return {"policy": sched.policy + ("+ce" if sched.copy_engine else "") + ("+tasks" if sched.task_ctas else ""),
+            "copy_ctas": sched.copy_ctas,
             "measured_gaps_ms": [round(sum(sched.weights), 3), len(sched.weights)] if sched.weights else None,
             "hash_ctas": sched.hash_ctas, "step_ms_without": round(b, 3), "step_ms_with": round(w, 3),
             "overhead_pct": round(100.0 * (w - b) / b, 3), "steps_each": steps,

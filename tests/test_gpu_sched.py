@@ -126,15 +126,17 @@ def _train_ms(train, a, b, reps=1):
     return e0, e1
 
 
-@pytest.mark.parametrize("cap", [32, 0])
-def test_train_waits_at_most_one_state_batch(ffx, cap):
+@pytest.mark.parametrize("cap,tasks", [(32, False), (0, False), (0, True)])
+def test_train_waits_at_most_one_state_batch(ffx, cap, tasks):
     """TRAIN > STATE with bounded inversion (sim_net.cpp:401-454; the pin is
     test_transport.cpp:173-197: a TRAIN chunk queued while a STATE chunk is
     on the wire starts at the next chunk boundary).  Here a STATE batch (one
     fused snapshot batch, low-priority stream, optionally CTA-capped) is
     resident when one full-GPU TRAIN GEMM arrives on the high-priority
     stream: the GEMM's extra time is at most one batch's duration (the batch
-    is never cut; nothing of STATE starts ahead of the queued TRAIN kernel)."""
+    is never cut; nothing of STATE starts ahead of the queued TRAIN kernel).
+    With task-granular batches (task_ctas) the unit of inversion shrinks to
+    one task: TRAIN's CTAs take every SM a finished task frees."""
     spec = ffx.make_spec(d=2, phi=64, distributed=True)
     holder = ffx.Context(0, spec, (0, 0, 0))
     origin = ffx.Context(0, spec, (1, 0, 0))
@@ -152,7 +154,7 @@ def test_train_waits_at_most_one_state_batch(ffx, cap):
     try:
         batches = 4
         # one STATE batch alone
-        origin.snapshot_begin(1, batches=batches, max_ctas=cap)
+        origin.snapshot_begin(1, batches=batches, max_ctas=cap, task_ctas=tasks)
         f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         f0.record(low)
         origin.snapshot_next(stream=low)
@@ -170,7 +172,7 @@ def test_train_waits_at_most_one_state_batch(ffx, cap):
         # batches are issued only after TRAIN finished
         worst = 0.0
         for it in (2, 3, 4):
-            origin.snapshot_begin(it, batches=batches, max_ctas=cap)
+            origin.snapshot_begin(it, batches=batches, max_ctas=cap, task_ctas=tasks)
             origin.snapshot_next(stream=low)
             e0, e1 = _train_ms(train, a, b)
             train.synchronize()
@@ -179,8 +181,8 @@ def test_train_waits_at_most_one_state_batch(ffx, cap):
                 pass
             torch.cuda.synchronize()
         assert rep.newest() == 4
-        print("inversion cap=%d: batch %.3f ms, train alone %.3f ms, worst extra %.3f ms"
-              % (cap, batch_ms, alone, worst))
+        print("inversion cap=%d tasks=%d: batch %.3f ms, train alone %.3f ms, worst extra %.3f ms"
+              % (cap, tasks, batch_ms, alone, worst))
         assert worst <= batch_ms * 1.1 + 0.05, (worst, batch_ms, alone)
     finally:
         torch.cuda.synchronize()

@@ -3,8 +3,8 @@ HBM beside its holder's own 123.5 GB of state; SURVEY 7.2 hard part 3).  The
 replica's slot range is device memory up to hbm_bytes and pinned host memory
 after it, one VA range, so the same kernels snapshot into it and recover from
 it; every byte, the checksum table and the SNP1 frame must be exactly what an
-all-HBM replica holds, with the tier boundary inside the payload, inside a
-region, and (one version) inside the checksum table."""
+all-HBM replica holds -- with the tier boundary inside a region's payload,
+and with no HBM at all (slot metadata and checksum table in host memory)."""
 import pytest
 
 import pyoracle as orc

@@ -39,6 +39,8 @@ def main():
     policy = os.environ.get("POLICY", "fused")
     for cap in [int(x) for x in os.environ.get("CAPS", "16,32,64").split(",")]:
         kw = {"copy_ctas": cap} if policy == "fused" else {"copy_ctas": 8, "hash_ctas": cap, "copy_engine": True}
+        if policy == "fused" and cap == 0:
+            kw = {"copy_ctas": 32, "task_ctas": True}  # cap 0: task-granular batches
         sched = SliceScheduler(R.ctx, step, policy=policy, **kw)
         r = measure_overhead(step, sched, steps=steps, warmup=2, it0=10 + 1000 * cap)
         sched.close()
