@@ -75,7 +75,7 @@ def parse():
                     help="(--impl reference) print only the cpu_baseline object the ffx arm embeds")
     ap.add_argument("--fused-permille", type=int, default=50,
                     help="hybrid mode: share of the warp tasks the fused kernel pushes (the copy engines the rest)")
-    ap.add_argument("--mode", default="push", choices=["push", "pull", "ce", "hybrid", "nccl", "nccl-copy"],
+    ap.add_argument("--mode", default="push", choices=["push", "pull", "ce", "ce-verify", "hybrid", "nccl", "nccl-copy"],
                     help="N>1 ring stream: origin pushes into its successor's replica (fused kernel), the holder "
                          "pulls its predecessor's regions (NeighborBuffer::store side), or ce: copy engines + "
                          "a concurrent checksum kernel (split policy)")
@@ -292,6 +292,13 @@ class Ring:
                     self.ffx.slice_checksums(self.state[0], self.slice_bytes, self.nccl_sums, stream=stream)
                 for r in reqs:
                     r.wait()
+        elif mode == "ce-verify":
+            # copy engines + source checksum, then the HOLDER re-hashes what
+            # landed from its own HBM (checksum-as-landed, ffx_replica_verify)
+            self.snapshot(it, stream, "ce", max_ctas, fused_permille)
+            stream.synchronize()
+            self.dist.barrier()
+            self.ctx.verify_held(self.held, it, stream=stream)
         elif mode in ("ce", "hybrid"):
             # split policy, unscheduled: the copy engines move the bytes on a
             # side stream while the checksum kernel hashes the local state;
@@ -459,7 +466,8 @@ def main():
     alt = None
     if world > 1:
         alt = []
-        for other in [m for m in ("push", "pull", "ce", "hybrid", "nccl", "nccl-copy") if m != args.mode]:
+        for other in [m for m in ("push", "pull", "ce", "ce-verify", "hybrid", "nccl", "nccl-copy")
+                      if m != args.mode]:
             barrier()
             torch.cuda.synchronize()
             for _ in range(2):
@@ -476,6 +484,8 @@ def main():
             ams = max_over_ranks(a0.elapsed_time(a1))
             alt.append({"mode": other, "per_gpu_gbs": round(n * args.steps / (ams * 1e-3) / 1e9, 2),
                         "committed": R.target.newest() == it if not other.startswith("nccl") else None,
+                        **({"holder_verify": "every landed byte re-hashed by the holder (ffx_replica_verify)"}
+                           if other == "ce-verify" else {}),
                         **({"fused_permille": args.fused_permille} if other == "hybrid" else {})})
 
     # ---- recovery: rank (1 % world) loses its state and pulls it back --------

@@ -600,6 +600,17 @@ typedef struct ffx_recover_report {
   double seconds;          /* device time of the gather/verify */
 } ffx_recover_report;
 
+/* Holder: verify a committed slot as landed -- re-hash its payload from the
+ * holder's own HBM against the slot's checksum table (NeighborBuffer::store
+ * validates before accepting, ckpt.cpp:78; storage.cpp:98-99).  For the split
+ * / copy-engine policies, whose table is computed from the origin's source,
+ * this is the check on the bytes that crossed NVLink.  FFX_ECORRUPT with the
+ * first bad slice in rep (the slot is then marked torn and never restored
+ * from); max_ctas caps the launch (0 = whole GPU).  Blocks on stream. */
+int ffx_replica_verify(ffx_ctx* ctx, ffx_replica* held, uint64_t iteration, uint32_t max_ctas, void* stream,
+                       ffx_recover_report* rep);
+
+
 /* Rebuild ctx's unique regions at `target` from a replica (the holder's
  * NeighborBuffer for this role), pulling over NVLink/P2P with fused slice
  * verification.  FFX_ERESTORE: slot missing / stale / torn / wrong role or

@@ -203,6 +203,66 @@ extern "C" int ffx_recover_full(ffx_ctx* c, ffx_replica* const* srcs, uint32_t n
   return FFX_OK;
 }
 
+// NeighborBuffer::store validates a frame before accepting it (ckpt.cpp:78,
+// storage.cpp:98-99).  On the B200 the bytes land first; the holder then
+// re-hashes the committed slot from its own HBM against the slot's table
+// (computed by the origin from its source bytes) -- checksum-as-landed, one
+// local HBM read, no NVLink traffic.  A mismatch drops the slot to WRITING
+// (torn: never restored from) and returns FFX_ECORRUPT with the first slice.
+extern "C" int ffx_replica_verify(ffx_ctx* c, ffx_replica* held, uint64_t iteration, uint32_t max_ctas,
+                                  void* stream, ffx_recover_report* rep) {
+  if (!c || !held) return fail(FFX_EINVAL, "replica_verify: null argument");
+  if (!held->owned) return fail(FFX_EINVAL, "replica_verify: only the holder verifies (its local HBM)");
+  DeviceGuard g(c->device);
+  ffx_recover_report local{};
+  ffx_recover_report& R = rep ? *rep : local;
+  std::memset(&R, 0, sizeof R);
+  R.first_bad_slice = ~0ull;
+  SlotMeta m;
+  const int v = find_slot(held, iteration, &m);
+  if (v == -2) return fail(FFX_ECUDA, "replica_verify: cannot read slot metadata: %s", g_err.c_str());
+  if (v < 0 || m.state != kSlotCommitted)
+    return fail(FFX_ERESTORE, "replica_verify: no committed snapshot at iteration %llu", (unsigned long long)iteration);
+  if (m.num_regions > kMaxRegions) return fail(FFX_ECORRUPT, "replica_verify: %u regions", m.num_regions);
+  SliceJob job{};
+  uint64_t phys = 0;
+  for (uint32_t i = 0; i < m.num_regions; ++i) {
+    job.reg[job.nregions++] = SliceRegion{held->payload(v) + phys, nullptr, m.region_bytes[i], 0, 0};
+    phys = align_up(phys + m.region_bytes[i], kRegionAlign);
+  }
+  job.slice_bytes = m.slice_bytes;
+  job.sums_expected = held->sums(v);
+  job.result = c->result;
+  job.sched = c->done + 12;
+  finalize_job(job, rows_for_cap(max_ctas));
+  cudaStream_t s = as_stream(stream);
+  const unsigned long long init[2] = {~0ull, 0ull};
+  FFX_CUDA(cudaMemcpyAsync(c->result, init, sizeof init, cudaMemcpyHostToDevice, s));
+  FFX_CUDA(cudaEventRecord(c->ev0, s));
+  FFX_CUDA(launch_slices(job, SliceMode::HashVerify, false, max_ctas, s));
+  FFX_CUDA(cudaEventRecord(c->ev1, s));
+  c->stats.kernel_launches++;
+  FFX_CUDA(cudaMemcpyAsync(c->result_host, c->result, 16, cudaMemcpyDeviceToHost, s));
+  FFX_CUDA(cudaStreamSynchronize(s));
+  float ms = 0;
+  cudaEventElapsedTime(&ms, c->ev0, c->ev1);
+  R.seconds = ms * 1e-3;
+  R.bytes = m.payload_len;
+  R.slot = static_cast<uint32_t>(v);
+  R.first_bad_slice = c->result_host[0];
+  R.bad_slices = c->result_host[1];
+  if (R.bad_slices) {
+    c->stats.verify_failures++;
+    const uint32_t torn = kSlotWriting;
+    FFX_CUDA(cudaMemcpy(held->slot(static_cast<uint32_t>(v)) + offsetof(SlotMeta, state), &torn, 4,
+                        cudaMemcpyHostToDevice));
+    held->cache[v].state = kSlotWriting;
+    return fail(FFX_ECORRUPT, "replica_verify: %llu slices differ from the origin's table (first %llu); "
+                "slot %d dropped", (unsigned long long)R.bad_slices, (unsigned long long)R.first_bad_slice, v);
+  }
+  return FFX_OK;
+}
+
 extern "C" int ffx_recover(ffx_ctx* c, ffx_replica* src, uint64_t target, void* stream,
                            ffx_recover_report* rep) {
   if (!c || !src) return fail(FFX_EINVAL, "recover: null argument");

@@ -296,6 +296,7 @@ SIGNATURES = {
     "ffx_snapshot_next": (_I, [_P, _P, _P, ctypes.POINTER(_U32)]),
     "ffx_snapshot_next_kind": (_I, [_P, _I, _P, _P, ctypes.POINTER(_U32)]),
     "ffx_snapshot_read_sums": (_I, [_P, _P, _U64, ctypes.POINTER(_U64), _P]),
+    "ffx_replica_verify": (_I, [_P, _P, _U64, _U32, _P, ctypes.POINTER(RecoverReport)]),
     "ffx_recover": (_I, [_P, _P, _U64, _P, ctypes.POINTER(RecoverReport)]),
     "ffx_recover_full": (_I, [_P, ctypes.POINTER(_P), _U32, _U64, ctypes.POINTER(PeerRegion), _U32, _P,
                               ctypes.POINTER(RecoverReport)]),
@@ -1114,6 +1115,13 @@ class Context:
         check(lib.ffx_snapshot_read_sums(self._c, _ptr(host_tensor), host_tensor.numel(), ctypes.byref(n),
                                          _stream_ptr(stream)), "snapshot_read_sums")
         return n.value
+
+    def verify_held(self, held: Replica, iteration: int, max_ctas: int = 0, stream=None) -> RecoverReport:
+        """Holder-side checksum-as-landed of a committed slot (ffx_replica_verify)."""
+        rep = RecoverReport()
+        check(lib.ffx_replica_verify(self._c, held.ptr, iteration, max_ctas, _stream_ptr(stream),
+                                     ctypes.byref(rep)), "replica_verify")
+        return rep
 
     def recover(self, replica: Replica, target: int, stream=None) -> RecoverReport:
         rep = RecoverReport()

@@ -568,3 +568,31 @@ def test_snapshots_on_two_streams_do_not_overlap(ffx):
     assert rep.export_frame(1) == orc.pack_blob((1, 0, 0), 1, 1, want)
     assert rep.export_frame(2) == orc.pack_blob((1, 0, 0), 2, 1, want)
     del d2
+
+
+@pytest.mark.parametrize("copy_engine", [False, True])
+def test_holder_verifies_landed_bytes(ffx, copy_engine):
+    """Checksum-as-landed on the holder (ffx_replica_verify; NeighborBuffer::
+    store validates before accepting, ckpt.cpp:78): the split / copy-engine
+    policies hash the origin's SOURCE, so a byte damaged after the table was
+    computed is caught only by re-hashing what landed.  The holder re-hashes
+    its committed slot from its own HBM; a flipped byte drops the slot (torn)
+    and recovery then refuses it."""
+    n = 5 * (1 << 20) + 333
+    spec, holder, origin, rep, view = ring_pair(ffx, n)
+    state, want = blob_for(ffx, 1, n)
+    origin.register(ffx.REGION_BLOB, state)
+    origin.snapshot(4, split=True, copy_engine=copy_engine, hash_ctas=32)
+    torch.cuda.synchronize()
+    r = holder.verify_held(rep, 4, max_ctas=16)
+    assert r.bad_slices == 0 and r.bytes == n
+    slot = rep.held()[4]
+    origin.inject(ffx.FAULT_CORRUPT_REPLICA, view, (slot << 48) | 777_777)
+    with pytest.raises(ffx.CorruptSnapshot) as ei:
+        holder.verify_held(rep, 4)
+    assert "first 189" in str(ei.value)  # 777777 // 4096
+    assert 4 not in rep.held()          # dropped: torn
+    with pytest.raises(ffx.RestoreError):
+        origin.recover(view, 4)
+    with pytest.raises(ffx.InvalidArgument):
+        origin.verify_held(view, 4)      # only the holder (its local HBM) verifies
