@@ -65,7 +65,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-llama", action="store_true", help="skip the Llama-3 8B recovery/overhead legs")
-    ap.add_argument("--sched-ctas", type=int, default=32, help="SM budget of scheduled snapshot batches")
+    ap.add_argument("--sched-ctas", type=int, default=16, help="SM budget of scheduled snapshot batches")
     ap.add_argument("--overhead-steps", type=int, default=50, help="interleaved A/B steps per policy (median)")
     ap.add_argument("--no-70b", action="store_true", help="skip the 70B double-neighbour leg (N >= 3)")
     ap.add_argument("--prefix-70b", type=int, default=16 << 30, help="70B state prefix per rank (bytes)")
@@ -1298,16 +1298,22 @@ def llama_leg(args, ffx, torch, dist, world, rank, local, barrier, max_over_rank
                     ("split", {"copy_ctas": 8, "hash_ctas": 96}),
                     ("split", {"copy_ctas": 8, "hash_ctas": 96, "copy_engine": True}),
                     ("split", {"copy_ctas": 8, "hash_ctas": 0, "copy_engine": True}))
-        # designated: the fused kernel policy (the north star's single-kernel
-        # path); the copy-engine split policies are reported beside it
-        designated = 0
+        # designated policy, declared per topology (not the minimum over
+        # policies): N=1 has no collectives to hide behind, so the fused
+        # kernel; N>1 puts the checksum into the SM-idle collective windows and
+        # the bytes on idle copy engines (split+ce).  Both are reported.
+        designated = 0 if world == 1 else 2
         for policy, kw in policies:
             sched = SliceScheduler(R.ctx, step, policy=policy, **kw)
             runs.append(measure_overhead(step, sched, steps=args.overhead_steps, warmup=2,
                                          it0=10 + 1000 * len(runs)))
             sched.close()
-        out["step_overhead"] = dict(runs[designated], headline="designated policy (fused copy+checksum kernel, "
-                                                               "%d-CTA batches in the idle-link gaps)" % args.sched_ctas,
+        out["step_overhead"] = dict(runs[designated],
+                                    headline=("designated policy: fused copy+checksum kernel, %d-CTA batches in the "
+                                              "step's gaps" % args.sched_ctas) if designated == 0 else
+                                             "designated policy: split+ce (checksum kernel in the SM-idle collective "
+                                             "windows, 96 CTAs; copy engines in the idle-link windows)",
+                                    fused_kernel_policy_pct=runs[0]["overhead_pct"],
                                     split_ce_policy_pct=runs[2]["overhead_pct"],
                                     min_over_policies_pct=min(r["overhead_pct"] for r in runs),
                                     all_policies=runs,
