@@ -21,8 +21,10 @@ committed slot records, pulls + verifies them (assemble_restore, ckpt.cpp:
 process-group generation as rank 1.  Worker 0 re-targets its snapshots and
 both continue.  The launcher then runs the same job without the failure and
 prints one JSON line: losses and final parameters must be bit-identical.
-Collectives are gloo on host copies (small model; a dead peer raises instead
-of hanging); the state path is ffx on the GPUs.
+Collectives are gloo on host copies (small model); gloo notices a dead peer
+only at its 10 s collective timeout -- failure detection is the controller's
+job (heartbeats, controller.cpp:46-58) and is not what this times: the spare's
+clock starts at the launcher's notice.  The state path is ffx on the GPUs.
 """
 import argparse
 import datetime
@@ -147,7 +149,7 @@ class Trainer:
 
 def join_group(dist, store, gen, rank, world):
     dist.init_process_group("gloo", init_method="file://" + os.path.join(store, "pg%d" % gen), rank=rank,
-                            world_size=world, timeout=datetime.timedelta(seconds=30))
+                            world_size=world, timeout=datetime.timedelta(seconds=10))
 
 
 # ---------------------------------------------------------------------------
@@ -305,12 +307,14 @@ def launch(args):
                     os.kill(w1.pid, signal.SIGKILL)  # rank 1's process and its GPU state are gone
                     w1.wait()
                     t0 = time.monotonic_ns()         # failure notice
-                    detected = int(get(store, "worker0_detected"))
-                    note = {"rank": 1, "resume": detected, "gen": 1, "t0": t0}
+                    # both ranks committed fail_at (the ledger's global consistent iteration)
+                    note = {"rank": 1, "resume": args.fail_at, "gen": 1, "t0": t0}
                     sp.stdin.write(json.dumps(note) + "\n")
                     sp.stdin.flush()
                     put(store, "new_generation", json.dumps(note).encode())
                     out["spare"] = json.loads(get(store, "spare_report", timeout=300))
+                    out["survivor_detected_after_s"] = round((time.monotonic_ns() - t0) * 1e-9, 2) \
+                        if os.path.exists(os.path.join(store, "worker0_detected")) else None
                     out["killed_after_iteration"] = args.fail_at
                 for p in procs:
                     if p is not w1 or not fail:
