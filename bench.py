@@ -991,7 +991,7 @@ def _restore_failed_rank(ffx, R, plan, peer, w, wbytes, stream, opened):
         index = 1  # registration order: the Adam blob, then the weights
         runs = []
         for _ in range(3):
-            rpt = R.ctx.recover_full([R.target], it, redundant=[(index, pw, ps)], stream=stream)
+            rpt = R.ctx.recover_full([R.target], it, redundant=[(index, pw, ps, R.slice_bytes)], stream=stream)
             runs.append(rpt.seconds)
         ok = (rpt.bad_slices == 0 and ffx.blob_is_sound(R.state[0]) and
               ffx.blob_first_bad(w, wbytes) == ffx.U64_MAX)
@@ -1014,7 +1014,8 @@ def zero1_full_restore(ffx, torch, dist, R, world, rank, local, spec, barrier, s
     from paper_2512_03644_b200 import state
     wbytes = 2 * PHI_GPT2_XL
     wdig = state.weights_init(42, 0, 0)
-    nsl = (wbytes + 4095) // 4096
+    sb = R.slice_bytes
+    nsl = (wbytes + sb - 1) // sb
     ptrs = []
 
     def alloc(nb):
@@ -1032,10 +1033,10 @@ def zero1_full_restore(ffx, torch, dist, R, world, rank, local, spec, barrier, s
             # the live peer's copy of the redundant weights and its slice table
             pw, ps = alloc(wbytes), alloc(nsl * 8)
             ffx.materialize(pw, wdig, wbytes)
-            ffx.slice_checksums(pw, 4096, ps, nbytes=wbytes)
+            ffx.slice_checksums(pw, sb, ps, nbytes=wbytes)
             peers = [(pw, ps)]
         else:
-            ffx.slice_checksums(w, 4096, sums, nbytes=wbytes)  # this rank as a live peer
+            ffx.slice_checksums(w, sb, sums, nbytes=wbytes)  # this rank as a live peer
         torch.cuda.synchronize()
         if world > 1:
             peers = [None] * world

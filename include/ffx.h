@@ -629,11 +629,13 @@ int ffx_recover_from(ffx_ctx* ctx, ffx_replica* const* srcs, uint32_t nsrc, uint
                      ffx_recover_report* report);
 
 /* A redundant region's live copy on a DP peer (weights, ckpt.cpp:150-152):
- * peer-mapped pointer + the peer's slice table (ffx_slice_checksums with this
- * ctx's slice size). */
+ * peer-mapped pointer + the peer's slice table (ffx_slice_checksums).  The
+ * table holds ceil(bytes / slice_bytes) entries; it must have been computed
+ * with this ctx's slice size (FFX_ECONFIG otherwise -- a table cut at another
+ * size would be read past its end). */
 typedef struct ffx_peer_region {
   uint32_t region_index; /* index in this ctx's registration order */
-  uint32_t pad_;
+  uint32_t slice_bytes;  /* slice size of `sums` (0: this ctx's, as before) */
   const void* src;
   const uint64_t* sums;
 } ffx_peer_region;

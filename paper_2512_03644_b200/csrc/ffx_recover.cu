@@ -165,6 +165,9 @@ extern "C" int ffx_recover_full(ffx_ctx* c, ffx_replica* const* srcs, uint32_t n
     if (pr.region_index >= c->regions.size() || c->regions[pr.region_index].unique)
       return fail(FFX_ERANGE, "recover_full: region %u is not a registered redundant region", pr.region_index);
     if (!pr.src || !pr.sums) return fail(FFX_EINVAL, "recover_full: null peer pointer");
+    if (pr.slice_bytes && pr.slice_bytes != c->slice_bytes)
+      return fail(FFX_ECONFIG, "recover_full: region %u's peer table has %u-byte slices, the context %llu",
+                  pr.region_index, pr.slice_bytes, (unsigned long long)c->slice_bytes);
     const Region& reg = c->regions[pr.region_index];
     int st = add(static_cast<const uint8_t*>(pr.src), reg.dev, reg.bytes, pr.sums);
     if (st) return st;

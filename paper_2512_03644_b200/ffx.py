@@ -166,7 +166,7 @@ class RecoverReport(ctypes.Structure):
 
 
 class PeerRegion(ctypes.Structure):
-    _fields_ = [("region_index", ctypes.c_uint32), ("pad_", ctypes.c_uint32),
+    _fields_ = [("region_index", ctypes.c_uint32), ("slice_bytes", ctypes.c_uint32),
                 ("src", ctypes.c_void_p), ("sums", ctypes.c_void_p)]
 
 
@@ -1130,10 +1130,12 @@ class Context:
 
     def recover_full(self, replicas, target: int, redundant=(), stream=None) -> RecoverReport:
         """Full-state restore: unique regions from the replica holders, redundant
-        regions [(region_index, peer_ptr, peer_sums_ptr)] from live peers, one kernel."""
+        regions [(region_index, peer_ptr, peer_sums_ptr[, table_slice_bytes])]
+        from live peers, one kernel."""
         rep = RecoverReport()
         arr = (ctypes.c_void_p * max(1, len(replicas)))(*[r.ptr.value for r in replicas])
-        red = (PeerRegion * max(1, len(redundant)))(*[PeerRegion(i, 0, p, s) for i, p, s in redundant])
+        red = (PeerRegion * max(1, len(redundant)))(*[PeerRegion(e[0], e[3] if len(e) > 3 else 0, e[1], e[2])
+                                                      for e in redundant])
         check(lib.ffx_recover_full(self._c, arr, len(replicas), target, red, len(redundant),
                                    _stream_ptr(stream), ctypes.byref(rep)), "recover_full")
         return rep

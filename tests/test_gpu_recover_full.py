@@ -58,3 +58,37 @@ def test_full_state_restore_from_holder_and_live_peer(ffx):
     # registering the wrong region index is refused
     with pytest.raises(ffx.OutOfRange):
         me.recover_full([view], 3, redundant=[(0, peer_w.data_ptr(), peer_sums.data_ptr())])
+
+
+def test_peer_table_of_another_slice_size_is_refused(ffx):
+    """A live peer's table cut at 4 KiB handed to a 2 KiB context would be
+    read past its end (it has half the entries): the region carries its
+    table's slice size and a mismatch is a ConfigError, not a fault."""
+    spec = ffx.make_spec(d=2, phi=(1 << 20), distributed=True)
+    n_w = 3 * (1 << 20) + 5
+    holder = ffx.Context(0, spec, (0, 0, 0), 2048)
+    me = ffx.Context(0, spec, (1, 0, 0), 2048)
+    opt = torch.empty(1 << 20, dtype=torch.uint8, device="cuda")
+    w = torch.empty(n_w, dtype=torch.uint8, device="cuda")
+    ffx.materialize(opt, orc.optimizer_init(1, 1, 0, 0, True))
+    ffx.materialize(w, orc.weights_init(1, 0, 0))
+    me.register(ffx.REGION_BLOB, opt)
+    me.register(ffx.REGION_PARAMS, w, unique=False)
+    rep = holder.create_replica((1, 0, 0), 1 << 20, 2)
+    view = me.open_replica(rep.export())
+    me.set_target(view)
+    me.snapshot(1)
+    peer_w = w.clone()
+    s4 = torch.empty((n_w + 4095) // 4096, dtype=torch.int64, device="cuda")
+    ffx.slice_checksums(peer_w, 4096, s4)
+    with pytest.raises(ffx.ConfigError):
+        me.recover_full([view], 1, redundant=[(1, peer_w.data_ptr(), s4.data_ptr(), 4096)])
+    s2 = torch.empty((n_w + 2047) // 2048, dtype=torch.int64, device="cuda")
+    ffx.slice_checksums(peer_w, 2048, s2)
+    torch.cuda.synchronize()
+    w.fill_(0)
+    r = me.recover_full([view], 1, redundant=[(1, peer_w.data_ptr(), s2.data_ptr(), 2048)])
+    assert r.bad_slices == 0 and torch.equal(w, peer_w)
+    torch.cuda.synchronize()
+    view.destroy()
+    rep.destroy()
