@@ -649,9 +649,9 @@ int ffx_recover_full(ffx_ctx* ctx, ffx_replica* const* srcs, uint32_t nsrc, uint
 
 /* Pull one redundant region (weights from a live DP peer, ckpt.cpp:150-152)
  * from a peer device pointer, verifying against the peer's slice table
- * (computed by the peer with ffx_slice_checksums). */
-int ffx_recover_region(ffx_ctx* ctx, uint32_t region_index, const void* peer_src,
-                       const uint64_t* peer_sums, void* stream, ffx_recover_report* report);
+ * (computed by the peer with ffx_slice_checksums; same slice-size rule as
+ * ffx_recover_full). */
+int ffx_recover_region(ffx_ctx* ctx, const ffx_peer_region* peer, void* stream, ffx_recover_report* report);
 
 /* Map / unmap a raw device allocation exported by another process (for the
  * redundant-region pull).  handle = cudaIpcMemHandle_t bytes (64). */

@@ -272,10 +272,15 @@ extern "C" int ffx_recover(ffx_ctx* c, ffx_replica* src, uint64_t target, void* 
   return ffx_recover_from(c, &src, 1, target, stream, rep);
 }
 
-extern "C" int ffx_recover_region(ffx_ctx* c, uint32_t idx, const void* peer_src,
-                                  const uint64_t* peer_sums, void* stream, ffx_recover_report* rep) {
-  if (!c || !peer_src || !peer_sums) return fail(FFX_EINVAL, "recover_region: null argument");
+extern "C" int ffx_recover_region(ffx_ctx* c, const ffx_peer_region* peer, void* stream, ffx_recover_report* rep) {
+  if (!c || !peer || !peer->src || !peer->sums) return fail(FFX_EINVAL, "recover_region: null argument");
+  const uint32_t idx = peer->region_index;
+  const void* peer_src = peer->src;
+  const uint64_t* peer_sums = peer->sums;
   if (idx >= c->regions.size()) return fail(FFX_ERANGE, "recover_region: no region %u", idx);
+  if (peer->slice_bytes && peer->slice_bytes != c->slice_bytes)
+    return fail(FFX_ECONFIG, "recover_region: the peer table has %u-byte slices, the context %llu",
+                peer->slice_bytes, (unsigned long long)c->slice_bytes);
   DeviceGuard g(c->device);
   ffx_recover_report local{};
   ffx_recover_report& R = rep ? *rep : local;

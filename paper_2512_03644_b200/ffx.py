@@ -301,7 +301,7 @@ SIGNATURES = {
     "ffx_recover_full": (_I, [_P, ctypes.POINTER(_P), _U32, _U64, ctypes.POINTER(PeerRegion), _U32, _P,
                               ctypes.POINTER(RecoverReport)]),
     "ffx_recover_from": (_I, [_P, ctypes.POINTER(_P), _U32, _U64, _P, ctypes.POINTER(RecoverReport)]),
-    "ffx_recover_region": (_I, [_P, _U32, _P, _P, _P, ctypes.POINTER(RecoverReport)]),
+    "ffx_recover_region": (_I, [_P, ctypes.POINTER(PeerRegion), _P, ctypes.POINTER(RecoverReport)]),
     "ffx_ipc_export": (_I, [_P, _P]),
     "ffx_ipc_open": (_I, [_P, ctypes.POINTER(_P)]),
     "ffx_ipc_close": (_I, [_P]),
@@ -1148,10 +1148,12 @@ class Context:
               "recover_from")
         return rep
 
-    def recover_region(self, index: int, peer_src: int, peer_sums: int, stream=None) -> RecoverReport:
+    def recover_region(self, index: int, peer_src: int, peer_sums: int, stream=None,
+                       slice_bytes: int = 0) -> RecoverReport:
         rep = RecoverReport()
-        check(lib.ffx_recover_region(self._c, index, peer_src, peer_sums, _stream_ptr(stream),
-                                     ctypes.byref(rep)), "recover_region")
+        pr = PeerRegion(index, slice_bytes, peer_src, peer_sums)
+        check(lib.ffx_recover_region(self._c, ctypes.byref(pr), _stream_ptr(stream), ctypes.byref(rep)),
+              "recover_region")
         return rep
 
     def inject(self, fault: int, replica: Optional[Replica] = None, arg: int = 0):
