@@ -606,7 +606,8 @@ typedef struct ffx_recover_report {
  * / copy-engine policies, whose table is computed from the origin's source,
  * this is the check on the bytes that crossed NVLink.  FFX_ECORRUPT with the
  * first bad slice in rep (the slot is then marked torn and never restored
- * from); max_ctas caps the launch (0 = whole GPU).  Blocks on stream. */
+ * from; the writer re-arms with ffx_snapshot_target to reuse it first);
+ * max_ctas caps the launch (0 = whole GPU).  Blocks on stream. */
 int ffx_replica_verify(ffx_ctx* ctx, ffx_replica* held, uint64_t iteration, uint32_t max_ctas, void* stream,
                        ffx_recover_report* rep);
 

@@ -31,7 +31,9 @@ extern "C" int ffx_snapshot_target2(ffx_ctx* c, ffx_replica* t) {
 namespace {
 
 // Two-version rule (ckpt.cpp:46-52, :86-92): replace the slot holding this
-// iteration, else an empty slot, else the oldest.
+// iteration, else a free slot -- empty, or torn (WRITING at rest: a writer
+// that died, or a slot the holder dropped after a failed verify) -- else the
+// oldest committed one.
 uint32_t pick_slot(const ffx_replica* t, uint64_t iteration) {
   int v = -1;
   for (uint32_t i = 0; i < t->versions; ++i)
@@ -39,6 +41,9 @@ uint32_t pick_slot(const ffx_replica* t, uint64_t iteration) {
   if (v < 0)
     for (uint32_t i = 0; i < t->versions && v < 0; ++i)
       if (t->cache[i].state == kSlotEmpty) v = static_cast<int>(i);
+  if (v < 0)
+    for (uint32_t i = 0; i < t->versions && v < 0; ++i)
+      if (t->cache[i].state != kSlotCommitted) v = static_cast<int>(i);
   if (v < 0) {
     v = 0;
     for (uint32_t i = 1; i < t->versions; ++i)

@@ -596,3 +596,12 @@ def test_holder_verifies_landed_bytes(ffx, copy_engine):
         origin.recover(view, 4)
     with pytest.raises(ffx.InvalidArgument):
         origin.verify_held(view, 4)      # only the holder (its local HBM) verifies
+    # the writer re-arms and re-sends: the dropped slot is reused first, so
+    # the other version (3) is never evicted for it
+    origin.snapshot(3, split=True, copy_engine=copy_engine, hash_ctas=32)
+    torch.cuda.synchronize()
+    origin.set_target(view)
+    origin.snapshot(5, split=True, copy_engine=copy_engine, hash_ctas=32)
+    torch.cuda.synchronize()
+    assert sorted(rep.held()) == [3, 5]
+    assert holder.verify_held(rep, 5).bad_slices == 0
