@@ -95,7 +95,7 @@ def check_slot(ffx, rep, slot, stride, allowed):
     return bool((host[mask] == CANARY).all())
 
 
-@pytest.mark.parametrize("mode", ["fused", "batched", "split", "split_ce", "verify", "hybrid"])
+@pytest.mark.parametrize("mode", ["fused", "batched", "tasks", "split", "split_ce", "verify", "hybrid"])
 @pytest.mark.parametrize("misalign", [0, 16])
 def test_snapshot_and_recover_write_only_their_bytes(ffx, mode, misalign):
     sizes = [3 * (1 << 20) + 4099, 16, 200_000 + 3]
@@ -119,7 +119,7 @@ def test_snapshot_and_recover_write_only_their_bytes(ffx, mode, misalign):
                 v.copy_(torch.arange(n, dtype=torch.uint8, device="cuda"))
             origin.register(ffx.REGION_MASTER, v)
         before = src.buf.clone()
-        kw = {"fused": {}, "batched": {"batches": 3, "max_ctas": 8},
+        kw = {"fused": {}, "batched": {"batches": 3, "max_ctas": 8}, "tasks": {"batches": 3, "task_ctas": True},
               "split": {"split": True, "batches": 2, "hash_batches": 2},
               "split_ce": {"split": True, "copy_engine": True, "hash_ctas": 16},
               "verify": {"verify_on_store": True},
