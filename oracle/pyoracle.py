@@ -202,6 +202,23 @@ def ref_lib():
     r.ref_optimizer_init.argtypes = [_u64, ctypes.c_uint16, ctypes.c_uint16, ctypes.c_uint16, ctypes.c_int, _P]
     r.ref_optimizer_at.restype = ctypes.c_int
     r.ref_optimizer_at.argtypes = [_u64] + [ctypes.c_uint16] * 3 + [ctypes.c_uint32] * 4 + [_u64, ctypes.c_int, _P]
+    if hasattr(r, "ref_hs_create"):  # ckpt::HostSnapshots / NeighborBuffer (ckpt.cpp:35-105)
+        u16 = ctypes.c_uint16
+        r.ref_hs_create.restype = _P
+        r.ref_hs_create.argtypes = [u16, u16, u16, _u64]
+        r.ref_hs_free.argtypes = [_P]
+        r.ref_hs_take.argtypes = [_P, _u64, _P, _u64]
+        r.ref_hs_newest.argtypes = [_P, ctypes.POINTER(_u64)]
+        r.ref_hs_previous.argtypes = [_P, ctypes.POINTER(_u64)]
+        r.ref_hs_framed.restype = _u64
+        r.ref_hs_framed.argtypes = [_P, _u64, _P, _u64]
+        r.ref_nb_create.restype = _P
+        r.ref_nb_create.argtypes = [u16, u16, u16]
+        r.ref_nb_free.argtypes = [_P]
+        r.ref_nb_store.argtypes = [_P, _P, _u64]
+        r.ref_nb_newest.argtypes = [_P, ctypes.POINTER(_u64)]
+        r.ref_nb_framed_at.restype = _u64
+        r.ref_nb_framed_at.argtypes = [_P, _u64, _P, _u64]
     if hasattr(r, "ref_hb_create"):  # controller state machines (controller.cpp:16-121, :144-209)
         i64, u32, u16 = ctypes.c_int64, ctypes.c_uint32, ctypes.c_uint16
         r.ref_hb_create.restype = _P

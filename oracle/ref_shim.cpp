@@ -224,6 +224,70 @@ int ref_ring_run(void* h, std::uint64_t iteration, double* secs) {
 }
 
 
+// ---- ckpt::HostSnapshots / ckpt::NeighborBuffer (ckpt.cpp:35-105) ----------
+// Handles onto the reference's two-version containers, for the differential
+// fuzz of the B200 replica semantics (tests/test_gpu_replica_fuzz.py).
+// Return codes: 0 ok, 1 ConfigError, 2 CorruptSnapshot, 3 not held, -1 other.
+
+void* ref_hs_create(std::uint16_t dp, std::uint16_t pp, std::uint16_t tp, std::uint64_t capacity) {
+  return new ckpt::HostSnapshots(Role{dp, pp, tp}, capacity);
+}
+void ref_hs_free(void* h) { delete static_cast<ckpt::HostSnapshots*>(h); }
+int ref_hs_take(void* h, std::uint64_t it, const void* p, std::uint64_t n) {
+  try {
+    static_cast<ckpt::HostSnapshots*>(h)->take(it, p, n);
+    return 0;
+  } catch (const ckpt::ConfigError&) {
+    return 1;
+  } catch (...) {
+    return -1;
+  }
+}
+// newest / previous: 1 and *it set, or 0 when absent
+int ref_hs_newest(void* h, std::uint64_t* it) {
+  const auto v = static_cast<ckpt::HostSnapshots*>(h)->newest();
+  if (v) *it = *v;
+  return v ? 1 : 0;
+}
+int ref_hs_previous(void* h, std::uint64_t* it) {
+  const auto v = static_cast<ckpt::HostSnapshots*>(h)->previous();
+  if (v) *it = *v;
+  return v ? 1 : 0;
+}
+// framed(it): its length (0 when not held); copies up to cap bytes
+std::uint64_t ref_hs_framed(void* h, std::uint64_t it, std::uint8_t* out, std::uint64_t cap) {
+  const auto* f = static_cast<ckpt::HostSnapshots*>(h)->framed(it);
+  if (!f) return 0;
+  std::memcpy(out, f->data(), f->size() < cap ? f->size() : cap);
+  return f->size();
+}
+
+void* ref_nb_create(std::uint16_t dp, std::uint16_t pp, std::uint16_t tp) {
+  return new ckpt::NeighborBuffer(Role{dp, pp, tp});
+}
+void ref_nb_free(void* h) { delete static_cast<ckpt::NeighborBuffer*>(h); }
+int ref_nb_store(void* h, const std::uint8_t* frame, std::uint64_t n) {
+  try {
+    static_cast<ckpt::NeighborBuffer*>(h)->store(std::vector<std::uint8_t>(frame, frame + n));
+    return 0;
+  } catch (const store::CorruptSnapshot&) {
+    return 2;
+  } catch (...) {
+    return -1;
+  }
+}
+int ref_nb_newest(void* h, std::uint64_t* it) {
+  const auto v = static_cast<ckpt::NeighborBuffer*>(h)->newest();
+  if (v) *it = *v;
+  return v ? 1 : 0;
+}
+std::uint64_t ref_nb_framed_at(void* h, std::uint64_t it, std::uint8_t* out, std::uint64_t cap) {
+  const auto* f = static_cast<ckpt::NeighborBuffer*>(h)->framed_at(it);
+  if (!f) return 0;
+  std::memcpy(out, f->data(), f->size() < cap ? f->size() : cap);
+  return f->size();
+}
+
 // ---- the controller's state machines (controller.cpp:16-121, :144-209) -----
 // Thin handles onto ctl::HeartbeatTable / ctl::IterationLedger / plan_recovery
 // for the parity tests of libffx's ffx_heartbeats / ffx_ledger / plan.
