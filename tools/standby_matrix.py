@@ -28,9 +28,9 @@ def run(warm, shared, prealloc, hdev=0, phi=state.PHI_LLAMA3_8B, d=8, role=1):
         common = ["--d", str(d), "--phi", str(phi), "--store", store]
         procs = []
 
-        def spawn(a, dev):
+        def spawn(a, dev, env=None):
             p = subprocess.Popen([EXE] + a + common + ["--device", str(dev)], stdin=subprocess.PIPE,
-                                 stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True)
+                                 stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True, env=env)
             procs.append(p)
             return p
 
@@ -52,8 +52,11 @@ def run(warm, shared, prealloc, hdev=0, phi=state.PHI_LLAMA3_8B, d=8, role=1):
             line(o, "SNAPSHOTTED")
             sb = ["standby", "--role", str(role), "--check", "--target", "2"]
             s = None
+            senv = None
+            if os.environ.get("STANDBY_VISIBLE"):  # e.g. "0": the replacement sees only its own GPU
+                senv = dict(os.environ, CUDA_VISIBLE_DEVICES=os.environ["STANDBY_VISIBLE"])
             if warm:
-                s = spawn(sb + ["--warm"] + (["--prealloc", str(nbytes + 4096)] if prealloc else []), 0)
+                s = spawn(sb + ["--warm"] + (["--prealloc", str(nbytes + 4096)] if prealloc else []), 0, senv)
                 line(s, "ARMED")
             os.kill(o.pid, signal.SIGKILL)
             o.wait()
@@ -62,12 +65,13 @@ def run(warm, shared, prealloc, hdev=0, phi=state.PHI_LLAMA3_8B, d=8, role=1):
                 s.stdin.write("FAIL %d\n" % t0)
                 s.stdin.flush()
             else:
-                s = spawn(sb + ["--t0", str(t0)], 0)
+                s = spawn(sb + ["--t0", str(t0)], 0, senv)
             out, err = s.communicate(timeout=600)
             if s.returncode:
                 return {"error": err[-400:]}
             r = json.loads(out.strip().splitlines()[-1])
-            r.update(shared=shared, prealloc=prealloc, holder_device=hdev)
+            r.update(shared=shared, prealloc=prealloc, holder_device=hdev,
+                     standby_visible=os.environ.get("STANDBY_VISIBLE", "all"))
             return r
         finally:
             for p in procs:
