@@ -68,7 +68,8 @@ struct Args {
   int device = 0, origin = -1, role = -1, holder = -1;
   uint32_t d = 2, versions = 2;
   uint64_t phi = 0, capacity = 0, t0 = 0, slice = 4096, target = 0, prealloc = 0;
-  bool warm = false, check = false, shared = false;
+  bool warm = false, check = false, shared = false, touch = false;
+  int repeat = 0;
 };
 
 Args parse(int argc, char** argv) {
@@ -106,6 +107,8 @@ Args parse(int argc, char** argv) {
     else if (k == "--warm") a.warm = true;
     else if (k == "--check") a.check = true;
     else if (k == "--shared") a.shared = true;
+    else if (k == "--touch") a.touch = true;
+    else if (k == "--repeat") a.repeat = std::atoi(val().c_str());
     else {
       std::fprintf(stderr, "ffx_standby: unknown option %s\n", k.c_str());
       std::exit(2);
@@ -288,6 +291,23 @@ int run_origin(const Args& a) {
   return 0;
 }
 
+// A spare loads the gather/verify kernel before any failure (the first launch
+// in a process pays the module load): one tiny copy + verify.
+void warm_kernels(int device) {
+  const uint64_t n = 1 << 16, s = 4096;
+  void *a = nullptr, *b = nullptr, *sums = nullptr, *res = nullptr;
+  ck(ffx_device_alloc(device, n, &a), "warm alloc");
+  ck(ffx_device_alloc(device, n, &b), "warm alloc");
+  ck(ffx_device_alloc(device, n / s * 8, &sums), "warm alloc");
+  ck(ffx_device_alloc(device, 16, &res), "warm alloc");
+  ck(ffx_expand(a, std::vector<uint8_t>(32, 1).data(), n, nullptr), "warm expand");
+  ck(ffx_slice_checksums(a, n, s, static_cast<uint64_t*>(sums), nullptr), "warm checksums");
+  ck(ffx_copy_verify(b, a, n, s, static_cast<const uint64_t*>(sums), static_cast<uint64_t*>(res), nullptr),
+     "warm copy_verify");
+  ck(ffx_stream_sync(nullptr), "warm sync");
+  for (void* p : {a, b, sums, res}) ffx_device_free(device, p);
+}
+
 // ---- standby (the replacement) ----------------------------------------------
 
 int run_standby(const Args& a) {
@@ -302,7 +322,14 @@ int run_standby(const Args& a) {
     t_ctx_start = now_ns();
     ck(ffx_open(a.device, &spec, me, a.slice, &ctx), "open");
     ck(ffx_prepare_peers(a.device, nullptr), "prepare_peers");
-    if (a.prealloc) ck(ffx_device_alloc(a.device, a.prealloc, &arena), "prealloc");
+    warm_kernels(a.device);
+    if (a.prealloc) {
+      ck(ffx_device_alloc(a.device, a.prealloc, &arena), "prealloc");
+      // --touch: write the arena once while arming, so the restore's stores
+      // meet memory the GPU has already touched
+      if (a.touch) ck(ffx_expand(arena, std::vector<uint8_t>(32, 0).data(), a.prealloc, nullptr), "touch");
+      if (a.touch) ck(ffx_stream_sync(nullptr), "sync");
+    }
     t_ctx = now_ns();
     std::printf("ARMED\n");
     std::fflush(stdout);
@@ -394,6 +421,14 @@ int run_standby(const Args& a) {
   const uint64_t t_done = now_ns();
   if (rst != FFX_OK) die("recover", rst);
 
+  // ---- untimed: the same gather again (warm caches / touched destination) ----
+  std::vector<double> again;
+  for (int k = 0; k < a.repeat; ++k) {
+    ffx_recover_report r2{};
+    ck(ffx_recover(ctx, src, target, nullptr, &r2), "recover (repeat)");
+    again.push_back(r2.seconds * 1e3);
+  }
+
   // ---- untimed checks for the harness -----------------------------------
   int sound = -1;
   if (a.check) {
@@ -426,13 +461,18 @@ int run_standby(const Args& a) {
       "\"time_to_restore_s\": %.6f, \"breakdown_ms\": {\"notice_to_main\": %.3f, \"context\": %.3f, "
       "\"plan\": %.3f, \"ipc_map\": %.3f, \"ipc_open\": %.3f, \"alloc_register\": %.3f, \"gather_verify\": %.3f, "
       "\"gather_verify_kernel\": %.3f}, \"warm_context_ms\": %.3f, \"bad_slices\": %llu, \"verified\": %s, "
-      "\"blob_is_sound\": %d, \"gbs_kernel\": %.1f}\n",
+      "\"blob_is_sound\": %d, \"gbs_kernel\": %.1f, \"repeat_kernel_ms\": [%s]}\n",
       a.warm ? "warm" : "cold", (unsigned long long)target, holder, (unsigned long long)total, n,
       (t_done - t0) * 1e-9, a.warm ? ms(t0, t_notice) : ms(t0, t_main), a.warm ? 0.0 : ms(t_ctx_start, t_ctx),
       ms(a.warm ? t_notice : t_ctx, t_plan), ms(t_plan, t_map), ms(t_plan, t_open), ms(t_map, t_alloc),
       ms(t_alloc, t_done),
       rpt.seconds * 1e3, a.warm ? ms(t_ctx_start, t_ctx) : 0.0, (unsigned long long)rpt.bad_slices,
-      rpt.bad_slices == 0 ? "true" : "false", sound, rpt.seconds > 0 ? total / rpt.seconds / 1e9 : 0.0);
+      rpt.bad_slices == 0 ? "true" : "false", sound, rpt.seconds > 0 ? total / rpt.seconds / 1e9 : 0.0,
+      [&] {
+        std::string j;
+        for (double v : again) j += (j.empty() ? "" : ", ") + std::to_string(v);
+        return j;
+      }().c_str());
   std::fflush(stdout);
   for (void* p : dev)
     if (!arena || p < arena || p >= static_cast<uint8_t*>(arena) + a.prealloc) ffx_device_free(a.device, p);

@@ -55,6 +55,7 @@ def run(warm, shared, prealloc, hdev=0, phi=state.PHI_LLAMA3_8B, d=8, role=1):
             senv = None
             if os.environ.get("STANDBY_VISIBLE"):  # e.g. "0": the replacement sees only its own GPU
                 senv = dict(os.environ, CUDA_VISIBLE_DEVICES=os.environ["STANDBY_VISIBLE"])
+            sb += ["--repeat", "2"] + (["--touch"] if os.environ.get("STANDBY_TOUCH") else [])
             if warm:
                 s = spawn(sb + ["--warm"] + (["--prealloc", str(nbytes + 4096)] if prealloc else []), 0, senv)
                 line(s, "ARMED")
