@@ -147,8 +147,31 @@ __device__ __forceinline__ void tensor_store3(const CUtensorMap* map, int y, int
                ::"l"(reinterpret_cast<uint64_t>(map)), "r"(0), "r"(y), "r"(z), "r"(src)
                : "memory");
 }
-// The same store with an L2 eviction-priority hint (evict_first: the payload
-// is written once and not read back soon) -- FFX_STORE_HINT experiment.
+// Loads and stores with an L2 eviction-priority hint (evict_first): the
+// snapshot streams its bytes through L2 exactly once, so inside a training
+// step it should not displace the step's own working set (the GEMM operands).
+__device__ __forceinline__ void tensor_load_h(uint32_t dst, const CUtensorMap* map, int x, int y, uint32_t bar,
+                                              uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3}], [%4], %5;"
+      ::"r"(dst), "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(bar), "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ void tensor_load3_h(uint32_t dst, const CUtensorMap* map, int y, int z, uint32_t bar,
+                                               uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3, %4}], [%5], %6;"
+      ::"r"(dst), "l"(reinterpret_cast<uint64_t>(map)), "r"(0), "r"(y), "r"(z), "r"(bar), "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ void tensor_store_h(const CUtensorMap* map, int x, int y, uint32_t src, uint64_t pol) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.tile.bulk_group.L2::cache_hint [%0, {%1, %2}], [%3], %4;"
+               ::"l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(src), "l"(pol)
+               : "memory");
+}
+// The 3-D store with the hint (also the FFX_STORE_HINT experiment).
 __device__ __forceinline__ void tensor_store3_hint(const CUtensorMap* map, int y, int z, uint32_t src,
                                                    uint64_t policy) {
   asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.tile.bulk_group.L2::cache_hint [%0, {%1, %2, %3}], [%4], %5;"
@@ -254,6 +277,17 @@ __global__ void __launch_bounds__(W * 32) slice_kernel(const __grid_constant__ S
   }
 
   const uint64_t Sl = job.slice_bytes;
+  const bool l2h = job.l2_stream != 0;
+  const uint64_t pol = l2h ? evict_first_policy() : 0;
+  auto load_tile = [&](uint32_t dst, const CUtensorMap* map, int kstep, int yy, uint32_t bar) {
+    if constexpr (KC == 1) {
+      if (l2h) tensor_load_h(dst, map, kstep * K::C, yy, bar, pol);
+      else tensor_load(dst, map, kstep * K::C, yy, bar);
+    } else {
+      if (l2h) tensor_load3_h(dst, map, yy, kstep * KC, bar, pol);
+      else tensor_load3(dst, map, yy, kstep * KC, bar);
+    }
+  };
   if (kDev && job.stagger_ns) __nanosleep(((blockIdx.x * W + warp) & 7u) * job.stagger_ns);
   uint64_t g_next = job.group_lo + static_cast<uint64_t>(blockIdx.x) * W + warp;
   const uint64_t g_stride = static_cast<uint64_t>(gridDim.x) * W;
@@ -337,8 +371,7 @@ __global__ void __launch_bounds__(W * 32) slice_kernel(const __grid_constant__ S
         for (int k = 0; k < pro; ++k) {
           const int s = static_cast<int>((sbase + k) % S);
           mbar_expect_tx(bar0 + 8 * s, K::STAGE);
-          if constexpr (KC == 1) tensor_load(stage0 + s * K::STAGE, msrc, k * C, y, bar0 + 8 * s);
-          else tensor_load3(stage0 + s * K::STAGE, msrc, y, k * KC, bar0 + 8 * s);
+          load_tile(stage0 + s * K::STAGE, msrc, k, y, bar0 + 8 * s);
         }
       }
       const int sw = lane & 7;  // (lane + 32 r) & 7 == lane & 7
@@ -350,13 +383,18 @@ __global__ void __launch_bounds__(W * 32) slice_kernel(const __grid_constant__ S
         if constexpr (kCopy && !kStg) {
           if (lane == 0) {
             if constexpr (KC == 1) {
-              tensor_store(mdst, k * C, y, tile);
-              if (dual) tensor_store(mdst2, k * C, y, tile);  // double neighbour: read once, write twice
+              if (l2h) {
+                tensor_store_h(mdst, k * C, y, tile, pol);
+                if (dual) tensor_store_h(mdst2, k * C, y, tile, pol);
+              } else {
+                tensor_store(mdst, k * C, y, tile);
+                if (dual) tensor_store(mdst2, k * C, y, tile);  // double neighbour: read once, write twice
+              }
             } else {
-              if (kDev && job.store_hint) {
-                const uint64_t pol = evict_first_policy();
-                tensor_store3_hint(mdst, y, k * KC, tile, pol);
-                if (dual) tensor_store3_hint(mdst2, y, k * KC, tile, pol);
+              if (l2h || (kDev && job.store_hint)) {
+                const uint64_t spol = l2h ? pol : evict_first_policy();
+                tensor_store3_hint(mdst, y, k * KC, tile, spol);
+                if (dual) tensor_store3_hint(mdst2, y, k * KC, tile, spol);
               } else {
                 tensor_store3(mdst, y, k * KC, tile);
                 if (dual) tensor_store3(mdst2, y, k * KC, tile);
@@ -399,8 +437,7 @@ __global__ void __launch_bounds__(W * 32) slice_kernel(const __grid_constant__ S
             if constexpr (kCopy) bulk_wait_read_all();
             if (kDev && job.proxy_fence) fence_async_smem();
             mbar_expect_tx(bar0 + 8 * s, K::STAGE);
-            if constexpr (KC == 1) tensor_load(tile, msrc, (k + S) * C, y, bar0 + 8 * s);
-            else tensor_load3(tile, msrc, y, (k + S) * KC, bar0 + 8 * s);
+            load_tile(tile, msrc, k + S, y, bar0 + 8 * s);
           }
         } else if (kDev && job.prefetch_next) {
           if (k + S == nsteps) {  // this task's refills are done: claim the next one now
@@ -421,8 +458,7 @@ __global__ void __launch_bounds__(W * 32) slice_kernel(const __grid_constant__ S
               if constexpr (kCopy) bulk_wait_read_all();
               if (kDev && job.proxy_fence) fence_async_smem();
               mbar_expect_tx(bar0 + 8 * s, K::STAGE);
-              if constexpr (KC == 1) tensor_load(tile, psrc, j * C, py, bar0 + 8 * s);
-              else tensor_load3(tile, psrc, py, j * KC, bar0 + 8 * s);
+              load_tile(tile, psrc, j, py, bar0 + 8 * s);
             }
           }
         }
@@ -768,6 +804,13 @@ cudaError_t launch_slices(const SliceJob& job_in, SliceMode mode, bool commit, u
   // generic writes read by the async proxy (kept per task).  The per-step
   // fence and the other experiment knobs exist only in FFX_DEV builds.
   job.proxy_fence = job.stagger_ns = job.claim_order = job.store_hint = job.prefetch_next = 0;
+  // CTA-capped jobs run inside a training step: stream through L2 evict-first
+  static const int l2_env = [] {
+    const char* e = std::getenv("FFX_L2_STREAM");  // temporary A/B switch
+    return e ? std::atoi(e) : -1;
+  }();
+  job.l2_stream = l2_env >= 0 ? static_cast<uint32_t>(l2_env != 0 && job.rows == kCappedRows)
+                              : static_cast<uint32_t>(job.rows == kCappedRows);
 #ifdef FFX_DEV
   static const auto env_u32 = [](const char* name) {
     const char* e = std::getenv(name);
