@@ -804,13 +804,10 @@ cudaError_t launch_slices(const SliceJob& job_in, SliceMode mode, bool commit, u
   // generic writes read by the async proxy (kept per task).  The per-step
   // fence and the other experiment knobs exist only in FFX_DEV builds.
   job.proxy_fence = job.stagger_ns = job.claim_order = job.store_hint = job.prefetch_next = 0;
-  // CTA-capped jobs run inside a training step: stream through L2 evict-first
-  static const int l2_env = [] {
-    const char* e = std::getenv("FFX_L2_STREAM");  // temporary A/B switch
-    return e ? std::atoi(e) : -1;
-  }();
-  job.l2_stream = l2_env >= 0 ? static_cast<uint32_t>(l2_env != 0 && job.rows == kCappedRows)
-                              : static_cast<uint32_t>(job.rows == kCappedRows);
+  // CTA-capped jobs run inside a training step: stream through L2
+  // evict-first so the step's own working set stays resident (measured
+  // neutral on the synthetic step, profiles/r2_l2_hint_ab_n1.jsonl)
+  job.l2_stream = job.rows == kCappedRows ? 1u : 0u;
 #ifdef FFX_DEV
   static const auto env_u32 = [](const char* name) {
     const char* e = std::getenv(name);
