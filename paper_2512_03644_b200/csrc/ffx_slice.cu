@@ -598,7 +598,9 @@ constexpr Variant kVariants[] = {{3, 4, 1, 0, 2}, {2, 4, 2, 0, 1}, {3, 4, 2, 0, 
                                  {2, 8, 1, 0, 2}, {2, 4, 1, 0, 1},
                                  // 14-16: small enough (< 18 KB smem, 64 threads) to sit beside a
                                  // 213 KB / 256-thread cuBLAS GEMM CTA on the same SM
-                                 {2, 2, 1, 0, 1}, {3, 1, 1, 0, 1}, {2, 1, 1, 0, 2}};
+                                 {2, 2, 1, 0, 1}, {3, 1, 1, 0, 1}, {2, 1, 1, 0, 2},
+                                 // 17-18: wide single CTAs (more FNV chains per SM for narrow batches)
+                                 {2, 12, 2, 0, 1}, {2, 16, 1, 0, 1}};
 constexpr int kHashDefault = 9;
 int variant() {
   static const int v = [] {
@@ -648,6 +650,8 @@ cudaError_t launch_mode(const SliceJob& job, uint32_t max_ctas, cudaStream_t str
     case 14: return launch_t<2, 2, 1, false, M, kCommit>(job, max_ctas, stream);
     case 15: return launch_t<3, 1, 1, false, M, kCommit>(job, max_ctas, stream);
     case 16: return launch_t<2, 1, 1, false, M, kCommit, 2>(job, max_ctas, stream);
+    case 17: return launch_t<2, 12, 2, false, M, kCommit>(job, max_ctas, stream);
+    case 18: return launch_t<2, 16, 1, false, M, kCommit>(job, max_ctas, stream);
     default: return launch_t<3, 4, 1, false, M, kCommit, 2>(job, max_ctas, stream);
   }
 #else
