@@ -370,10 +370,43 @@ def free_port():
         return so.getsockname()[1]
 
 
+def cpu_baseline_native(threads, per, iters=4):
+    """The reference's own CPU path (take + store on every host thread) timed
+    by oracle/_ref/ref_bench, a native executable over the reference library:
+    no Python process of the GPU run maps the reference or the oracle."""
+    exe = os.path.join(ROOT, "oracle", "_ref", "ref_bench")
+    if not os.path.exists(exe):
+        return None
+    p = subprocess.run([exe, str(threads), str(per), str(iters)], capture_output=True, text=True, timeout=600)
+    if p.returncode != 0:
+        return {"error": p.stderr[-300:]}
+    r = json.loads(p.stdout.strip().splitlines()[-1])
+    agg = threads * per
+    return {
+        "value": round(agg / r["snapshot_s"] / 1e9, 3), "unit": "GB/s", "cores": threads, "kind": "reference",
+        "sample": "%d threads x %d MiB per rank x %d iterations (median of the slowest thread's take + store): "
+                  "HostSnapshots::take + NeighborBuffer::store (the snapshot); reference proj/src compiled -O3 "
+                  "into oracle/_ref, timed by oracle/_ref/ref_bench" % (threads, per >> 20, iters),
+        "same_config": False,
+        "sample_vs_config": "a 256 MiB per-thread sample of the %d-byte shard (the metric is GB/s)" %
+                            ((12 * PHI_GPT2_XL + D_REF - 1) // D_REF),
+        "stages_gbs": {"take": round(agg / r["take_s"] / 1e9, 3), "store": round(agg / r["store_s"] / 1e9, 3),
+                       "restore": round(agg / r["restore_s"] / 1e9, 3)},
+        "nproc": os.cpu_count(), "cpu_model": cpu_model(),
+    }
+
+
 def cpu_baseline_subprocess(args):
-    """The reference's CPU path timed in a child process (bench.py --impl
-    reference --baseline-line), so the measured process never maps the
-    reference / oracle libraries."""
+    """The reference's CPU path timed in a child process -- the native
+    oracle/_ref/ref_bench when built, else bench.py --impl reference
+    --baseline-line -- so the measured process never maps the reference /
+    oracle libraries."""
+    try:
+        native = cpu_baseline_native(os.cpu_count() or 1, 256 << 20)
+        if native is not None:
+            return native
+    except Exception as ex:  # fall back to the Python child
+        native = {"error": repr(ex)}
     env = {k: v for k, v in os.environ.items()
            if k not in ("RANK", "LOCAL_RANK", "WORLD_SIZE", "LOCAL_WORLD_SIZE", "GROUP_RANK")}
     try:
