@@ -1337,10 +1337,11 @@ def llama_leg(args, ffx, torch, dist, world, rank, local, barrier, max_over_rank
         # kernel; N>1 puts the checksum into the SM-idle collective windows and
         # the bytes on idle copy engines (split+ce).  Both are reported.
         designated = 0 if world == 1 else 2
-        for policy, kw in policies:
+        for i, (policy, kw) in enumerate(policies):
             sched = SliceScheduler(R.ctx, step, policy=policy, **kw)
-            runs.append(measure_overhead(step, sched, steps=args.overhead_steps, warmup=2,
-                                         it0=10 + 1000 * len(runs)))
+            # the designated policy gets twice the A/B steps: its median is the headline
+            runs.append(measure_overhead(step, sched, steps=args.overhead_steps * (2 if i == designated else 1),
+                                         warmup=2, it0=10 + 1000 * len(runs)))
             sched.close()
         out["step_overhead"] = dict(runs[designated],
                                     headline=("designated policy: fused copy+checksum kernel, %d-CTA batches in the "
