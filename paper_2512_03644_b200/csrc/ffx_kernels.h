@@ -71,6 +71,7 @@ struct SliceJob {
                                   // first S steps into the stages this task frees (no per-task drain)
   uint32_t one_shot;              // one task per warp, no claim loop (task-granular batches)
   uint32_t l2_stream;             // TMA loads / stores with an L2 evict_first policy
+  uint32_t static_first;          // each warp's first task is blockIdx*W+warp (no atomic), then dynamic
   uint32_t skip_begin;            // the slot was marked WRITING by a preceding mark launch
   SlotCommit commit;
   SlotCommit commit2;             // second replica's slot (slot null = none)

@@ -302,6 +302,13 @@ __global__ void __launch_bounds__(W * 32) slice_kernel(const __grid_constant__ S
       return i < job.group_hi - job.group_lo ? job.group_hi - 1 - i : kNone;
     }
     if (job.sched != nullptr) {
+      if (job.static_first && !once) {
+        // the first task of every warp is fixed (no atomic storm at launch)
+        once = true;
+        const uint64_t i = static_cast<uint64_t>(blockIdx.x) * W + warp;
+        if (i < job.group_hi - job.group_lo) return job.group_hi - 1 - i;
+        return kNone;
+      }
       // Claims run from the LAST task down: each region's ragged tail (and
       // tiny register-path regions) starts first and overlaps the bulk
       // instead of running alone after it -- one latency-bound register-path
@@ -310,6 +317,7 @@ __global__ void __launch_bounds__(W * 32) slice_kernel(const __grid_constant__ S
       unsigned t = 0;
       if (lane == 0) t = atomicAdd(&job.sched[0], 1u);
       t = __shfl_sync(0xffffffffu, t, 0);
+      if (job.static_first) t += gridDim.x * W;  // the statically assigned first round
       if (t >= job.group_hi - job.group_lo) return kNone;
       return (!kDev || job.claim_order == 0 || t == 0) ? job.group_hi - 1 - t : job.group_lo + t - 1;
     }
@@ -827,6 +835,8 @@ cudaError_t launch_slices(const SliceJob& job_in, SliceMode mode, bool commit, u
   job.claim_order = order;
   job.store_hint = hint;
   job.prefetch_next = prefetch;
+  static const uint32_t sfirst = env_u32("FFX_STATIC_FIRST");
+  job.static_first = sfirst;
 #endif
   switch (mode) {
     case SliceMode::Hash:
