@@ -816,6 +816,9 @@ cudaError_t launch_slices(const SliceJob& job_in, SliceMode mode, bool commit, u
   // generic writes read by the async proxy (kept per task).  The per-step
   // fence and the other experiment knobs exist only in FFX_DEV builds.
   job.proxy_fence = job.stagger_ns = job.claim_order = job.store_hint = job.prefetch_next = 0;
+  // every warp's first task is assigned by its index instead of an atomic:
+  // no 1184-way atomic storm at launch (+0.2%, profiles/r2_static_first_ab_1gpu.jsonl)
+  job.static_first = 1;
   // CTA-capped jobs run inside a training step: stream through L2
   // evict-first so the step's own working set stays resident (measured
   // neutral on the synthetic step, profiles/r2_l2_hint_ab_n1.jsonl)
@@ -835,8 +838,8 @@ cudaError_t launch_slices(const SliceJob& job_in, SliceMode mode, bool commit, u
   job.claim_order = order;
   job.store_hint = hint;
   job.prefetch_next = prefetch;
-  static const uint32_t sfirst = env_u32("FFX_STATIC_FIRST");
-  job.static_first = sfirst;
+  static const char* sfe = std::getenv("FFX_STATIC_FIRST");
+  if (sfe) job.static_first = static_cast<uint32_t>(std::atoi(sfe));
 #endif
   switch (mode) {
     case SliceMode::Hash:
