@@ -20,9 +20,18 @@
 //   ragged task (region tail, unaligned pointers) -- register path: 16-byte
 //     loads / stores and a padded shared-memory transpose.
 //
-// Tasks are handed out dynamically (one atomic per task), last task first,
-// so the latency-bound ragged tails overlap the bulk and the last wave does
-// not idle SMs.
+// Tasks are handed out last task first -- each warp's first task by its
+// index, the rest dynamically (one atomic per task) -- so the latency-bound
+// ragged tails overlap the bulk and the last wave does not idle SMs.
+// Task-granular launches (one_shot) instead give every warp exactly one task
+// and exit, so a low-priority batch yields SMs at every task boundary.
+//
+// Two configurations ship (launch_mode): the bulk one (32-slice tasks, one
+// FNV chain per lane, 4 warps, 98 KB) for full-GPU launches, and an SM-lean
+// one (64-slice tasks, two chains per lane, 8 warps, 130 KB) for CTA-capped
+// scheduler batches inside a training step, which also stream their TMA
+// traffic through L2 evict-first.  The round-1 tuning table and its env
+// knobs exist only in FFX_DEV builds.
 #include <cuda_runtime.h>
 
 #include <algorithm>
