@@ -20,7 +20,7 @@ struct SliceRegion {
   uint64_t slice_base;   // first checksum-table index of this region
   uint64_t group_base;   // first 32-slice warp task of this region
   int32_t tmap;          // index of this region's src/dst tensor-map pair, -1 = none
-  uint32_t pad_;
+  uint32_t slice_bytes;  // this region's slice size (0 = the job's)
   uint64_t nfull;        // full-length slices (the tensor maps' outer extent)
   uint8_t* dst2;         // second replica (double-neighbour), null = none
   const uint64_t* expected;  // verify: this region's own table (region-local index), else the job's

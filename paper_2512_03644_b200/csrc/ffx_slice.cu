@@ -285,7 +285,6 @@ __global__ void __launch_bounds__(W * 32) slice_kernel(const __grid_constant__ S
     }
   }
 
-  const uint64_t Sl = job.slice_bytes;
   const bool l2h = job.l2_stream != 0;
   const uint64_t pol = l2h ? evict_first_policy() : 0;
   auto load_tile = [&](uint32_t dst, const CUtensorMap* map, int kstep, int yy, uint32_t bar) {
@@ -354,6 +353,7 @@ __global__ void __launch_bounds__(W * 32) slice_kernel(const __grid_constant__ S
     bool claimed = false, pf_ok = false;
 
     const SliceRegion R = region_of(g);
+    const uint64_t Sl = R.slice_bytes ? R.slice_bytes : job.slice_bytes;
     const bool al = aligned16(R.src) && (!kCopy || aligned16(R.dst));
     const uint64_t s0 = (g - R.group_base) * K::ROWS;
 
@@ -729,7 +729,8 @@ void finalize_job(SliceJob& job, uint32_t rows_in) {
   const uint64_t rows = job.rows;
   uint64_t groups = 0, slices = 0;
   for (uint32_t r = 0; r < job.nregions; ++r) {
-    const uint64_t ns = (job.reg[r].bytes + job.slice_bytes - 1) / job.slice_bytes;
+    const uint64_t S = job.reg[r].slice_bytes ? job.reg[r].slice_bytes : job.slice_bytes;
+    const uint64_t ns = (job.reg[r].bytes + S - 1) / S;
     job.reg[r].slice_base = slices;
     job.reg[r].group_base = groups;
     slices += ns;
@@ -785,22 +786,23 @@ bool encode_rows(CUtensorMap* map, const void* base, uint64_t slice_bytes, uint6
 // Give the (up to kTmaRegions) largest eligible regions 2-D tensor maps.
 void attach_tensor_maps(SliceJob& job, bool copy, int kc_planes) {
   for (uint32_t r = 0; r < kMaxRegions; ++r) job.reg[r].tmap = -1;
-  if (job.slice_bytes % 128 != 0 || job.slice_bytes > (1ull << 31)) return;
   int used = 0;
   for (uint32_t r = 0; r < job.nregions && used < kTmaRegions; ++r) {
     SliceRegion& R = job.reg[r];
-    R.nfull = R.bytes / job.slice_bytes;
+    const uint64_t S = R.slice_bytes ? R.slice_bytes : job.slice_bytes;
+    if (S % 128 != 0 || S > (1ull << 31)) continue;
+    R.nfull = R.bytes / S;
     const bool al = (reinterpret_cast<uintptr_t>(R.src) % 16 == 0) &&
                     (!copy || reinterpret_cast<uintptr_t>(R.dst) % 16 == 0);
     const uint32_t rows = job.rows;
     if (!al || R.nfull < rows || R.nfull > (1ull << 31)) continue;
     if (R.dst2 != nullptr && reinterpret_cast<uintptr_t>(R.dst2) % 16 != 0) continue;
     const uint32_t kc = static_cast<uint32_t>(kc_planes);
-    if (job.slice_bytes % (128ull * kc) != 0) continue;
-    if (!encode_rows(&job.maps[3 * used], R.src, job.slice_bytes, R.nfull, rows, kc)) continue;
-    if (copy && !encode_rows(&job.maps[3 * used + 1], R.dst, job.slice_bytes, R.nfull, rows, kc)) continue;
+    if (S % (128ull * kc) != 0) continue;
+    if (!encode_rows(&job.maps[3 * used], R.src, S, R.nfull, rows, kc)) continue;
+    if (copy && !encode_rows(&job.maps[3 * used + 1], R.dst, S, R.nfull, rows, kc)) continue;
     if (copy && R.dst2 != nullptr &&
-        !encode_rows(&job.maps[3 * used + 2], R.dst2, job.slice_bytes, R.nfull, rows, kc))
+        !encode_rows(&job.maps[3 * used + 2], R.dst2, S, R.nfull, rows, kc))
       continue;
     R.tmap = used++;
   }

@@ -120,6 +120,25 @@ int begin_impl(ffx_ctx* c, ffx_replica* t, ffx_replica* t2, const std::vector<Sr
   for (size_t i = 0; i < srcs.size(); ++i)
     job.reg[i] = SliceRegion{srcs[i].dev, t->wpayload(slot) + offs[i], srcs[i].bytes, 0, 0};
   job.slice_bytes = c->slice_bytes;
+#ifdef FFX_DEV
+  // timing prototype (FFX_HEAD_SPLIT=bytes, FFX_HEAD_SLICE=bytes): the head
+  // of region 0 -- the tasks claimed last -- in smaller slices.  The table
+  // layout then differs from what recovery expects: measurement only.
+  if (const char* hs = std::getenv("FFX_HEAD_SPLIT")) {
+    const uint64_t head = std::strtoull(hs, nullptr, 10);
+    const char* hsl = std::getenv("FFX_HEAD_SLICE");
+    const uint32_t small = hsl ? static_cast<uint32_t>(std::atoi(hsl)) : 1024u;
+    if (head && job.nregions < kMaxRegions && job.reg[0].bytes > 2 * head) {
+      for (uint32_t i = job.nregions; i > 0; --i) job.reg[i] = job.reg[i - 1];
+      job.reg[0].bytes = head;
+      job.reg[0].slice_bytes = small;
+      job.reg[1].src += head;
+      job.reg[1].dst += head;
+      job.reg[1].bytes -= head;
+      ++job.nregions;
+    }
+  }
+#endif
   job.sums_out = t->wsums(slot);
   job.sched = c->done + 8;  // dynamic task counter (words 8-9 of the ctx scratch)
   // CTA-capped snapshots (scheduler batches inside a step) use the SM-lean
