@@ -280,6 +280,23 @@ typedef struct ffx_plan_info {
 } ffx_plan_info;
 int ffx_plan(ffx_ctx* ctx, ffx_plan_info* out);
 
+/* How a snapshot's payload is cut into checksum slices (the checksum table
+ * order).  Every region is one run of slice_bytes slices, except that the
+ * first region of a payload of fewer than FFX_MAX_REGIONS regions, when it
+ * holds at least 4 x 48 MiB and slice_bytes is a multiple of 1 KiB, opens
+ * with a 48 MiB head of slice_bytes/4 slices: the tasks claimed last by the
+ * persistent snapshot kernel are then short, which trims its tail.  Writes
+ * up to `cap` runs and their count (<= n + 1). */
+typedef struct ffx_slice_run {
+  uint32_t region;      /* index into region_bytes */
+  uint32_t slice_bytes; /* slice size of this run */
+  uint64_t offset;      /* byte offset of the run inside its region */
+  uint64_t bytes;
+  uint64_t first_slice; /* checksum-table index of the run's first slice */
+} ffx_slice_run;
+int ffx_slice_runs(const uint64_t* region_bytes, uint32_t n, uint64_t slice_bytes, ffx_slice_run* out,
+                   uint32_t cap, uint32_t* count);
+
 /* ---- neighbour replica manager (NeighborBuffer, ckpt.hpp:105-120) --------- */
 
 /* Holder side: device slots for `origin`'s snapshots, `versions` of them

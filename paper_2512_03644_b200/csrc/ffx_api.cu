@@ -555,21 +555,42 @@ extern "C" int ffx_clear_regions(ffx_ctx* c) {
   return FFX_OK;
 }
 
+extern "C" int ffx_slice_runs(const uint64_t* region_bytes, uint32_t n, uint64_t slice_bytes, ffx_slice_run* out,
+                              uint32_t cap, uint32_t* count) {
+  if ((n && !region_bytes) || !count || (cap && !out)) return fail(FFX_EINVAL, "slice_runs: null argument");
+  if (!slice_ok(slice_bytes)) return fail(FFX_EINVAL, "slice_runs: bad slice size %llu", (unsigned long long)slice_bytes);
+  uint32_t k = 0;
+  uint64_t first = 0;
+  for (uint32_t i = 0; i < n; ++i) {
+    SliceRun runs[2];
+    const int m = region_runs(region_bytes[i], slice_bytes, head_region(i, n), runs);
+    for (int j = 0; j < m; ++j, ++k) {
+      if (k < cap)
+        out[k] = ffx_slice_run{i, static_cast<uint32_t>(runs[j].slice), runs[j].offset, runs[j].bytes, first};
+      first += run_slices(runs[j]);
+    }
+  }
+  *count = k;
+  return k <= cap ? FFX_OK : fail(FFX_EINVAL, "slice_runs: %u runs, room for %u", k, cap);
+}
+
 extern "C" int ffx_plan(ffx_ctx* c, ffx_plan_info* out) {
   if (!c || !out) return fail(FFX_EINVAL, "plan: null argument");
   std::memset(out, 0, sizeof *out);
   ffx_razor(&c->spec, &out->razor);
   out->slice_bytes = c->slice_bytes;
   out->num_regions = static_cast<uint32_t>(c->regions.size());
+  std::vector<uint64_t> unique;  // payload regions, in payload order
   for (const auto& r : c->regions) {
     if (r.unique) {
       out->registered_unique_bytes += r.bytes;
-      out->num_slices += slices_of(r.bytes, c->slice_bytes);
+      unique.push_back(r.bytes);
       out->num_unique_regions++;
     } else {
       out->registered_redundant_bytes += r.bytes;
     }
   }
+  out->num_slices = table_entries(unique.data(), static_cast<uint32_t>(unique.size()), c->slice_bytes);
   return FFX_OK;
 }
 

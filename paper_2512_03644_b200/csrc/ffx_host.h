@@ -247,6 +247,21 @@ struct PayloadMap {
   uint64_t physical = 0;
 };
 PayloadMap payload_map(const ffx_ctx* c);
+// The slice runs of a payload map in table order (ffx_layout.h).
+struct RunRef {
+  uint32_t region;  // index into PayloadMap::regs
+  SliceRun run;
+};
+inline std::vector<RunRef> payload_runs(const PayloadMap& pm, uint64_t S) {
+  std::vector<RunRef> out;
+  const uint32_t n = static_cast<uint32_t>(pm.regs.size());
+  for (uint32_t r = 0; r < n; ++r) {
+    SliceRun runs[2];
+    const int k = region_runs(pm.regs[r]->bytes, S, head_region(r, n), runs);
+    for (int j = 0; j < k; ++j) out.push_back(RunRef{r, runs[j]});
+  }
+  return out;
+}
 
 int read_meta(ffx_replica* r, uint32_t v, SlotMeta* m);
 int refresh_cache(ffx_replica* r);

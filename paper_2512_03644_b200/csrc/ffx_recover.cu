@@ -61,23 +61,26 @@ extern "C" int ffx_recover_from(ffx_ctx* c, ffx_replica* const* srcs, uint32_t n
   }
   R.slot = slot[0];
   const PayloadMap pm = payload_map(c);
-  if (pm.regs.size() * nsrc > kMaxRegions) nsrc = 1;  // not enough region entries to split
   const uint64_t S = m[0].slice_bytes;
+  const std::vector<RunRef> runs = payload_runs(pm, S);
+  if (runs.size() * nsrc > kMaxRegions) nsrc = 1;  // not enough region entries to split
 
-  // Parallel peer gathers: region r's slices are cut into nsrc consecutive
-  // parts, part i pulled from source i.  Sub-regions keep registration
+  // Parallel peer gathers: every slice run (ffx_layout.h) is cut into nsrc
+  // consecutive parts, part i pulled from source i.  Parts keep payload
   // order, so the global slice numbering (and the checksum table) is that
   // of the whole snapshot; every part verifies against source 0's table.
   cudaStream_t s = as_stream(stream);
   SliceJob job{};
-  for (size_t r = 0; r < pm.regs.size(); ++r) {
-    const uint64_t ns = slices_of(pm.regs[r]->bytes, S);
+  for (const RunRef& q : runs) {
+    const uint64_t ns = run_slices(q.run);
     for (uint32_t i = 0; i < nsrc; ++i) {
       const uint64_t a = ns * i / nsrc, b = ns * (i + 1) / nsrc;
-      const uint64_t lo = a * S, hi = std::min(b * S, pm.regs[r]->bytes);
+      const uint64_t lo = q.run.offset + a * q.run.slice;
+      const uint64_t hi = std::min(q.run.offset + b * q.run.slice, q.run.offset + q.run.bytes);
       if (hi <= lo && !(nsrc == 1)) continue;
-      job.reg[job.nregions++] =
-          SliceRegion{srcs[i]->payload(slot[i]) + pm.offs[r] + lo, pm.regs[r]->dev + lo, hi - lo, 0, 0};
+      SliceRegion part{srcs[i]->payload(slot[i]) + pm.offs[q.region] + lo, pm.regs[q.region]->dev + lo, hi - lo, 0, 0};
+      part.slice_bytes = static_cast<uint32_t>(q.run.slice);
+      job.reg[job.nregions++] = part;
     }
   }
   job.slice_bytes = S;
@@ -138,27 +141,28 @@ extern "C" int ffx_recover_full(ffx_ctx* c, ffx_replica* const* srcs, uint32_t n
   // replica holders, each redundant region from its live DP peer (weights,
   // ckpt.cpp:150-152), each part verified against its own source's table.
   SliceJob job{};
-  auto add = [&](const uint8_t* src, uint8_t* dst, uint64_t bytes, const uint64_t* expected) -> int {
+  auto add = [&](const uint8_t* src, uint8_t* dst, uint64_t bytes, const uint64_t* expected, uint64_t slice) -> int {
     if (job.nregions >= kMaxRegions) return fail(FFX_ECONFIG, "recover_full: more than %u parts", kMaxRegions);
     SliceRegion sr{src, dst, bytes, 0, 0};
     sr.expected = expected;
+    sr.slice_bytes = static_cast<uint32_t>(slice);
     job.reg[job.nregions++] = sr;
     return FFX_OK;
   };
-  uint64_t total = 0;
-  for (size_t r = 0; r < pm.regs.size(); ++r) {
-    const uint64_t ns = slices_of(pm.regs[r]->bytes, S);
-    const uint64_t base = std::accumulate(pm.regs.begin(), pm.regs.begin() + r, uint64_t{0},
-                                          [&](uint64_t a, const Region* q) { return a + slices_of(q->bytes, S); });
+  uint64_t total = 0, base = 0;  // base: table entries of the runs before this one
+  for (const RunRef& q : payload_runs(pm, S)) {
+    const uint64_t ns = run_slices(q.run);
     for (uint32_t i = 0; i < nsrc; ++i) {
       const uint64_t a = ns * i / nsrc, b = ns * (i + 1) / nsrc;
-      const uint64_t lo = a * S, hi = std::min(b * S, pm.regs[r]->bytes);
+      const uint64_t lo = q.run.offset + a * q.run.slice;
+      const uint64_t hi = std::min(q.run.offset + b * q.run.slice, q.run.offset + q.run.bytes);
       if (hi <= lo) continue;
-      int st = add(srcs[i]->payload(slot[i]) + pm.offs[r] + lo, pm.regs[r]->dev + lo, hi - lo,
-                   srcs[i]->sums(slot[i]) + base + a);
+      int st = add(srcs[i]->payload(slot[i]) + pm.offs[q.region] + lo, pm.regs[q.region]->dev + lo, hi - lo,
+                   srcs[i]->sums(slot[i]) + base + a, q.run.slice);
       if (st) return st;
     }
-    total += pm.regs[r]->bytes;
+    base += ns;
+    total += q.run.bytes;
   }
   for (uint32_t j = 0; j < nred; ++j) {
     const ffx_peer_region& pr = redundant[j];
@@ -169,7 +173,7 @@ extern "C" int ffx_recover_full(ffx_ctx* c, ffx_replica* const* srcs, uint32_t n
       return fail(FFX_ECONFIG, "recover_full: region %u's peer table has %u-byte slices, the context %llu",
                   pr.region_index, pr.slice_bytes, (unsigned long long)c->slice_bytes);
     const Region& reg = c->regions[pr.region_index];
-    int st = add(static_cast<const uint8_t*>(pr.src), reg.dev, reg.bytes, pr.sums);
+    int st = add(static_cast<const uint8_t*>(pr.src), reg.dev, reg.bytes, pr.sums, S);  // peer tables: uniform
     if (st) return st;
     total += reg.bytes;
   }
@@ -230,7 +234,13 @@ extern "C" int ffx_replica_verify(ffx_ctx* c, ffx_replica* held, uint64_t iterat
   SliceJob job{};
   uint64_t phys = 0;
   for (uint32_t i = 0; i < m.num_regions; ++i) {
-    job.reg[job.nregions++] = SliceRegion{held->payload(v) + phys, nullptr, m.region_bytes[i], 0, 0};
+    SliceRun runs[2];
+    const int k = region_runs(m.region_bytes[i], m.slice_bytes, head_region(i, m.num_regions), runs);
+    for (int j = 0; j < k; ++j) {
+      SliceRegion R{held->payload(v) + phys + runs[j].offset, nullptr, runs[j].bytes, 0, 0};
+      R.slice_bytes = static_cast<uint32_t>(runs[j].slice);
+      job.reg[job.nregions++] = R;
+    }
     phys = align_up(phys + m.region_bytes[i], kRegionAlign);
   }
   job.slice_bytes = m.slice_bytes;

@@ -73,14 +73,15 @@ int begin_impl(ffx_ctx* c, ffx_replica* t, ffx_replica* t2, const std::vector<Sr
   if (srcs.size() > kMaxRegions) return fail(FFX_ECONFIG, "at most %u regions", kMaxRegions);
   ffx_snapshot_opts opts{};
   if (o) opts = *o;
-  uint64_t logical = 0, physical = 0, nslices = 0;
-  std::vector<uint64_t> offs;
+  uint64_t logical = 0, physical = 0;
+  std::vector<uint64_t> offs, sizes;
   for (const SrcRegion& r : srcs) {
     offs.push_back(physical);
+    sizes.push_back(r.bytes);
     logical += r.bytes;
     physical = align_up(physical + r.bytes, kRegionAlign);
-    nslices += slices_of(r.bytes, c->slice_bytes);
   }
+  const uint64_t nslices = table_entries(sizes.data(), static_cast<uint32_t>(sizes.size()), c->slice_bytes);
   for (ffx_replica* rr : {t, t2}) {
     if (!rr) continue;
     if (logical > rr->capacity)
@@ -116,29 +117,22 @@ int begin_impl(ffx_ctx* c, ffx_replica* t, ffx_replica* t2, const std::vector<Sr
   P.tgt = t;
   P.tgt2 = t2;
   SliceJob& job = P.job;
-  job.nregions = static_cast<uint32_t>(srcs.size());
-  for (size_t i = 0; i < srcs.size(); ++i)
-    job.reg[i] = SliceRegion{srcs[i].dev, t->wpayload(slot) + offs[i], srcs[i].bytes, 0, 0};
-  job.slice_bytes = c->slice_bytes;
-#ifdef FFX_DEV
-  // timing prototype (FFX_HEAD_SPLIT=bytes, FFX_HEAD_SLICE=bytes): the head
-  // of region 0 -- the tasks claimed last -- in smaller slices.  The table
-  // layout then differs from what recovery expects: measurement only.
-  if (const char* hs = std::getenv("FFX_HEAD_SPLIT")) {
-    const uint64_t head = std::strtoull(hs, nullptr, 10);
-    const char* hsl = std::getenv("FFX_HEAD_SLICE");
-    const uint32_t small = hsl ? static_cast<uint32_t>(std::atoi(hsl)) : 1024u;
-    if (head && job.nregions < kMaxRegions && job.reg[0].bytes > 2 * head) {
-      for (uint32_t i = job.nregions; i > 0; --i) job.reg[i] = job.reg[i - 1];
-      job.reg[0].bytes = head;
-      job.reg[0].slice_bytes = small;
-      job.reg[1].src += head;
-      job.reg[1].dst += head;
-      job.reg[1].bytes -= head;
-      ++job.nregions;
+  // one job region per slice run (ffx_layout.h): the first region's head in
+  // quarter-size slices, everything else at the context's slice size
+  std::vector<std::pair<uint32_t, uint64_t>> run_of;  // (registered region, offset within it) per job region
+  job.nregions = 0;
+  for (size_t i = 0; i < srcs.size(); ++i) {
+    SliceRun runs[2];
+    const int k = region_runs(srcs[i].bytes, c->slice_bytes,
+                              head_region(static_cast<uint32_t>(i), static_cast<uint32_t>(srcs.size())), runs);
+    for (int j = 0; j < k; ++j) {
+      SliceRegion R{srcs[i].dev + runs[j].offset, t->wpayload(slot) + offs[i] + runs[j].offset, runs[j].bytes, 0, 0};
+      R.slice_bytes = static_cast<uint32_t>(runs[j].slice);
+      job.reg[job.nregions++] = R;
+      run_of.emplace_back(static_cast<uint32_t>(i), runs[j].offset);
     }
   }
-#endif
+  job.slice_bytes = c->slice_bytes;
   job.sums_out = t->wsums(slot);
   job.sched = c->done + 8;  // dynamic task counter (words 8-9 of the ctx scratch)
   // CTA-capped snapshots (scheduler batches inside a step) use the SM-lean
@@ -157,7 +151,7 @@ int begin_impl(ffx_ctx* c, ffx_replica* t, ffx_replica* t2, const std::vector<Sr
   m.pp = role.pp;
   m.tp = role.tp;
   m.kind = opts.weights_kind ? 0 : 1;
-  m.num_regions = job.nregions;
+  m.num_regions = static_cast<uint32_t>(srcs.size());
   for (size_t i = 0; i < srcs.size(); ++i) {
     m.region_bytes[i] = srcs[i].bytes;
     m.region_kinds[i] = static_cast<uint8_t>(srcs[i].kind);
@@ -179,7 +173,8 @@ int begin_impl(ffx_ctx* c, ffx_replica* t, ffx_replica* t2, const std::vector<Sr
   if (t2) {
     // Double-neighbour replication: the same tiles stored twice, one table
     // per replica, each slot committed by its own counter.
-    for (size_t i = 0; i < srcs.size(); ++i) job.reg[i].dst2 = t2->wpayload(slot2) + offs[i];
+    for (uint32_t q = 0; q < job.nregions; ++q)
+      job.reg[q].dst2 = t2->wpayload(slot2) + offs[run_of[q].first] + run_of[q].second;
     job.sums_out2 = t2->wsums(slot2);
     job.commit2 = cm;
     job.commit2.slot = t2->wslot(slot2);
@@ -244,9 +239,10 @@ int begin_impl(ffx_ctx* c, ffx_replica* t, ffx_replica* t2, const std::vector<Sr
       const uint64_t rows = job.rows;
       for (uint32_t i = 0; i < job.nregions; ++i) {
         const SliceRegion& R = job.reg[i];
-        const uint64_t ns = slices_of(R.bytes, job.slice_bytes);
+        const uint64_t S = R.slice_bytes ? R.slice_bytes : job.slice_bytes;
+        const uint64_t ns = slices_of(R.bytes, S);
         const uint64_t fs = P.gcut > R.group_base ? std::min(ns, (P.gcut - R.group_base) * rows) : 0;
-        const uint64_t fb = std::min(R.bytes, fs * job.slice_bytes);
+        const uint64_t fb = std::min(R.bytes, fs * S);
         CopyRegion& C = cj.reg[i];
         C.src += fb;
         C.dst += fb;

@@ -131,6 +131,11 @@ class PlanInfo(ctypes.Structure):
                 ("num_unique_regions", ctypes.c_uint32)]
 
 
+class SliceRun(ctypes.Structure):
+    _fields_ = [("region", ctypes.c_uint32), ("slice_bytes", ctypes.c_uint32), ("offset", ctypes.c_uint64),
+                ("bytes", ctypes.c_uint64), ("first_slice", ctypes.c_uint64)]
+
+
 class SlotInfo(ctypes.Structure):
     _fields_ = [("state", ctypes.c_uint32), ("num_regions", ctypes.c_uint32), ("role", Role),
                 ("kind", ctypes.c_uint8), ("whole_checksum_valid", ctypes.c_uint8),
@@ -252,6 +257,7 @@ SIGNATURES = {
     "ffx_register_region": (_I, [_P, _I, _P, _U64, _I]),
     "ffx_clear_regions": (_I, [_P]),
     "ffx_plan": (_I, [_P, ctypes.POINTER(PlanInfo)]),
+    "ffx_slice_runs": (_I, [ctypes.POINTER(_U64), _U32, _U64, ctypes.POINTER(SliceRun), _U32, ctypes.POINTER(_U32)]),
     "ffx_replica_create": (_I, [_P, Role, _U64, _U32, ctypes.POINTER(_P)]),
     "ffx_replica_export": (_I, [_P, _P]),
     "ffx_replica_open": (_I, [_P, _P, ctypes.POINTER(_P)]),
@@ -608,6 +614,25 @@ def checksum64(dev_tensor, nbytes: Optional[int] = None, stream=None) -> int:
     out = ctypes.c_uint64()
     check(lib.ffx_checksum64(_ptr(dev_tensor), n, ctypes.byref(out), _stream_ptr(stream)), "checksum64")
     return out.value
+
+
+def slice_runs(region_bytes: Sequence[int], slice_bytes: int) -> list:
+    """The payload's checksum-slice runs, in table order (ffx_slice_runs):
+    [(region, offset, bytes, slice_bytes, first_slice), ...]."""
+    n = len(region_bytes)
+    arr = (_U64 * max(1, n))(*region_bytes)
+    out = (SliceRun * (n + 1))()
+    cnt = _U32()
+    check(lib.ffx_slice_runs(arr, n, slice_bytes, out, n + 1, ctypes.byref(cnt)), "slice_runs")
+    return [(r.region, r.offset, r.bytes, r.slice_bytes, r.first_slice) for r in out[:cnt.value]]
+
+
+def slice_index(runs: list, region: int, offset: int) -> int:
+    """Checksum-table index of the slice holding byte `offset` of `region`."""
+    for reg, off, nb, sl, first in runs:
+        if reg == region and off <= offset < off + max(nb, 1):
+            return first + (offset - off) // sl
+    raise ValueError(f"offset {offset} outside region {region}")
 
 
 def slice_checksums(dev_tensor, slice_bytes: int, out_tensor, nbytes=None, stream=None):

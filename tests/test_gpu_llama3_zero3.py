@@ -84,7 +84,9 @@ def test_llama3_8b_zero3_d8_shard_snapshot_recover_export(ffx):
         slot2 = rep.held()[2]
         info = rep.slot_info(slot2)
         assert info.payload_len == n and info.num_regions == 6
-        assert info.num_slices == sum((r.nbytes + SLICE - 1) // SLICE for r in regs1)
+        runs = ffx.slice_runs([r.nbytes for r in regs2], SLICE)  # the table's slicing (head split included)
+        assert runs[0][3] == SLICE // 4 and len(runs) == 7  # the first region (> 192 MiB) opens with a small-slice head
+        assert info.num_slices == plan.num_slices == runs[-1][4] + (runs[-1][2] + SLICE - 1) // SLICE
         assert rep.slot_regions(slot2) == [(r.kind, r.nbytes) for r in regs2]
 
         # the slot's checksum table at the sampled slices = the oracle's FNV
@@ -93,15 +95,15 @@ def test_llama3_8b_zero3_d8_shard_snapshot_recover_export(ffx):
         scratch = torch.empty((info.num_slices * 8 + SLICE - 1) // SLICE, dtype=torch.int64, device="cuda")
         ffx.copy_checksums(table, sums, SLICE, scratch, nbytes=info.num_slices * 8)
         tab = table.cpu()
-        base = 0
-        for r in regs2:
+        for reg, off, nb, sl, first in runs:
+            r = regs2[reg]
             if r.digest is not None:
-                for s in sample_slices(r.nbytes)[:4]:
-                    lo = s * SLICE
-                    ln = min(SLICE, r.nbytes - lo)
+                ns = (nb + sl - 1) // sl
+                for s in sorted({0, 1, ns // 2, ns - 1} & set(range(ns))):
+                    lo = off + s * sl
+                    ln = min(sl, off + nb - lo)
                     want = orc.materialize_range(r.digest, r.nbytes, lo, ln)
-                    assert int(tab[base + s]) & ffx.U64_MAX == orc.fnv1a64(want)
-            base += (r.nbytes + SLICE - 1) // SLICE
+                    assert int(tab[first + s]) & ffx.U64_MAX == orc.fnv1a64(want), (reg, off, s)
         del table, scratch, tab
 
         # failure of the origin rank: every region poisoned, restored from the replica
@@ -123,7 +125,7 @@ def test_llama3_8b_zero3_d8_shard_snapshot_recover_export(ffx):
         origin.inject(ffx.FAULT_CORRUPT_REPLICA, view, (slot2 << 48) | off)
         with pytest.raises(ffx.RestoreError) as ei:
             origin.recover(view, 2)
-        want_slice = sum(-(-r.nbytes // SLICE) for r in regs2[:2]) + 123_456_789 // SLICE  # per-region slicing
+        want_slice = ffx.slice_index(runs, 2, 123_456_789)  # per-region slicing
         assert "first slice %d" % want_slice in str(ei.value)
 
         # SNP1 export above 4 GiB: the parts the reference's parser accepts

@@ -323,7 +323,10 @@ def test_full_size_gpt2xl_shard_roundtrip(ffx):
     # size-independent properties: the restored blob is sound, and sampled
     # slices (bytes and table entries) equal the oracle's.
     pay, sums = rep.slot_ptrs(rep.held()[11])
-    nsl = (n + 4095) // 4096
+    runs = ffx.slice_runs([n], 4096)  # a 48 MiB head of 1 KiB slices, then 4 KiB slices
+    assert [(r[1], r[3]) for r in runs] == [(0, 1024), (48 << 20, 4096)]
+    nsl = runs[-1][4] + (runs[-1][2] + 4095) // 4096
+    assert rep.slot_info(rep.held()[11]).num_slices == nsl
     table = torch.empty(nsl, dtype=torch.int64, device="cuda")
     scratch = torch.empty((nsl * 8 + 4095) // 4096, dtype=torch.int64, device="cuda")
     ffx.copy_checksums(table, sums, 4096, scratch, nbytes=nsl * 8)  # device copy of the table
@@ -332,12 +335,14 @@ def test_full_size_gpt2xl_shard_roundtrip(ffx):
     rpt = origin.recover(view, 11)
     assert rpt.bad_slices == 0 and rpt.bytes == n
     assert ffx.blob_is_sound(state)
-    for s in (0, 1, 12345, nsl // 2, nsl - 2, nsl - 1):
-        lo = s * 4096
-        ln = min(4096, n - lo)
-        want = orc.materialize_range(d, n, lo, ln)
-        assert host(state[lo:lo + ln]) == want
-        assert tab[s] == orc.fnv1a64(want)
+    for _, off, nb, sl, first in runs:
+        ns = (nb + sl - 1) // sl
+        for s in (0, 1, 12345, ns // 2, ns - 2, ns - 1):
+            lo = off + s * sl
+            ln = min(sl, off + nb - lo)
+            want = orc.materialize_range(d, n, lo, ln)
+            assert host(state[lo:lo + ln]) == want
+            assert tab[first + s] == orc.fnv1a64(want)
 
 
 def test_scheduler_begin_next_gated(ffx):
