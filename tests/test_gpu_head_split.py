@@ -32,8 +32,8 @@ def fill(ts, seed):
         t.copy_(torch.randint(0, 256, t.shape, dtype=torch.uint8, device="cuda", generator=g))
 
 
-def want_table(ffx, regions):
-    runs = ffx.slice_runs([len(r) for r in regions], 4096)
+def want_table(ffx, regions, slice_bytes=4096):
+    runs = ffx.slice_runs([len(r) for r in regions], slice_bytes)
     out = []
     for reg, off, nb, sl, first in runs:
         assert first == len(out)
@@ -182,6 +182,86 @@ def test_head_split_pull(ffx):
         torch.cuda.synchronize()
         if remote is not None:
             remote.close()
+        rep.destroy()
+        origin.close()
+        holder.close()
+
+
+@pytest.mark.parametrize("policy,copy_ctas,task_ctas", [(0, 16, False), (0, 16, True), (1, 8, False),
+                                                        (2, 8, False), (0, 0, False)])
+def test_head_split_scheduled_batches(ffx, policy, copy_ctas, task_ctas):
+    """The slice scheduler cuts a snapshot into gap-sized batches by task
+    range; with the head the task ranges span runs of two slice sizes (and,
+    CTA-capped, the 64-slice task configuration)."""
+    spec = ffx.make_spec(d=2, phi=64, distributed=True)
+    holder = ffx.Context(0, spec, (0, 0, 0))
+    origin = ffx.Context(0, spec, (1, 0, 0))
+    ts = [torch.empty(n, dtype=torch.uint8, device="cuda") for n in SIZES]
+    rep = holder.create_replica((1, 0, 0), sum(SIZES) + 3 * 4096, 2)
+    view = origin.open_replica(rep.export())
+    origin.set_target(view)
+    gaps = 7
+    train = torch.cuda.Stream(priority=-1)
+    sched = None
+    try:
+        fill(ts, 3)
+        for t in ts:
+            origin.register(ffx.REGION_MASTER, t)
+        sched = ffx.Sched(origin, policy, link_gaps=gaps, sm_gaps=0 if policy == ffx.SCHED_FUSED else gaps,
+                          copy_ctas=copy_ctas or (1 << 20), hash_ctas=32,
+                          gap_ms=[1.0, 3.0, 0.5, 2.0, 2.0, 1.5, 0.7], task_ctas=task_ctas)
+        sched.begin(4)
+        for _ in range(gaps):
+            sched.gap(ffx.GAP_SM_IDLE, train)
+            sched.gap(ffx.GAP_LINK_IDLE, train)
+        sched.finish(train)
+        train.synchronize()
+        torch.cuda.synchronize()
+        regions = [host(t) for t in ts]
+        runs, want = want_table(ffx, regions)
+        slot = rep.held()[4]
+        assert slot_table(ffx, rep, slot, len(want)) == want
+        assert rep.export_frame(4) == orc.pack_blob((1, 0, 0), 4, 1, b"".join(regions))
+        origin.inject(ffx.FAULT_POISON_STATE)
+        assert origin.recover(view, 4).bad_slices == 0 and [host(t) for t in ts] == regions
+    finally:
+        if sched is not None:
+            sched.destroy()
+        torch.cuda.synchronize()
+        view.destroy()
+        rep.destroy()
+        origin.close()
+        holder.close()
+
+
+@pytest.mark.parametrize("slice_bytes", [1024, 2048])
+def test_head_split_other_slice_sizes(ffx, slice_bytes):
+    """Head slices of 256 B (one 2-plane TMA box per slice) and 512 B."""
+    spec = ffx.make_spec(d=2, phi=64, distributed=True)
+    holder = ffx.Context(0, spec, (0, 0, 0), slice_bytes)
+    origin = ffx.Context(0, spec, (1, 0, 0), slice_bytes)
+    ts = [torch.empty(n, dtype=torch.uint8, device="cuda") for n in SIZES]
+    rep = holder.create_replica((1, 0, 0), sum(SIZES) + 3 * 4096, 2)
+    view = origin.open_replica(rep.export())
+    origin.set_target(view)
+    try:
+        fill(ts, 9)
+        for t in ts:
+            origin.register(ffx.REGION_MASTER, t)
+        origin.snapshot(2)
+        torch.cuda.synchronize()
+        regions = [host(t) for t in ts]
+        runs, want = want_table(ffx, regions, slice_bytes)
+        assert runs[0][3] == slice_bytes // 4
+        slot = rep.held()[2]
+        assert rep.slot_info(slot).num_slices == len(want)
+        assert slot_table(ffx, rep, slot, len(want)) == want
+        assert holder.verify_held(rep, 2).bad_slices == 0
+        origin.inject(ffx.FAULT_POISON_STATE)
+        assert origin.recover(view, 2).bad_slices == 0 and [host(t) for t in ts] == regions
+    finally:
+        torch.cuda.synchronize()
+        view.destroy()
         rep.destroy()
         origin.close()
         holder.close()
