@@ -562,7 +562,7 @@ extern "C" int ffx_slice_runs(const uint64_t* region_bytes, uint32_t n, uint64_t
   uint32_t k = 0;
   uint64_t first = 0;
   for (uint32_t i = 0; i < n; ++i) {
-    SliceRun runs[2];
+    SliceRun runs[kRegionRuns];
     const int m = region_runs(region_bytes[i], slice_bytes, head_region(i, n), runs);
     for (int j = 0; j < m; ++j, ++k) {
       if (k < cap)

@@ -256,7 +256,7 @@ inline std::vector<RunRef> payload_runs(const PayloadMap& pm, uint64_t S) {
   std::vector<RunRef> out;
   const uint32_t n = static_cast<uint32_t>(pm.regs.size());
   for (uint32_t r = 0; r < n; ++r) {
-    SliceRun runs[2];
+    SliceRun runs[kRegionRuns];
     const int k = region_runs(pm.regs[r]->bytes, S, head_region(r, n), runs);
     for (int j = 0; j < k; ++j) out.push_back(RunRef{r, runs[j]});
   }

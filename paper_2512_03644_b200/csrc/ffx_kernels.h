@@ -26,7 +26,11 @@ struct SliceRegion {
   const uint64_t* expected;  // verify: this region's own table (region-local index), else the job's
 };
 
-constexpr int kTmaRegions = 4;  // regions that get 2-D TMA tensor maps per launch
+// regions that get TMA tensor maps per launch (the largest ones): a Llama-3
+// ZeRO-3 shard is 4 large regions + the first one's head run, a two-source
+// gather twice that; 8 x 3 maps make the job a 5 KB kernel parameter
+// (CUDA >= 12.1 allows 32 KB)
+constexpr int kTmaRegions = 8;
 
 // Optional slot commit fused into the snapshot kernel: every CTA marks the
 // slot WRITING before its first payload store; the last CTA to finish writes

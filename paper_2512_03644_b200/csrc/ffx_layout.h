@@ -57,12 +57,14 @@ inline uint64_t align_up(uint64_t x, uint64_t a) { return (x + a - 1) / a * a; }
 // A snapshot claims its warp tasks last task first, so the tasks it runs LAST
 // are the first ones of the payload.  The head of the first region is cut
 // into quarter-size slices: the final round of warp tasks is then 4x shorter
-// and the launch's tail shrinks (N=1, 2.34 GB: 3024 -> 3095 GB/s,
-// profiles/r2_head_split_1gpu.jsonl).  Everything that builds a job over a
+// and the launch's tail shrinks (N=1, 2.34 GB: 3024 -> 3112 GB/s,
+// profiles/r2_head_split_1gpu.jsonl; a further 8-16 MiB of S/16 slices
+// measured no gain, profiles/r2_fine_head_ab_1gpu.jsonl).  Everything that builds a job over a
 // slot (snapshot, recovery, verify, plan) cuts the regions the same way, so
 // the checksum table is entries of the head slices, then the rest of region
 // 0 at the context's slice size, then the other regions.
 constexpr uint64_t kHeadBytes = 48ull << 20;
+constexpr int kRegionRuns = 2;  // runs per region, at most (head + rest)
 inline uint64_t head_slice_bytes(uint64_t S) { return (S % 1024 == 0 && S >= 1024) ? S / 4 : 0; }
 inline uint64_t head_bytes(uint64_t region0_bytes, uint64_t S) {
   return head_slice_bytes(S) && region0_bytes >= 4 * kHeadBytes ? kHeadBytes : 0;
@@ -72,8 +74,8 @@ struct SliceRun {
   uint64_t bytes;
   uint64_t slice;   // slice size of this run
 };
-// The runs of one region (first = the first region of the payload); returns 1 or 2.
-inline int region_runs(uint64_t bytes, uint64_t S, bool first, SliceRun out[2]) {
+// The runs of one region (first = the first region of the payload); returns 1..kRegionRuns.
+inline int region_runs(uint64_t bytes, uint64_t S, bool first, SliceRun out[kRegionRuns]) {
   const uint64_t h = first ? head_bytes(bytes, S) : 0;
   if (!h) {
     out[0] = SliceRun{0, bytes, S};
@@ -86,12 +88,12 @@ inline int region_runs(uint64_t bytes, uint64_t S, bool first, SliceRun out[2]) 
 inline uint64_t run_slices(const SliceRun& r) { return (r.bytes + r.slice - 1) / r.slice; }
 // Region i of n gets the head when it is the first and a job region is left
 // for it (a job holds at most kMaxRegions).
-inline bool head_region(uint32_t i, uint32_t n) { return i == 0 && n < kMaxRegions; }
+inline bool head_region(uint32_t i, uint32_t n) { return i == 0 && n + kRegionRuns - 1 <= kMaxRegions; }
 // Checksum-table entries of a payload of n regions.
 inline uint64_t table_entries(const uint64_t* region_bytes, uint32_t n, uint64_t S) {
   uint64_t e = 0;
   for (uint32_t i = 0; i < n; ++i) {
-    SliceRun r[2];
+    SliceRun r[kRegionRuns];
     const int k = region_runs(region_bytes[i], S, head_region(i, n), r);
     for (int j = 0; j < k; ++j) e += run_slices(r[j]);
   }
@@ -101,9 +103,12 @@ inline uint64_t table_entries(const uint64_t* region_bytes, uint32_t n, uint64_t
 inline SlotLayout make_layout(uint64_t capacity, uint64_t slice_bytes) {
   SlotLayout L;
   L.payload_cap = align_up(capacity, kRegionAlign) + kMaxRegions * kRegionAlign;
-  const uint64_t head = head_bytes(capacity, slice_bytes);
-  L.table_cap = (capacity + slice_bytes - 1) / slice_bytes + kMaxRegions +
-                (head ? head / head_slice_bytes(slice_bytes) - head / slice_bytes : 0);
+  // a capacity-sized first region: its head runs' extra entries
+  SliceRun r[kRegionRuns];
+  const int k = region_runs(capacity, slice_bytes, true, r);
+  uint64_t extra = 0;
+  for (int j = 0; j + 1 < k; ++j) extra += r[j].bytes / r[j].slice - r[j].bytes / slice_bytes;
+  L.table_cap = (capacity + slice_bytes - 1) / slice_bytes + kMaxRegions + extra;
   L.payload_off = align_up(kMetaBytes + 8 * L.table_cap + 32, 4096);
   L.slot_stride = align_up(L.payload_off + L.payload_cap, 1 << 21);
   return L;

@@ -234,7 +234,7 @@ extern "C" int ffx_replica_verify(ffx_ctx* c, ffx_replica* held, uint64_t iterat
   SliceJob job{};
   uint64_t phys = 0;
   for (uint32_t i = 0; i < m.num_regions; ++i) {
-    SliceRun runs[2];
+    SliceRun runs[kRegionRuns];
     const int k = region_runs(m.region_bytes[i], m.slice_bytes, head_region(i, m.num_regions), runs);
     for (int j = 0; j < k; ++j) {
       SliceRegion R{held->payload(v) + phys + runs[j].offset, nullptr, runs[j].bytes, 0, 0};

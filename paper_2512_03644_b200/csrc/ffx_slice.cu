@@ -786,9 +786,15 @@ bool encode_rows(CUtensorMap* map, const void* base, uint64_t slice_bytes, uint6
 // Give the (up to kTmaRegions) largest eligible regions 2-D tensor maps.
 void attach_tensor_maps(SliceJob& job, bool copy, int kc_planes) {
   for (uint32_t r = 0; r < kMaxRegions; ++r) job.reg[r].tmap = -1;
+  // largest first: a region left without a map runs on the latency-bound
+  // register path, which only suits small or unaligned regions
+  uint32_t order[kMaxRegions];
+  for (uint32_t r = 0; r < job.nregions; ++r) order[r] = r;
+  std::stable_sort(order, order + job.nregions,
+                   [&](uint32_t a, uint32_t b) { return job.reg[a].bytes > job.reg[b].bytes; });
   int used = 0;
-  for (uint32_t r = 0; r < job.nregions && used < kTmaRegions; ++r) {
-    SliceRegion& R = job.reg[r];
+  for (uint32_t q = 0; q < job.nregions && used < kTmaRegions; ++q) {
+    SliceRegion& R = job.reg[order[q]];
     const uint64_t S = R.slice_bytes ? R.slice_bytes : job.slice_bytes;
     if (S % 128 != 0 || S > (1ull << 31)) continue;
     R.nfull = R.bytes / S;

@@ -122,7 +122,7 @@ int begin_impl(ffx_ctx* c, ffx_replica* t, ffx_replica* t2, const std::vector<Sr
   std::vector<std::pair<uint32_t, uint64_t>> run_of;  // (registered region, offset within it) per job region
   job.nregions = 0;
   for (size_t i = 0; i < srcs.size(); ++i) {
-    SliceRun runs[2];
+    SliceRun runs[kRegionRuns];
     const int k = region_runs(srcs[i].bytes, c->slice_bytes,
                               head_region(static_cast<uint32_t>(i), static_cast<uint32_t>(srcs.size())), runs);
     for (int j = 0; j < k; ++j) {
