@@ -359,12 +359,20 @@ __global__ void __launch_bounds__(W * 32) slice_kernel(const __grid_constant__ S
 
     std::conditional_t<kCopy, Fnv, FnvAlu> h[RPL];  // hash form per mode (ffx_device.cuh)
     uint64_t len[RPL];
+    uint64_t want[RPL];  // verify modes: the expected checksums, loaded now so the
+                         // load latency hides under the task instead of after it
 #pragma unroll
     for (int r = 0; r < RPL; ++r) {
       const uint64_t off = (s0 + lane + 32 * r) * Sl;
       len[r] = off < R.bytes ? umin64(Sl, R.bytes - off) : 0;
       h[r].init();
       if (job.init_state != nullptr && len[r]) h[r].set(job.init_state[R.slice_base + s0 + lane + 32 * r]);
+      want[r] = 0;
+      if constexpr (kVerify) {
+        if (len[r])
+          want[r] = R.expected != nullptr ? R.expected[s0 + lane + 32 * r]
+                                          : job.sums_expected[R.slice_base + s0 + lane + 32 * r];
+      }
     }
 
     // Stages are free once this lane's earlier bulk stores finished reading
@@ -532,8 +540,7 @@ __global__ void __launch_bounds__(W * 32) slice_kernel(const __grid_constant__ S
       if (job.sums_out != nullptr) job.sums_out[idx] = v;
       if (job.sums_out2 != nullptr) job.sums_out2[idx] = v;
       if constexpr (kVerify) {
-        const uint64_t want = R.expected != nullptr ? R.expected[s0 + lane + 32 * r] : job.sums_expected[idx];
-        if (v != want) {
+        if (v != want[r]) {
           atomicMin(&job.result[0], static_cast<unsigned long long>(idx));
           atomicAdd(&job.result[1], 1ull);
         }
