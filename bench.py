@@ -730,7 +730,8 @@ def e2e_leg(args, ffx, torch, R, world, rank, local, n, stream, barrier, max_ove
       N > 1: the C ABI with host buffers: ffx_memcpy H2D into the registered
              state, ffx_snapshot into the ring successor's replica,
              ffx_snapshot_read_sums D2H (max over ranks)."""
-    nsl = (n + args.slice_bytes - 1) // args.slice_bytes
+    runs = ffx.slice_runs([n], args.slice_bytes)  # the table's entries (with the small-slice head)
+    nsl = runs[-1][4] + (runs[-1][2] + runs[-1][3] - 1) // runs[-1][3]
     host = torch.empty(n, dtype=torch.uint8, pin_memory=True)
     host.copy_(R.state[0])
     table = torch.empty(nsl, dtype=torch.int64, pin_memory=True)
@@ -785,6 +786,7 @@ def e2e_leg(args, ffx, torch, R, world, rank, local, n, stream, barrier, max_ove
                                                  ctypes.byref(got), st), "read_sums")
         f1.record(stream)
         stream.synchronize()
+        assert got.value == nsl  # the whole table came back
         ems = max_over_ranks(f0.elapsed_time(f1))
         out = {"value": round(world * n * k / (ems * 1e-3) / 1e9, 3), "unit": "GB/s",
                "h2d_bytes_per_step": n, "d2h_bytes_per_step": nsl * 8,
