@@ -207,6 +207,9 @@ def test_head_split_scheduled_batches(ffx, policy, copy_ctas, task_ctas):
         fill(ts, 3)
         for t in ts:
             origin.register(ffx.REGION_MASTER, t)
+        # the batches run on the scheduler's own stream, gated only on events
+        # of `train`: the state must be complete before the step starts
+        torch.cuda.synchronize()
         sched = ffx.Sched(origin, policy, link_gaps=gaps, sm_gaps=0 if policy == ffx.SCHED_FUSED else gaps,
                           copy_ctas=copy_ctas or (1 << 20), hash_ctas=32,
                           gap_ms=[1.0, 3.0, 0.5, 2.0, 2.0, 1.5, 0.7], task_ctas=task_ctas)
