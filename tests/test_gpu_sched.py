@@ -37,6 +37,7 @@ def test_sched_policies_commit_the_reference_frame(ffx, policy, weights):
     d = orc.optimizer_init(42, 1, 0, 0, True)
     state = torch.empty(n, dtype=torch.uint8, device="cuda")
     ffx.materialize(state, d)
+    torch.cuda.synchronize()  # the scheduler's streams do not wait on the default stream
     origin.register(ffx.REGION_BLOB, state)
     gaps = 6
     train = torch.cuda.Stream(priority=-1)
@@ -89,6 +90,7 @@ def test_sched_zero_weight_gaps_and_idle_calls(ffx):
     d = orc.optimizer_init(5, 1, 0, 0, True)
     state = torch.empty(n, dtype=torch.uint8, device="cuda")
     ffx.materialize(state, d)
+    torch.cuda.synchronize()  # the scheduler's streams do not wait on the default stream
     origin.register(ffx.REGION_BLOB, state)
     train = torch.cuda.Stream()
     sched = ffx.Sched(origin, ffx.SCHED_SPLIT_CE, link_gaps=4, sm_gaps=4, gap_ms=[0.0, 0.0, 2.0, 0.0])
@@ -146,6 +148,7 @@ def test_train_waits_at_most_one_state_batch(ffx, cap, tasks):
     origin.set_target(view)
     state = torch.empty(n, dtype=torch.uint8, device="cuda")
     ffx.materialize(state, orc.optimizer_init(3, 1, 0, 0, True))
+    torch.cuda.synchronize()  # the scheduler's streams do not wait on the default stream
     origin.register(ffx.REGION_BLOB, state)
     train = torch.cuda.Stream(priority=-1)
     low = torch.cuda.Stream(priority=0)
