@@ -32,10 +32,23 @@ int check_source(ffx_ctx* c, ffx_replica* src, uint64_t target, SlotMeta* m, uin
     if (m->region_bytes[i] != pm.regs[i]->bytes)
       return fail(FFX_ERESTORE, "region %zu: snapshot %llu bytes, registered %llu", i,
                   (unsigned long long)m->region_bytes[i], (unsigned long long)pm.regs[i]->bytes);
-  return FFX_OK;
+  return check_table(*m);
 }
 
 }  // namespace
+
+// The slot's slice size and table length agree with its regions (a corrupt
+// meta must not steer a job past the table).
+int ffx::host::check_table(const SlotMeta& m) {
+  if (!slice_ok(m.slice_bytes))
+    return fail(FFX_ECORRUPT, "slot metadata: slice size %llu", (unsigned long long)m.slice_bytes);
+  if (m.num_regions > kMaxRegions) return fail(FFX_ECORRUPT, "slot metadata: %u regions", m.num_regions);
+  const uint64_t want = table_entries(m.region_bytes, m.num_regions, m.slice_bytes);
+  if (m.num_slices != want)
+    return fail(FFX_ECORRUPT, "slot metadata: %llu table entries, the regions need %llu",
+                (unsigned long long)m.num_slices, (unsigned long long)want);
+  return FFX_OK;
+}
 
 int ffx::host::reset_ack(ffx_ctx* c, cudaStream_t s) {
   FFX_CUDA(cudaMemsetAsync(c->done + kAckWord, 0xff, 8, s));
@@ -230,16 +243,16 @@ extern "C" int ffx_replica_verify(ffx_ctx* c, ffx_replica* held, uint64_t iterat
   if (v == -2) return fail(FFX_ECUDA, "replica_verify: cannot read slot metadata: %s", g_err.c_str());
   if (v < 0 || m.state != kSlotCommitted)
     return fail(FFX_ERESTORE, "replica_verify: no committed snapshot at iteration %llu", (unsigned long long)iteration);
-  if (m.num_regions > kMaxRegions) return fail(FFX_ECORRUPT, "replica_verify: %u regions", m.num_regions);
+  if (int st = check_table(m)) return st;
   SliceJob job{};
   uint64_t phys = 0;
   for (uint32_t i = 0; i < m.num_regions; ++i) {
     SliceRun runs[kRegionRuns];
     const int k = region_runs(m.region_bytes[i], m.slice_bytes, head_region(i, m.num_regions), runs);
     for (int j = 0; j < k; ++j) {
-      SliceRegion R{held->payload(v) + phys + runs[j].offset, nullptr, runs[j].bytes, 0, 0};
-      R.slice_bytes = static_cast<uint32_t>(runs[j].slice);
-      job.reg[job.nregions++] = R;
+      SliceRegion part{held->payload(v) + phys + runs[j].offset, nullptr, runs[j].bytes, 0, 0};
+      part.slice_bytes = static_cast<uint32_t>(runs[j].slice);
+      job.reg[job.nregions++] = part;
     }
     phys = align_up(phys + m.region_bytes[i], kRegionAlign);
   }

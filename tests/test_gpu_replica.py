@@ -610,3 +610,42 @@ def test_holder_verifies_landed_bytes(ffx, copy_engine):
     torch.cuda.synchronize()
     assert sorted(rep.held()) == [3, 5]
     assert holder.verify_held(rep, 5).bad_slices == 0
+
+
+def test_corrupt_slot_metadata_is_refused_not_followed(ffx):
+    """A slot whose metadata lies about its slicing (slice size, table
+    length) is refused with CorruptSnapshot by recovery and by the holder's
+    verify -- the job is never built from it (ffx_recover.cu check_table)."""
+    import ctypes
+    n = 3 * (1 << 20) + 77
+    spec, holder, origin, rep, view = ring_pair(ffx, n)
+    state, want = blob_for(ffx, 1, n)
+    origin.register(ffx.REGION_BLOB, state)
+    origin.snapshot(6)
+    torch.cuda.synchronize()
+    slot = rep.held()[6]
+    pay, sums = rep.slot_ptrs(slot)
+    meta = sums - 256  # SlotMeta sits right before the table
+
+    def poke(off, value):
+        v = ctypes.c_uint64(value)
+        ffx.check(ffx.lib.ffx_memcpy(ctypes.c_void_p(meta + off), ctypes.c_void_p(ctypes.addressof(v)), 8, None, 1), "poke")
+
+    nsl = rep.slot_info(slot).num_slices
+    try:
+        for off, bad, good in ((32, 0, 4096), (32, 100, 4096), (40, nsl + 1, nsl), (40, 1 << 40, nsl)):
+            poke(off, bad)
+            with pytest.raises(ffx.CorruptSnapshot, match="slot metadata"):
+                origin.recover(view, 6)
+            with pytest.raises(ffx.CorruptSnapshot, match="slot metadata"):
+                holder.verify_held(rep, 6)
+            poke(off, good)
+        origin.inject(ffx.FAULT_POISON_STATE)
+        assert origin.recover(view, 6).bad_slices == 0
+        assert host(state) == want
+    finally:
+        torch.cuda.synchronize()
+        view.destroy()
+        rep.destroy()
+        origin.close()
+        holder.close()
