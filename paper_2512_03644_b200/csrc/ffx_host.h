@@ -282,8 +282,9 @@ int preload_fetch(ffx_preload* p, uint64_t iteration, const void* host_src, cons
 namespace ffx::host {
 // Set ctx's pull-mode ack word to kAckNone on stream s (stream-ordered).
 int reset_ack(ffx_ctx* c, cudaStream_t s);
-// Slot metadata sanity: slice size, region count and table length agree (FFX_ECORRUPT).
-int check_table(const SlotMeta& m);
+// Slot metadata sanity: regions, payload length, slice size and table length
+// agree with each other and with r's layout (FFX_ECORRUPT otherwise).
+int check_meta(const ffx_replica* r, const SlotMeta& m);
 }  // namespace ffx::host
 
 using namespace ffx::host;

@@ -25,6 +25,7 @@ int check_source(ffx_ctx* c, ffx_replica* src, uint64_t target, SlotMeta* m, uin
   if (m->dp != c->self.dp || m->pp != c->self.pp || m->tp != c->self.tp)
     return fail(FFX_ERESTORE, "unique-state source is for d%up%ut%u, want d%up%ut%u", m->dp, m->pp,
                 m->tp, c->self.dp, c->self.pp, c->self.tp);
+  if (int st = check_meta(src, *m)) return st;
   const PayloadMap pm = payload_map(c);
   if (m->num_regions != pm.regs.size())
     return fail(FFX_ERESTORE, "snapshot has %u regions, %zu registered", m->num_regions, pm.regs.size());
@@ -32,19 +33,30 @@ int check_source(ffx_ctx* c, ffx_replica* src, uint64_t target, SlotMeta* m, uin
     if (m->region_bytes[i] != pm.regs[i]->bytes)
       return fail(FFX_ERESTORE, "region %zu: snapshot %llu bytes, registered %llu", i,
                   (unsigned long long)m->region_bytes[i], (unsigned long long)pm.regs[i]->bytes);
-  return check_table(*m);
+  return FFX_OK;
 }
 
 }  // namespace
 
-// The slot's slice size and table length agree with its regions (a corrupt
-// meta must not steer a job past the table).
-int ffx::host::check_table(const SlotMeta& m) {
+// The slot's regions, payload and slicing agree with each other and with the
+// replica's layout: a corrupt meta must not steer a job (or an export) past
+// the payload or the table.
+int ffx::host::check_meta(const ffx_replica* r, const SlotMeta& m) {
+  if (m.num_regions > kMaxRegions) return fail(FFX_ECORRUPT, "slot metadata: %u regions", m.num_regions);
+  uint64_t logical = 0, physical = 0;
+  for (uint32_t i = 0; i < m.num_regions; ++i) {
+    if (m.region_bytes[i] > r->capacity)
+      return fail(FFX_ECORRUPT, "slot metadata: region %u of %llu bytes", i, (unsigned long long)m.region_bytes[i]);
+    logical += m.region_bytes[i];
+    physical = align_up(physical + m.region_bytes[i], kRegionAlign);
+  }
+  if (logical != m.payload_len || m.payload_len > r->capacity || physical > r->layout.payload_cap)
+    return fail(FFX_ECORRUPT, "slot metadata: payload %llu bytes, regions %llu, capacity %llu",
+                (unsigned long long)m.payload_len, (unsigned long long)logical, (unsigned long long)r->capacity);
   if (!slice_ok(m.slice_bytes))
     return fail(FFX_ECORRUPT, "slot metadata: slice size %llu", (unsigned long long)m.slice_bytes);
-  if (m.num_regions > kMaxRegions) return fail(FFX_ECORRUPT, "slot metadata: %u regions", m.num_regions);
   const uint64_t want = table_entries(m.region_bytes, m.num_regions, m.slice_bytes);
-  if (m.num_slices != want)
+  if (m.num_slices != want || want > r->layout.table_cap)
     return fail(FFX_ECORRUPT, "slot metadata: %llu table entries, the regions need %llu",
                 (unsigned long long)m.num_slices, (unsigned long long)want);
   return FFX_OK;
@@ -243,7 +255,7 @@ extern "C" int ffx_replica_verify(ffx_ctx* c, ffx_replica* held, uint64_t iterat
   if (v == -2) return fail(FFX_ECUDA, "replica_verify: cannot read slot metadata: %s", g_err.c_str());
   if (v < 0 || m.state != kSlotCommitted)
     return fail(FFX_ERESTORE, "replica_verify: no committed snapshot at iteration %llu", (unsigned long long)iteration);
-  if (int st = check_table(m)) return st;
+  if (int st = check_meta(held, m)) return st;
   SliceJob job{};
   uint64_t phys = 0;
   for (uint32_t i = 0; i < m.num_regions; ++i) {

@@ -212,7 +212,7 @@ extern "C" int ffx_replica_slot_regions(ffx_replica* r, uint32_t slot, uint32_t*
   *n = 0;
   if (m.magic != kSlotMagic || m.state != kSlotCommitted)
     return fail(FFX_ERESTORE, "slot_regions: slot %u holds no committed snapshot", slot);
-  if (m.num_regions > kMaxRegions) return fail(FFX_ECORRUPT, "slot_regions: %u regions", m.num_regions);
+  if (int cst = check_meta(r, m)) return cst;
   *n = m.num_regions;
   for (uint32_t i = 0; i < m.num_regions; ++i) {
     if (kinds) kinds[i] = m.region_kinds[i];
@@ -337,6 +337,7 @@ extern "C" int ffx_replica_export_frame(ffx_replica* r, uint64_t iteration, void
   if (v == -2) return fail(FFX_ECUDA, "export_frame: cannot read slot metadata: %s", g_err.c_str());
   if (v < 0 || m.state != kSlotCommitted)
     return fail(FFX_ERESTORE, "no committed snapshot at iteration %llu", (unsigned long long)iteration);
+  if (int st = check_meta(r, m)) return st;
   if (m.payload_len > 0xffffffffull)
     return fail(FFX_EINVAL, "snapshot payload exceeds 4 GiB framing limit");
   *framed_len = 32 + m.payload_len;
@@ -396,6 +397,7 @@ extern "C" int ffx_replica_export_frame_part(ffx_replica* r, uint64_t iteration,
   if (v == -2) return fail(FFX_ECUDA, "export_frame_part: cannot read slot metadata: %s", g_err.c_str());
   if (v < 0 || m.state != kSlotCommitted)
     return fail(FFX_ERESTORE, "no committed snapshot at iteration %llu", (unsigned long long)iteration);
+  if (int st = check_meta(r, m)) return st;
   const uint64_t F = FFX_FRAME_PART_BYTES;
   const uint32_t n_parts = m.payload_len ? static_cast<uint32_t>((m.payload_len + F - 1) / F) : 1;
   if (parts) *parts = n_parts;

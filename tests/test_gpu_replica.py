@@ -633,13 +633,20 @@ def test_corrupt_slot_metadata_is_refused_not_followed(ffx):
 
     nsl = rep.slot_info(slot).num_slices
     try:
-        for off, bad, good in ((32, 0, 4096), (32, 100, 4096), (40, nsl + 1, nsl), (40, 1 << 40, nsl)):
+        # slice size, table length, payload length, a region's size
+        for off, bad, good in ((32, 0, 4096), (32, 100, 4096), (40, nsl + 1, nsl), (40, 1 << 40, nsl),
+                               (24, n + 1, n), (72, 1 << 50, n)):
             poke(off, bad)
             with pytest.raises(ffx.CorruptSnapshot, match="slot metadata"):
                 origin.recover(view, 6)
             with pytest.raises(ffx.CorruptSnapshot, match="slot metadata"):
                 holder.verify_held(rep, 6)
+            with pytest.raises(ffx.CorruptSnapshot, match="slot metadata"):
+                rep.export_frame(6)
+            with pytest.raises(ffx.CorruptSnapshot, match="slot metadata"):
+                rep.slot_regions(slot)
             poke(off, good)
+        assert rep.export_frame(6) == orc.pack_blob((1, 0, 0), 6, 1, want)
         origin.inject(ffx.FAULT_POISON_STATE)
         assert origin.recover(view, 6).bad_slices == 0
         assert host(state) == want
