@@ -222,3 +222,32 @@ def test_facade_c_entry_points_exported():
     assert len(syms) == 7
     lib = ctypes.CDLL(os.path.join(ROOT, "paper_2512_03644_b200", "libftsim_b200.so"))
     assert [s for s in syms if not hasattr(lib, s)] == []
+
+
+def _runs_spec(sizes, S):
+    """The slice-run rule restated (ffx_layout.h region_runs / DESIGN §4.1):
+    the first of fewer than 16 regions, when it holds >= 4 x 48 MiB and S is
+    a multiple of 1 KiB, opens with a 48 MiB run of S/4 slices."""
+    head = 48 << 20
+    out, first = [], 0
+    for i, nb in enumerate(sizes):
+        runs = [(0, nb, S)]
+        if i == 0 and len(sizes) < 16 and S % 1024 == 0 and nb >= 4 * head:
+            runs = [(0, head, S // 4), (head, nb - head, S)]
+        for off, b, sl in runs:
+            out.append((i, off, b, sl, first))
+            first += (b + sl - 1) // sl
+    return out
+
+
+@pytest.mark.parametrize("sizes,S", [
+    ([], 4096), ([0], 4096), ([1], 256), ([192 << 20], 4096), ([(192 << 20) - 1], 4096),
+    ([(192 << 20) + 4099, 5 << 20, 16], 4096), ([400 << 20, 400 << 20], 2048), ([300 << 20], 1280),
+    ([300 << 20], 1536), ([1 << 30] * 15, 4096), ([1 << 30] * 16, 4096), ([14_052_957_216 // 2, 7], 1024)])
+def test_slice_runs_match_the_rule(sizes, S):
+    assert ffx.slice_runs(sizes, S) == _runs_spec(sizes, S)
+
+
+def test_slice_runs_rejects_bad_arguments():
+    with pytest.raises(ffx.FfxError):
+        ffx.slice_runs([1 << 20], 100)  # not a multiple of 256
