@@ -792,6 +792,24 @@ def e2e_leg(args, ffx, torch, R, world, rank, local, n, stream, barrier, max_ove
                "h2d_bytes_per_step": n, "d2h_bytes_per_step": nsl * 8,
                "path": "C ABI with host buffers: ffx_memcpy H2D -> ffx_snapshot (ring) -> "
                        "ffx_snapshot_read_sums D2H, stream-ordered, device-timed, max over ranks"}
+    # the PCIe ceiling this number sits under: the same H2D alone (all ranks
+    # at once), device-timed, max over ranks
+    lib = ffx.lib
+    st = ctypes.c_void_p(stream.cuda_stream)
+    barrier()
+    torch.cuda.synchronize()
+    h0, h1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    h0.record(stream)
+    for _ in range(3):
+        ffx.check(lib.ffx_memcpy(ctypes.c_void_p(R.state[0].data_ptr()), ctypes.c_void_p(host.data_ptr()), n, st, 0),
+                  "H2D")
+    h1.record(stream)
+    stream.synchronize()
+    hms = max_over_ranks(h0.elapsed_time(h1))
+    h2d = world * n * 3 / (hms * 1e-3) / 1e9
+    if out is not None:
+        out["h2d_alone_gbs"] = round(h2d, 2)
+        out["frac_of_h2d"] = round(out["value"] / h2d, 4)
     del host, table
     return out
 
