@@ -95,6 +95,40 @@ def test_multicast_snapshot_lands_in_every_holder(ffx, n_holders):
         teardown(*team)
 
 
+@pytest.mark.parametrize("n_holders", [1, 2])
+def test_multicast_with_the_small_slice_head(ffx, n_holders):
+    """A payload large enough for the head run (ffx_slice_runs): the tiles of
+    both slice sizes go through the multicast range, verify-on-store re-hashes
+    what landed, every holder verifies its own slot and restores bit-exactly."""
+    if torch.cuda.device_count() < n_holders + 1:
+        pytest.skip("needs %d GPUs" % (n_holders + 1))
+    n = (200 << 20) + 4099
+    assert ffx.slice_runs([n], 4096)[0][3] == 1024
+    team = build_team(ffx, n_holders, n)
+    origin, holders, held, mc, mcs, views = team
+    try:
+        torch.cuda.set_device(0)
+        d0 = orc.optimizer_init(44, 0, 0, 0, True)
+        state = torch.empty(n, dtype=torch.uint8, device="cuda:0")
+        ffx.materialize(state, d0)
+        origin.register(ffx.REGION_BLOB, state)
+        origin.snapshot(3, verify_on_store=True)
+        torch.cuda.synchronize()
+        want = orc.materialize(d0, n)
+        for h, r in zip(holders, held):
+            assert h.verify_held(r, 3).bad_slices == 0
+        for v in views:
+            state.fill_(0)
+            assert origin.recover(v, 3).bad_slices == 0
+            assert host(state) == want
+        # a flipped byte in the head is located at its 1 KiB slice
+        origin.inject(ffx.FAULT_CORRUPT_REPLICA, views[0], (held[0].held()[3] << 48) | (5 * 1024 + 7))
+        with pytest.raises(ffx.RestoreError, match="first slice 5\\b"):
+            origin.recover(views[0], 3)
+    finally:
+        teardown(*team)
+
+
 def test_multicast_verify_on_store_and_corruption(ffx):
     n = 1 << 20
     team = build_team(ffx, 1, n)
