@@ -15,6 +15,7 @@
 #pragma once
 
 #include <cstdint>
+#include <cstdlib>
 
 namespace ffx {
 
@@ -66,8 +67,22 @@ inline uint64_t align_up(uint64_t x, uint64_t a) { return (x + a - 1) / a * a; }
 constexpr uint64_t kHeadBytes = 48ull << 20;
 constexpr int kRegionRuns = 2;  // runs per region, at most (head + rest)
 inline uint64_t head_slice_bytes(uint64_t S) { return (S % 1024 == 0 && S >= 1024) ? S / 4 : 0; }
+#ifdef FFX_DEV
+// development builds: FFX_HEAD_MIB overrides the head size (every process of
+// a run must agree -- the layout is not recorded in the slot)
+inline uint64_t head_size() {
+  static const uint64_t h = [] {
+    const char* e = std::getenv("FFX_HEAD_MIB");
+    return e ? static_cast<uint64_t>(std::strtoull(e, nullptr, 10)) << 20 : kHeadBytes;
+  }();
+  return h;
+}
+#else
+inline uint64_t head_size() { return kHeadBytes; }
+#endif
 inline uint64_t head_bytes(uint64_t region0_bytes, uint64_t S) {
-  return head_slice_bytes(S) && region0_bytes >= 4 * kHeadBytes ? kHeadBytes : 0;
+  const uint64_t h = head_size();
+  return h && head_slice_bytes(S) && region0_bytes >= 4 * h ? h : 0;
 }
 struct SliceRun {
   uint64_t offset;  // within its region
