@@ -727,9 +727,9 @@ def e2e_leg(args, ffx, torch, R, world, rank, local, n, stream, barrier, max_ove
       N = 1: ckpt::HostSnapshots::take(it, host_ptr, len) of the C++ facade
              (libftsim_b200.so, through include/ftsim_capi.h), then the step's
              result -- the per-slice checksum table -- read back to the host;
-      N > 1: the C ABI with host buffers: ffx_memcpy H2D into the registered
-             state, ffx_snapshot into the ring successor's replica,
-             ffx_snapshot_read_sums D2H (max over ranks)."""
+      N > 1: the C ABI with host buffers: ffx_snapshot_from_host (H2D into
+             the registered state pipelined under the snapshot into the ring
+             successor's replica), ffx_snapshot_read_sums D2H (max over ranks)."""
     runs = ffx.slice_runs([n], args.slice_bytes)  # the table's entries (with the small-slice head)
     nsl = runs[-1][4] + (runs[-1][2] + runs[-1][3] - 1) // runs[-1][3]
     host = torch.empty(n, dtype=torch.uint8, pin_memory=True)
@@ -765,13 +765,13 @@ def e2e_leg(args, ffx, torch, R, world, rank, local, n, stream, barrier, max_ove
             out = {"value": round(n * k / t / 1e9, 3), "unit": "GB/s", "h2d_bytes_per_step": n,
                    "d2h_bytes_per_step": nsl * 8,
                    "path": "ckpt::HostSnapshots::take(it, pinned host ptr, len) -> D2H of the per-slice "
-                           "checksum table (facade libftsim_b200.so via ftsim_capi.h; H2D + fused copy/FNV "
-                           "into the two-version device slots); host wall clock, first call untimed"}
+                           "checksum table (facade libftsim_b200.so via ftsim_capi.h; H2D pipelined under the "
+                           "fused copy/FNV batches into the two-version device slots, ffx_snapshot_from_host); "
+                           "host wall clock, first call untimed"}
         finally:
             fl.ftsim_hs_destroy(hs)
     else:
         lib = ffx.lib
-        dev = R.state[0].data_ptr()
         st = ctypes.c_void_p(stream.cuda_stream)
         got = ctypes.c_uint64()
         barrier()
@@ -780,8 +780,9 @@ def e2e_leg(args, ffx, torch, R, world, rank, local, n, stream, barrier, max_ove
         for j in range(k + 1):
             if j == 1:
                 f0.record(stream)
-            ffx.check(lib.ffx_memcpy(ctypes.c_void_p(dev), ctypes.c_void_p(host.data_ptr()), n, st, 0), "H2D")
-            ffx.check(lib.ffx_snapshot(R.ctx._c, it + j + 1, st, None), "snapshot")
+            # H2D into the registered state, pipelined under the snapshot's batches
+            ffx.check(lib.ffx_snapshot_from_host(R.ctx._c, it + j + 1, ctypes.c_void_p(host.data_ptr()), n, 0, st),
+                      "snapshot_from_host")
             ffx.check(lib.ffx_snapshot_read_sums(R.ctx._c, ctypes.c_void_p(table.data_ptr()), nsl,
                                                  ctypes.byref(got), st), "read_sums")
         f1.record(stream)
@@ -790,8 +791,9 @@ def e2e_leg(args, ffx, torch, R, world, rank, local, n, stream, barrier, max_ove
         ems = max_over_ranks(f0.elapsed_time(f1))
         out = {"value": round(world * n * k / (ems * 1e-3) / 1e9, 3), "unit": "GB/s",
                "h2d_bytes_per_step": n, "d2h_bytes_per_step": nsl * 8,
-               "path": "C ABI with host buffers: ffx_memcpy H2D -> ffx_snapshot (ring) -> "
-                       "ffx_snapshot_read_sums D2H, stream-ordered, device-timed, max over ranks"}
+               "path": "C ABI with host buffers: ffx_snapshot_from_host (H2D pipelined under the ring "
+                       "snapshot's batches) -> ffx_snapshot_read_sums D2H, stream-ordered, device-timed, "
+                       "max over ranks"}
     # the PCIe ceiling this number sits under: the same H2D alone (all ranks
     # at once), device-timed, max over ranks
     lib = ffx.lib

@@ -570,6 +570,22 @@ int ffx_sched_preload_synthetic(ffx_sched* s, ffx_preload* p, uint64_t iteration
 /* fetches still queued in the scheduler */
 int ffx_sched_preload_pending(ffx_sched* s, uint32_t* pending);
 
+/* The logical payload bytes [*lo, *hi) (the registered unique regions
+ * concatenated) that fused batch `batch` of the pending snapshot reads:
+ * what must have landed before that batch's ffx_snapshot_next.  Batches cover
+ * consecutive, increasing spans.  FFX_ESTATE without a pending fused
+ * snapshot, FFX_ERANGE past the last batch. */
+int ffx_snapshot_batch_span(ffx_ctx* ctx, uint32_t batch, uint64_t* lo, uint64_t* hi);
+/* HostSnapshots::take(it, host_ptr, len) (ckpt.hpp:88) for device-resident
+ * state: copies `len` host bytes (the registered unique regions
+ * concatenated; len must equal their total) into those regions and snapshots
+ * them as `iteration`, pipelined -- the H2D copy of batch b+1's span runs on
+ * an internal stream while batch b's kernel runs on `stream`.  batches = 0:
+ * 8 for payloads >= 64 MiB, else 1.  Stream-ordered like ffx_snapshot; pinned
+ * host memory for the overlap (pageable memory is correct, just serial). */
+int ffx_snapshot_from_host(ffx_ctx* ctx, uint64_t iteration, const void* host, uint64_t len, uint32_t batches,
+                           void* stream);
+
 /* Copy the checksum table written by this ctx's most recent snapshot into
  * host memory (async on `stream`; pinned memory for true overlap).
  * *n_out = entries copied (min(table, max_entries)). */

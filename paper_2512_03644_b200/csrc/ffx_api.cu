@@ -532,6 +532,8 @@ extern "C" int ffx_close(ffx_ctx* c) {
   if (c->copy_done) cudaEventDestroy(c->copy_done);
   if (c->hash_done) cudaEventDestroy(c->hash_done);
   if (c->snap_done) cudaEventDestroy(c->snap_done);
+  for (cudaEvent_t e : c->h2d_ev) cudaEventDestroy(e);
+  if (c->h2d) cudaStreamDestroy(c->h2d);
   delete c;
   return FFX_OK;
 }

@@ -184,6 +184,7 @@ struct PendingSnapshot {
   // copied + hashed by the fused kernel (fjob), the copy engines move the rest
   uint64_t gcut = 0;
   SliceJob fjob{};
+  uint64_t logical_of[kMaxRegions] = {};  // logical payload offset of each job region (batch spans)
   std::vector<double> frac;  // cumulative batch boundaries in [0, 1] (measured-gap weights)
   uint64_t cut(uint64_t total, uint32_t b) const {
     return b >= batches ? total : static_cast<uint64_t>(static_cast<double>(total) * frac[b]);
@@ -214,6 +215,9 @@ struct ffx_ctx {
   ffx_replica* last_target = nullptr;
   uint64_t last_nslices = 0;
   ffx_stats stats{};
+  // ffx_snapshot_from_host: the H2D copy stream and one event per batch
+  cudaStream_t h2d = nullptr;
+  std::vector<cudaEvent_t> h2d_ev;
 };
 
 namespace ffx::host {

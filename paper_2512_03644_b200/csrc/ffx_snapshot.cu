@@ -121,16 +121,19 @@ int begin_impl(ffx_ctx* c, ffx_replica* t, ffx_replica* t2, const std::vector<Sr
   // quarter-size slices, everything else at the context's slice size
   std::vector<std::pair<uint32_t, uint64_t>> run_of;  // (registered region, offset within it) per job region
   job.nregions = 0;
+  uint64_t logical_at = 0;  // logical payload offset of srcs[i]
   for (size_t i = 0; i < srcs.size(); ++i) {
     SliceRun runs[kRegionRuns];
     const int k = region_runs(srcs[i].bytes, c->slice_bytes,
                               head_region(static_cast<uint32_t>(i), static_cast<uint32_t>(srcs.size())), runs);
     for (int j = 0; j < k; ++j) {
+      P.logical_of[job.nregions] = logical_at + runs[j].offset;
       SliceRegion R{srcs[i].dev + runs[j].offset, t->wpayload(slot) + offs[i] + runs[j].offset, runs[j].bytes, 0, 0};
       R.slice_bytes = static_cast<uint32_t>(runs[j].slice);
       job.reg[job.nregions++] = R;
       run_of.emplace_back(static_cast<uint32_t>(i), runs[j].offset);
     }
+    logical_at += srcs[i].bytes;
   }
   job.slice_bytes = c->slice_bytes;
   job.sums_out = t->wsums(slot);
@@ -671,6 +674,90 @@ extern "C" int ffx_snapshot(ffx_ctx* c, uint64_t iteration, void* stream, const 
       c->pending.active = false;
       return st;
     }
+  }
+  return FFX_OK;
+}
+
+extern "C" int ffx_snapshot_batch_span(ffx_ctx* c, uint32_t batch, uint64_t* lo, uint64_t* hi) {
+  if (!c || !lo || !hi) return fail(FFX_EINVAL, "snapshot_batch_span: null argument");
+  const PendingSnapshot& P = c->pending;
+  if (!P.active || P.split) return fail(FFX_ESTATE, "snapshot_batch_span: no fused snapshot pending");
+  if (batch >= P.batches) return fail(FFX_ERANGE, "snapshot_batch_span: batch %u of %u", batch, P.batches);
+  const SliceJob& J = P.job;
+  const uint64_t G = J.total_groups;
+  const uint64_t g0 = P.cut(G, batch), g1 = P.cut(G, batch + 1);
+  // job region of warp task g, and the logical bytes [first, end) the task reads
+  auto span_of = [&](uint64_t g, uint64_t* first, uint64_t* end) {
+    uint32_t r = 0;
+    for (uint32_t i = 1; i < J.nregions; ++i)
+      if (J.reg[i].group_base <= g) r = i;
+    const SliceRegion& R = J.reg[r];
+    const uint64_t S = R.slice_bytes ? R.slice_bytes : J.slice_bytes;
+    const uint64_t a = std::min(R.bytes, (g - R.group_base) * J.rows * S);
+    const uint64_t b = std::min(R.bytes, a + static_cast<uint64_t>(J.rows) * S);
+    *first = P.logical_of[r] + a;
+    *end = P.logical_of[r] + b;
+  };
+  if (g0 >= g1) {  // an empty batch reads nothing
+    uint64_t f = 0, e = 0;
+    if (g0 < G) span_of(g0, &f, &e);
+    else f = P.logical;
+    *lo = *hi = f;
+    return FFX_OK;
+  }
+  uint64_t f0, e0, f1, e1;
+  span_of(g0, &f0, &e0);
+  span_of(g1 - 1, &f1, &e1);
+  *lo = f0;
+  *hi = e1;
+  return FFX_OK;
+}
+
+extern "C" int ffx_snapshot_from_host(ffx_ctx* c, uint64_t iteration, const void* host, uint64_t len,
+                                      uint32_t batches, void* stream) {
+  if (!c) return fail(FFX_EINVAL, "snapshot_from_host: null ctx");
+  if (len && !host) return fail(FFX_EINVAL, "snapshot_from_host: null host pointer");
+  const PayloadMap pm = payload_map(c);
+  if (len != pm.logical)
+    return fail(FFX_ECONFIG, "snapshot_from_host: %llu host bytes, the registered regions hold %llu",
+                (unsigned long long)len, (unsigned long long)pm.logical);
+  DeviceGuard g(c->device);
+  if (!c->h2d) FFX_CUDA(cudaStreamCreateWithFlags(&c->h2d, cudaStreamNonBlocking));
+  ffx_snapshot_opts o{};
+  // ~8 batches for large payloads: each batch's kernel runs under the next
+  // chunk's copy, only the last one (~1/8 of the kernel) is exposed
+  o.batches = batches ? batches : (len >= (64ull << 20) ? 8u : 1u);
+  uint32_t nb = 1;
+  if (int st = ffx_snapshot_begin(c, iteration, &o, &nb)) return st;
+  while (c->h2d_ev.size() < nb + 1) {
+    cudaEvent_t e;
+    FFX_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    c->h2d_ev.push_back(e);
+  }
+  cudaStream_t s = as_stream(stream);
+  // the copies overwrite the registered regions: after earlier work on `stream`
+  FFX_CUDA(cudaEventRecord(c->h2d_ev[nb], s));
+  FFX_CUDA(cudaStreamWaitEvent(c->h2d, c->h2d_ev[nb], 0));
+  const uint8_t* src = static_cast<const uint8_t*>(host);
+  uint64_t copied = 0;  // logical bytes already queued
+  for (uint32_t b = 0; b < nb; ++b) {
+    uint64_t lo = 0, hi = 0;
+    if (int st = ffx_snapshot_batch_span(c, b, &lo, &hi)) return st;
+    hi = b + 1 == nb ? pm.logical : std::max(hi, copied);
+    // queue [copied, hi): region by region (the payload is the regions concatenated)
+    uint64_t at = 0;
+    for (size_t r = 0; r < pm.regs.size() && copied < hi; ++r) {
+      const uint64_t rb = pm.regs[r]->bytes;
+      if (copied < at + rb) {
+        const uint64_t n = std::min(hi, at + rb) - copied;
+        FFX_CUDA(cudaMemcpyAsync(pm.regs[r]->dev + (copied - at), src + copied, n, cudaMemcpyHostToDevice, c->h2d));
+        copied += n;
+      }
+      at += rb;
+    }
+    FFX_CUDA(cudaEventRecord(c->h2d_ev[b], c->h2d));
+    uint32_t left = 0;
+    if (int st = ffx_snapshot_next(c, stream, c->h2d_ev[b], &left)) return st;
   }
   return FFX_OK;
 }

@@ -78,9 +78,14 @@ struct Slots {
     b200::check(ffx_snapshot_target(ctx, rep), "snapshot_target");
   }
 
-  // Snapshot `len` bytes (device pointer or nullptr when len == 0) as `iteration`.
-  void write(std::uint64_t iteration, const std::uint8_t* dev, std::uint64_t len) {
-    if (len && reinterpret_cast<std::uintptr_t>(dev) % 16 != 0) {
+  // Snapshot `len` bytes as `iteration`: from device memory (dev; nullptr
+  // when len == 0), or from host memory (host), copied into the staging
+  // buffer under the snapshot's own batches (ffx_snapshot_from_host).
+  void write(std::uint64_t iteration, const std::uint8_t* dev, std::uint64_t len, const void* host = nullptr) {
+    if (host) {
+      staging.ensure(len);
+      dev = staging.get();
+    } else if (len && reinterpret_cast<std::uintptr_t>(dev) % 16 != 0) {
       staging.ensure(len);  // the kernels want 16-byte aligned regions
       b200::check(ffx_memcpy(staging.get(), dev, len, nullptr, 1), "align copy");
       dev = staging.get();
@@ -88,8 +93,12 @@ struct Slots {
     b200::check(ffx_clear_regions(ctx), "clear_regions");
     b200::check(ffx_register_region(ctx, FFX_REGION_BLOB, const_cast<std::uint8_t*>(dev), len, 1),
                 "register_region");
-    ffx_snapshot_opts o{};
-    b200::check(ffx_snapshot(ctx, iteration, nullptr, &o), "snapshot");
+    if (host) {
+      b200::check(ffx_snapshot_from_host(ctx, iteration, host, len, 0, nullptr), "snapshot_from_host");
+    } else {
+      ffx_snapshot_opts o{};
+      b200::check(ffx_snapshot(ctx, iteration, nullptr, &o), "snapshot");
+    }
     b200::check(ffx_stream_sync(nullptr), "sync");  // take()/store() complete on return
     if (auto f = frames.find(iteration); f != frames.end()) f->second.fresh = false;
     if (std::find(kept.begin(), kept.end(), iteration) == kept.end()) {
@@ -137,8 +146,11 @@ void HostSnapshots::take(std::uint64_t iteration, const void* unique, std::size_
   if (len > capacity_)
     throw ConfigError("snapshot payload " + std::to_string(len) + " exceeds the host buffer of " +
                       std::to_string(capacity_) + " bytes");
-  const std::uint8_t* dev = b200::on_device(unique, len, slots_->staging);
-  slots_->write(iteration, dev, len);
+  if (len && !b200::is_device_ptr(unique)) {  // host memory: copied in under the snapshot
+    slots_->write(iteration, nullptr, len, unique);
+    return;
+  }
+  slots_->write(iteration, static_cast<const std::uint8_t*>(unique), len);
 }
 
 void HostSnapshots::take(std::uint64_t iteration, const std::vector<std::uint8_t>& unique) {

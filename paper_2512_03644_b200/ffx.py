@@ -302,6 +302,8 @@ SIGNATURES = {
     "ffx_snapshot_next": (_I, [_P, _P, _P, ctypes.POINTER(_U32)]),
     "ffx_snapshot_next_kind": (_I, [_P, _I, _P, _P, ctypes.POINTER(_U32)]),
     "ffx_snapshot_read_sums": (_I, [_P, _P, _U64, ctypes.POINTER(_U64), _P]),
+    "ffx_snapshot_batch_span": (_I, [_P, _U32, ctypes.POINTER(_U64), ctypes.POINTER(_U64)]),
+    "ffx_snapshot_from_host": (_I, [_P, _U64, _P, _U64, _U32, _P]),
     "ffx_replica_verify": (_I, [_P, _P, _U64, _U32, _P, ctypes.POINTER(RecoverReport)]),
     "ffx_recover": (_I, [_P, _P, _U64, _P, ctypes.POINTER(RecoverReport)]),
     "ffx_recover_full": (_I, [_P, ctypes.POINTER(_P), _U32, _U64, ctypes.POINTER(PeerRegion), _U32, _P,
@@ -1133,6 +1135,20 @@ class Context:
             check(lib.ffx_snapshot_next_kind(self._c, kind, _stream_ptr(stream), ev, ctypes.byref(left)),
                   "snapshot_next_kind")
         return left.value
+
+    def batch_span(self, batch: int):
+        """Logical payload bytes [lo, hi) fused batch `batch` of the pending snapshot reads."""
+        lo, hi = _U64(), _U64()
+        check(lib.ffx_snapshot_batch_span(self._c, batch, ctypes.byref(lo), ctypes.byref(hi)), "batch_span")
+        return lo.value, hi.value
+
+    def snapshot_from_host(self, iteration: int, host_tensor, nbytes: Optional[int] = None, batches: int = 0,
+                           stream=None):
+        """HostSnapshots::take from host memory: H2D into the registered regions,
+        pipelined under the snapshot batches (ffx_snapshot_from_host)."""
+        n = host_tensor.numel() * host_tensor.element_size() if nbytes is None else nbytes
+        check(lib.ffx_snapshot_from_host(self._c, iteration, _ptr(host_tensor), n, batches, _stream_ptr(stream)),
+              "snapshot_from_host")
 
     def read_sums(self, host_tensor, stream=None) -> int:
         """D2H of the last snapshot's checksum table into a (pinned) int64 tensor."""
