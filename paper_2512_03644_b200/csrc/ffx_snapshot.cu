@@ -1,6 +1,7 @@
 // ffx_snapshot.cu -- the C ABI, part 3: snapshot issue (HostSnapshots::take
 // + the ring stream, ckpt.cpp:38-53), pull mode (the holder drives it,
-// NeighborBuffer::store), and the slice scheduler's batches.
+// NeighborBuffer::store), the slice scheduler's batches, and snapshots from
+// host memory with the H2D copy pipelined under those batches.
 #include "ffx_host.h"
 
 // ---------------------------------------------------------------------------
