@@ -730,20 +730,34 @@ extern "C" int ffx_snapshot_from_host(ffx_ctx* c, uint64_t iteration, const void
   o.batches = batches ? batches : (len >= (64ull << 20) ? 8u : 1u);
   uint32_t nb = 1;
   if (int st = ffx_snapshot_begin(c, iteration, &o, &nb)) return st;
+  cudaStream_t s = as_stream(stream);
+  // A failure after begin abandons the snapshot: its slot is left torn
+  // (never restored from) and the next snapshot still waits for whatever
+  // batches of this one were issued.
+  auto abandon = [&](int st) {
+    PendingSnapshot& P = c->pending;
+    if (P.active) {
+      P.active = false;
+      P.tgt->cache[P.slot].state = kSlotWriting;
+      if (P.tgt2) P.tgt2->cache[P.slot2].state = kSlotWriting;
+      cudaEventRecord(c->snap_done, s);
+    }
+    return st;
+  };
   while (c->h2d_ev.size() < nb + 1) {
     cudaEvent_t e;
-    FFX_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess)
+      return abandon(fail(FFX_ECUDA, "snapshot_from_host: event creation failed"));
     c->h2d_ev.push_back(e);
   }
-  cudaStream_t s = as_stream(stream);
   // the copies overwrite the registered regions: after earlier work on `stream`
-  FFX_CUDA(cudaEventRecord(c->h2d_ev[nb], s));
-  FFX_CUDA(cudaStreamWaitEvent(c->h2d, c->h2d_ev[nb], 0));
+  if (cudaEventRecord(c->h2d_ev[nb], s) != cudaSuccess || cudaStreamWaitEvent(c->h2d, c->h2d_ev[nb], 0) != cudaSuccess)
+    return abandon(fail(FFX_ECUDA, "snapshot_from_host: cannot order the copy stream"));
   const uint8_t* src = static_cast<const uint8_t*>(host);
   uint64_t copied = 0;  // logical bytes already queued
   for (uint32_t b = 0; b < nb; ++b) {
     uint64_t lo = 0, hi = 0;
-    if (int st = ffx_snapshot_batch_span(c, b, &lo, &hi)) return st;
+    if (int st = ffx_snapshot_batch_span(c, b, &lo, &hi)) return abandon(st);
     hi = b + 1 == nb ? pm.logical : std::max(hi, copied);
     // queue [copied, hi): region by region (the payload is the regions concatenated)
     uint64_t at = 0;
@@ -751,14 +765,17 @@ extern "C" int ffx_snapshot_from_host(ffx_ctx* c, uint64_t iteration, const void
       const uint64_t rb = pm.regs[r]->bytes;
       if (copied < at + rb) {
         const uint64_t n = std::min(hi, at + rb) - copied;
-        FFX_CUDA(cudaMemcpyAsync(pm.regs[r]->dev + (copied - at), src + copied, n, cudaMemcpyHostToDevice, c->h2d));
+        const cudaError_t e =
+            cudaMemcpyAsync(pm.regs[r]->dev + (copied - at), src + copied, n, cudaMemcpyHostToDevice, c->h2d);
+        if (e != cudaSuccess) return abandon(cuda_fail(e, "snapshot_from_host: H2D"));
         copied += n;
       }
       at += rb;
     }
-    FFX_CUDA(cudaEventRecord(c->h2d_ev[b], c->h2d));
+    if (cudaEventRecord(c->h2d_ev[b], c->h2d) != cudaSuccess)
+      return abandon(fail(FFX_ECUDA, "snapshot_from_host: event record failed"));
     uint32_t left = 0;
-    if (int st = ffx_snapshot_next(c, stream, c->h2d_ev[b], &left)) return st;
+    if (int st = ffx_snapshot_next(c, stream, c->h2d_ev[b], &left)) return abandon(st);
   }
   return FFX_OK;
 }
